@@ -1,0 +1,544 @@
+"""Python face of the parity oracle.  TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+legs may import this module; the product package never does.
+
+Two back ends:
+  * ``C``   -- oracle/_build/libgspmm_oracle.so, the C restatement of the
+              reference algorithm (oracle/gspmm_oracle.c), always built;
+  * ``REF`` -- oracle/_ref/libgspmm_ref.so, the unmodified reference library
+              compiled from /root/reference/proj/src (None when absent).
+
+Ops the reference lacks (mean, argmax, max backward, multi-head, GCN weights,
+softmax attention, self-loops, symmetrisation) are composed here from the
+restated primitives exactly as SURVEY.md section 8(a) a17 specifies.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+# enum values of the reference (ops.hpp:28,33; br_config.hpp Operand)
+U, V, E, NONE = 0, 1, 2, 3
+ADD, SUB, MUL, DIV, DOT, COPY = 0, 1, 2, 3, 4, 5
+SUM, MAX, MIN, PROD, LAST = 0, 1, 2, 3, 4
+SRC_MAJOR, DST_MAJOR = 0, 1
+PUSH, PULL, BLOCKED, SPMM = 0, 1, 2, 3
+
+OK, CONFIG, SHAPE, STRUCTURE = 0, 1, 2, 3
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status, what=""):
+        super().__init__(f"oracle status {status} {what}")
+        self.status = status
+
+
+class Feat(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("rows", C.c_int64), ("dim", C.c_int64)]
+
+
+def _feat(a):
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    f = Feat(a.ctypes.data, a.shape[0], a.shape[1])
+    f._keep = a
+    return f
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+_u32p = C.POINTER(C.c_uint32)
+
+
+def _load_c():
+    path = os.path.join(_HERE, "_build", "libgspmm_oracle.so")
+    if not os.path.exists(path):
+        raise OSError(f"{path} missing: run `make -C oracle`")
+    lib = C.CDLL(path)
+    vp, i64, u32, u64, i32, dbl = C.c_void_p, C.c_int64, C.c_uint32, C.c_uint64, C.c_int, C.c_double
+    fp = C.POINTER(Feat)
+    sig = {
+        "or_splitmix64_at": (u64, [u64, u64]),
+        "or_u01_at": (dbl, [u64, u64]),
+        "or_unit_float_at": (C.c_float, [u64, u64]),
+        "or_normal_at": (C.c_float, [u64, u64]),
+        "or_gen_er": (i64, [u32, u64, dbl, u64, C.POINTER(_u32p), C.POINTER(_u32p)]),
+        "or_gen_rmat": (i64, [u32, u64, dbl, dbl, dbl, dbl, u64, C.POINTER(_u32p), C.POINTER(_u32p)]),
+        "or_gen_sbm": (i64, [u32, i32, dbl, dbl, u64, C.POINTER(_u32p), C.POINTER(_u32p)]),
+        "or_free": (None, [vp]),
+        "or_random_features": (None, [i64, i64, u64, vp]),
+        "or_normal_features": (None, [i64, u64, vp]),
+        "or_build_csr": (i32, [u32, i64, vp, vp, i32, vp, vp, vp]),
+        "or_transpose": (i32, [u32, u32, vp, vp, vp, vp, vp, vp]),
+        "or_validate": (i32, [u32, u32, i64, vp, i64, vp, vp]),
+        "or_out_shape": (i32, [i32, u32, u32, i64, i32, i32, i32, i32, i32, fp, fp, fp,
+                               C.POINTER(i64), C.POINTER(i64)]),
+        "or_binary_reduce": (i32, [i32, u32, u32, vp, vp, vp, i32, i32, i32, i32, i32, fp, fp, fp, vp]),
+        "or_oracle_aggregate": (i32, [u32, i64, vp, vp, i32, i32, i32, i32, i32, fp, fp, fp, vp]),
+        "or_mean": (i32, [i32, u32, u32, vp, vp, vp, i32, fp, vp]),
+        "or_copy_max_argmax": (i32, [u32, u32, vp, vp, vp, i32, fp, vp, vp, vp]),
+        "or_argmax_backward": (None, [i64, i64, vp, vp, i64, vp]),
+        "or_max_rel_error": (dbl, [i64, vp, vp]),
+        "or_bit_equal": (i32, [i64, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def _load_ref():
+    path = os.path.join(_HERE, "_ref", "libgspmm_ref.so")
+    if not os.path.exists(path):
+        return None
+    lib = C.CDLL(path)
+    vp, i64, u32, u64, i32, dbl = C.c_void_p, C.c_int64, C.c_uint32, C.c_uint64, C.c_int, C.c_double
+    fp = C.POINTER(Feat)
+    sig = {
+        "ref_free": (None, [vp]),
+        "ref_generate": (i64, [i32, u32, u64, dbl, i32, dbl, dbl, dbl, dbl, dbl, dbl, u64,
+                               C.POINTER(_u32p), C.POINTER(_u32p)]),
+        "ref_random_features": (None, [i64, i64, u64, vp]),
+        "ref_build_csr": (i32, [u32, i64, vp, vp, i32, vp, vp, vp]),
+        "ref_transpose": (i32, [i32, u32, u32, vp, vp, vp, vp, vp, vp]),
+        "ref_binary_reduce": (i32, [i32, i32, u32, u32, vp, vp, vp, i32, i32, i32, i32, i32,
+                                    fp, fp, fp, i32, vp, C.POINTER(i64), C.POINTER(i64)]),
+        "ref_oracle_aggregate": (i32, [u32, i64, vp, vp, i32, i32, i32, i32, i32, fp, fp, fp, vp,
+                                       C.POINTER(i64), C.POINTER(i64)]),
+        "ref_views_create": (vp, [u32, i64, vp, vp]),
+        "ref_views_free": (None, [vp]),
+        "ref_views_csr": (i32, [vp, i32, vp, vp, vp]),
+        "ref_feat_create": (vp, [i64, i64, vp]),
+        "ref_feat_free": (None, [vp]),
+        "ref_run": (dbl, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, i32, vp]),
+        "ref_bench_case": (dbl, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, i32, i32, i32,
+                                 C.POINTER(dbl), C.POINTER(dbl)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+LIB = _load_c()
+REF = _load_ref()
+
+
+def _check(st, what=""):
+    if st != 0:
+        raise OracleError(st, what)
+
+
+# ------------------------------------------------------------------- rng
+def splitmix64_at(seed, counter):
+    return LIB.or_splitmix64_at(seed, counter)
+
+
+def random_features(rows, dim, seed):
+    """generate.cpp:256-266, U[-1,1)."""
+    out = np.empty((rows, dim), np.float32)
+    LIB.or_random_features(rows, dim, seed, out.ctypes.data)
+    return out
+
+
+def normal_features(rows, dim, seed):
+    """Builder-defined N(0,1), Box-Muller."""
+    out = np.empty((rows, dim), np.float32)
+    LIB.or_normal_features(rows * dim, seed, out.ctypes.data)
+    return out
+
+
+# ------------------------------------------------------------ generators
+def _take_edges(m, ps, pd, free):
+    if m < 0:
+        raise OracleError(-m, "generator")
+    src = np.ctypeslib.as_array(ps, shape=(max(m, 1),))[:m].copy()
+    dst = np.ctypeslib.as_array(pd, shape=(max(m, 1),))[:m].copy()
+    free(C.cast(ps, C.c_void_p))
+    free(C.cast(pd, C.c_void_p))
+    return src, dst
+
+
+def gen_er(n, num_edges=0, prob=-1.0, seed=0):
+    ps, pd = _u32p(), _u32p()
+    m = LIB.or_gen_er(n, num_edges, prob, seed, C.byref(ps), C.byref(pd))
+    return _take_edges(m, ps, pd, LIB.or_free)
+
+
+def gen_rmat(n, num_edges, a=0.57, b=0.19, c=0.19, d=0.05, seed=0):
+    ps, pd = _u32p(), _u32p()
+    m = LIB.or_gen_rmat(n, num_edges, a, b, c, d, seed, C.byref(ps), C.byref(pd))
+    return _take_edges(m, ps, pd, LIB.or_free)
+
+
+def gen_sbm(n, blocks, p_in, p_out, seed=0):
+    ps, pd = _u32p(), _u32p()
+    m = LIB.or_gen_sbm(n, blocks, p_in, p_out, seed, C.byref(ps), C.byref(pd))
+    return _take_edges(m, ps, pd, LIB.or_free)
+
+
+def random_small_graph(seed):
+    """test_util.hpp:30-61: n <= 200, m <= 2000, kind picked by seed."""
+    pick = splitmix64_at(seed, 9000)
+    n = 8 + splitmix64_at(seed, 9001) % 193
+    degree = 1.0 + float(splitmix64_at(seed, 9002) % 10)
+    kind = pick % 3
+    if kind == 0:
+        src, dst = gen_er(n, 0, min(1.0, degree / (n - 1.0)), seed)
+    elif kind == 1:
+        m = min(2000, int(degree * n))
+        src, dst = gen_rmat(n, m, 0.40, 0.25, 0.25, 0.10, seed)
+    else:
+        blocks = 1 + int(splitmix64_at(seed, 9004) % 4)
+        p_in = min(1.0, degree * blocks / float(n))
+        src, dst = gen_sbm(n, blocks, p_in, p_in / 20.0, seed)
+    return int(n), src, dst
+
+
+# ------------------------------------------------------------ graph core
+def build_csr(n, src, dst, orientation=DST_MAJOR):
+    src = np.ascontiguousarray(src, np.uint32)
+    dst = np.ascontiguousarray(dst, np.uint32)
+    m = len(src)
+    indptr = np.empty(n + 1, np.uint32)
+    indices = np.empty(max(m, 1), np.uint32)
+    eids = np.empty(max(m, 1), np.uint32)
+    _check(LIB.or_build_csr(n, m, _ptr(src), _ptr(dst), orientation, _ptr(indptr),
+                            _ptr(indices), _ptr(eids)), "build_csr")
+    return indptr, indices[:m], eids[:m]
+
+
+def transpose(num_rows, num_cols, indptr, indices, eids):
+    m = int(indptr[-1])
+    t_indptr = np.empty(num_cols + 1, np.uint32)
+    t_indices = np.empty(max(m, 1), np.uint32)
+    t_eids = np.empty(max(m, 1), np.uint32)
+    indices = np.ascontiguousarray(indices, np.uint32)
+    eids = np.ascontiguousarray(eids, np.uint32)
+    LIB.or_transpose(num_rows, num_cols, _ptr(np.ascontiguousarray(indptr, np.uint32)),
+                     _ptr(indices), _ptr(eids), _ptr(t_indptr), _ptr(t_indices), _ptr(t_eids))
+    return t_indptr, t_indices[:m], t_eids[:m]
+
+
+def validate(num_rows, num_cols, indptr, indices, eids):
+    indptr = np.ascontiguousarray(indptr, np.uint32)
+    indices = np.ascontiguousarray(indices, np.uint32)
+    eids = np.ascontiguousarray(eids, np.uint32)
+    if len(indptr) != num_rows + 1:
+        return 1
+    if len(indices) != len(eids):
+        return 4
+    return LIB.or_validate(num_rows, num_cols, len(indptr), _ptr(indptr), len(indices),
+                           _ptr(indices), _ptr(eids))
+
+
+class Graph:
+    """Both orientations of one edge list (make_views, bench.cpp:48-53)."""
+
+    def __init__(self, n, src, dst):
+        self.n = int(n)
+        self.src = np.ascontiguousarray(src, np.uint32)
+        self.dst = np.ascontiguousarray(dst, np.uint32)
+        self.m = len(self.src)
+        self.dst_major = build_csr(self.n, self.src, self.dst, DST_MAJOR)
+        self.src_major = transpose(self.n, self.n, *self.dst_major)
+
+    def csr(self, orientation):
+        return self.dst_major if orientation == DST_MAJOR else self.src_major
+
+
+# ---------------------------------------------------------- config names
+_OPS = {"u": U, "v": V, "e": E}
+_BIN = {"add": ADD, "sub": SUB, "mul": MUL, "div": DIV, "dot": DOT}
+_RED = {"add": SUM, "max": MAX, "min": MIN, "mul": PROD, "copy": LAST}
+
+
+def named_config(name):
+    """named_config, br_config.cpp:96-131 -> (lhs, rhs, binop, reduce, out)."""
+    t = name.split("_")
+    if len(t) == 4:
+        if t[0] not in ("u", "e") or t[1] != "copy" or t[2] not in _RED or t[3] != "v":
+            raise OracleError(CONFIG, name)
+        return (_OPS[t[0]], NONE, COPY, _RED[t[2]], V)
+    if len(t) == 5:
+        if t[0] not in _OPS or t[1] not in _BIN or t[2] not in _OPS or t[3] not in _RED \
+                or t[4] not in _OPS:
+            raise OracleError(CONFIG, name)
+        cfg = (_OPS[t[0]], _OPS[t[2]], _BIN[t[1]], _RED[t[3]], _OPS[t[4]])
+        if cfg[4] == E:
+            cfg = cfg[:3] + (LAST, E)
+        if cfg[0] == cfg[1]:
+            raise OracleError(CONFIG, name)
+        return cfg
+    raise OracleError(CONFIG, name)
+
+
+APPLICATION_CONFIGS = [  # br_config.cpp:148-161
+    "u_copy_add_v", "u_dot_v_add_e", "u_mul_e_add_v", "e_copy_add_v", "e_copy_max_v",
+    "u_add_v_copy_e", "e_sub_v_copy_e", "e_div_v_copy_e", "v_mul_e_copy_e",
+]
+
+
+# ----------------------------------------------------------- aggregation
+def out_shape(orientation, num_rows, num_cols, m, cfg, u=None, v=None, e=None):
+    fu, fv, fe = _feat(u), _feat(v), _feat(e)
+    r, d = C.c_int64(), C.c_int64()
+    st = LIB.or_out_shape(orientation, num_rows, num_cols, m, *cfg, fu, fv, fe,
+                          C.byref(r), C.byref(d))
+    _check(st, "out_shape")
+    return r.value, d.value
+
+
+def binary_reduce(g, cfg, u=None, v=None, e=None, orientation=None):
+    """binary_reduce(RowParallelSpmm, g.oriented(required), cfg, u, v, e)."""
+    if orientation is None:
+        orientation = SRC_MAJOR if cfg[4] == U else DST_MAJOR
+    indptr, indices, eids = g.csr(orientation)
+    fu, fv, fe = _feat(u), _feat(v), _feat(e)
+    r, d = C.c_int64(), C.c_int64()
+    _check(LIB.or_out_shape(orientation, g.n, g.n, g.m, *cfg, fu, fv, fe, C.byref(r),
+                            C.byref(d)), "binary_reduce")
+    out = np.empty((r.value, d.value), np.float32)
+    _check(LIB.or_binary_reduce(orientation, g.n, g.n, _ptr(indptr), _ptr(indices), _ptr(eids),
+                                *cfg, fu, fv, fe, out.ctypes.data), "binary_reduce")
+    return out
+
+
+def oracle_aggregate(g, cfg, u=None, v=None, e=None):
+    fu, fv, fe = _feat(u), _feat(v), _feat(e)
+    orientation = SRC_MAJOR if cfg[4] == U else DST_MAJOR
+    r, d = C.c_int64(), C.c_int64()
+    _check(LIB.or_out_shape(orientation, g.n, g.n, g.m, *cfg, fu, fv, fe, C.byref(r),
+                            C.byref(d)), "oracle_aggregate")
+    out = np.empty((r.value, d.value), np.float32)
+    _check(LIB.or_oracle_aggregate(g.n, g.m, _ptr(g.src), _ptr(g.dst), *cfg, fu, fv, fe,
+                                   out.ctypes.data), "oracle_aggregate")
+    return out
+
+
+def mean(g, src_feats, lhs=U, orientation=DST_MAJOR):
+    """a17.1: copy-sum / (float)in-degree, 0 for empty rows."""
+    indptr, indices, eids = g.csr(orientation)
+    f = _feat(src_feats)
+    out = np.empty((g.n, f.dim), np.float32)
+    _check(LIB.or_mean(orientation, g.n, g.n, _ptr(indptr), _ptr(indices), _ptr(eids), lhs,
+                       f, out.ctypes.data), "mean")
+    return out
+
+
+def copy_max_argmax(g, src_feats, lhs=U):
+    """a17.2: max value (== binary_reduce u_copy_max_v) + first-position argmax."""
+    indptr, indices, eids = g.dst_major
+    f = _feat(src_feats)
+    out = np.empty((g.n, f.dim), np.float32)
+    arg_u = np.empty((g.n, f.dim), np.int32)
+    arg_e = np.empty((g.n, f.dim), np.int32)
+    _check(LIB.or_copy_max_argmax(g.n, g.n, _ptr(indptr), _ptr(indices), _ptr(eids), lhs, f,
+                                  out.ctypes.data, arg_u.ctypes.data, arg_e.ctypes.data))
+    return out, arg_u, arg_e
+
+
+def argmax_backward(arg, grad_out, src_rows):
+    """a17.4: scatter grad_out through the argmax, f64 accumulation."""
+    arg = np.ascontiguousarray(arg, np.int32)
+    grad_out = np.ascontiguousarray(grad_out, np.float32)
+    out = np.empty((src_rows, arg.shape[1]), np.float32)
+    LIB.or_argmax_backward(arg.shape[0], arg.shape[1], arg.ctypes.data, grad_out.ctypes.data,
+                           src_rows, out.ctypes.data)
+    return out
+
+
+def sum_backward(g, grad_out, e=None):
+    """a17.3 grad_u of copy_u/u_mul_e + sum: binary_reduce on the src-major
+    graph with v_mul_e_add_u (or {V, None, Copy, Sum, U} without e)."""
+    if e is None:
+        return binary_reduce(g, (V, NONE, COPY, SUM, U), v=grad_out)
+    return binary_reduce(g, (V, E, MUL, SUM, U), v=grad_out, e=e)
+
+
+def edge_grad(g, x, grad_out):
+    """a17.3 grad_e: binary_reduce(dst_major, u_dot_v_copy_e, u=x, v=grad_out)."""
+    return binary_reduce(g, (U, V, DOT, LAST, E), u=x, v=grad_out)
+
+
+def in_degree(g):
+    return np.diff(g.dst_major[0].astype(np.int64))
+
+
+def mean_backward(g, grad_out):
+    """a17.3 for mean: v_mul_e_add_u with e = 1/(float)deg_in(dst(e))."""
+    deg = in_degree(g)
+    inv = np.zeros(g.n, np.float32)
+    nz = deg > 0
+    inv[nz] = np.float32(1.0) / deg[nz].astype(np.float32)
+    e = inv[g.dst].reshape(-1, 1)
+    return binary_reduce(g, (V, E, MUL, SUM, U), v=grad_out, e=e)
+
+
+def multihead_u_mul_e_sum(g, x, a, heads):
+    """a17.5: per head h, binary_reduce(u_mul_e_add_v) on the contiguous
+    head slice x[:, h*D:(h+1)*D] with scalar edge weight a[:, h]."""
+    n, width = x.shape
+    d = width // heads
+    out = np.empty((g.n, width), np.float32)
+    for h in range(heads):
+        xh = np.ascontiguousarray(x[:, h * d:(h + 1) * d])
+        ah = np.ascontiguousarray(a[:, h:h + 1])
+        out[:, h * d:(h + 1) * d] = binary_reduce(g, (U, E, MUL, SUM, V), u=xh, e=ah)
+    return out
+
+
+def multihead_backward(g, x, a, grad_out, heads):
+    """a17.5 backward: grad_x per head on the src-major graph, grad_a per head
+    as u_dot_v_copy_e of the head slices."""
+    n, width = x.shape
+    d = width // heads
+    grad_x = np.empty_like(x)
+    grad_a = np.empty((g.m, heads), np.float32)
+    for h in range(heads):
+        gh = np.ascontiguousarray(grad_out[:, h * d:(h + 1) * d])
+        ah = np.ascontiguousarray(a[:, h:h + 1])
+        xh = np.ascontiguousarray(x[:, h * d:(h + 1) * d])
+        grad_x[:, h * d:(h + 1) * d] = binary_reduce(g, (V, E, MUL, SUM, U), v=gh, e=ah)
+        grad_a[:, h] = binary_reduce(g, (U, V, DOT, LAST, E), u=xh, v=gh)[:, 0]
+    return grad_x, grad_a
+
+
+# ------------------------------------------------- input synthesis pieces
+def add_self_loops(n, src, dst):
+    """cfg2: append (i, i) for every node after the generated edges."""
+    loop = np.arange(n, dtype=np.uint32)
+    return np.concatenate([src, loop]), np.concatenate([dst, loop])
+
+
+def symmetrize(src, dst):
+    """cfg3: append the reverse of every edge (edge m+i = reverse of edge i)."""
+    return np.concatenate([src, dst]), np.concatenate([dst, src])
+
+
+def gcn_weights(n, src, dst):
+    """cfg2: w_e = 1/sqrt(deg_out(u) * deg_in(v)), f64 then rounded, edge-id order."""
+    dout = np.bincount(src, minlength=n).astype(np.float64)
+    din = np.bincount(dst, minlength=n).astype(np.float64)
+    w = 1.0 / np.sqrt(dout[src] * din[dst])
+    return w.astype(np.float32).reshape(-1, 1)
+
+
+def softmax_attention(n, dst, logits):
+    """cfg4: a[e,h] = softmax over the in-edges of dst(e) of logits[:, h],
+    computed in f64 and rounded to fp32."""
+    lg = logits.astype(np.float64)
+    m, heads = lg.shape
+    mx = np.full((n, heads), -np.inf)
+    np.maximum.at(mx, dst, lg)
+    ex = np.exp(lg - mx[dst])
+    den = np.zeros((n, heads))
+    np.add.at(den, dst, ex)
+    return (ex / den[dst]).astype(np.float32)
+
+
+# ----------------------------------------------------------- comparisons
+def max_rel_error(got, want):
+    got = np.ascontiguousarray(got, np.float32)
+    want = np.ascontiguousarray(want, np.float32)
+    if got.shape != want.shape:
+        return float("inf")
+    return LIB.or_max_rel_error(got.size, got.ctypes.data, want.ctypes.data)
+
+
+def bit_equal(a, b):
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    if a.shape != b.shape:
+        return False
+    return bool(LIB.or_bit_equal(a.size, a.ctypes.data, b.ctypes.data))
+
+
+def is_exact_reduce(reduce):
+    """compare.hpp:58-61."""
+    return reduce in (MAX, MIN, LAST)
+
+
+# ------------------------------------------------ the reference library
+def ref_available():
+    return REF is not None
+
+
+def ref_generate(kind, n, num_edges=0, prob=-1.0, blocks=2, p_in=0.0, p_out=0.0,
+                 a=0.57, b=0.19, c=0.19, d=0.05, seed=0):
+    ps, pd = _u32p(), _u32p()
+    m = REF.ref_generate(kind, n, num_edges, prob, blocks, p_in, p_out, a, b, c, d, seed,
+                         C.byref(ps), C.byref(pd))
+    return _take_edges(m, ps, pd, REF.ref_free)
+
+
+def ref_random_features(rows, dim, seed):
+    out = np.empty((rows, dim), np.float32)
+    REF.ref_random_features(rows, dim, seed, out.ctypes.data)
+    return out
+
+
+def ref_build_csr(n, src, dst, orientation=DST_MAJOR):
+    src = np.ascontiguousarray(src, np.uint32)
+    dst = np.ascontiguousarray(dst, np.uint32)
+    m = len(src)
+    indptr = np.empty(n + 1, np.uint32)
+    indices = np.empty(max(m, 1), np.uint32)
+    eids = np.empty(max(m, 1), np.uint32)
+    _check(REF.ref_build_csr(n, m, _ptr(src), _ptr(dst), orientation, _ptr(indptr),
+                             _ptr(indices), _ptr(eids)), "ref_build_csr")
+    return indptr, indices[:m], eids[:m]
+
+
+def ref_transpose(orientation, num_rows, num_cols, indptr, indices, eids):
+    m = int(indptr[-1])
+    t_indptr = np.empty(num_cols + 1, np.uint32)
+    t_indices = np.empty(max(m, 1), np.uint32)
+    t_eids = np.empty(max(m, 1), np.uint32)
+    _check(REF.ref_transpose(orientation, num_rows, num_cols,
+                             _ptr(np.ascontiguousarray(indptr, np.uint32)),
+                             _ptr(np.ascontiguousarray(indices, np.uint32)),
+                             _ptr(np.ascontiguousarray(eids, np.uint32)),
+                             _ptr(t_indptr), _ptr(t_indices), _ptr(t_eids)))
+    return t_indptr, t_indices[:m], t_eids[:m]
+
+
+def ref_binary_reduce(g, cfg, u=None, v=None, e=None, strategy=SPMM, threads=0):
+    orientation = SRC_MAJOR if cfg[4] == U else DST_MAJOR
+    if strategy == PUSH:
+        orientation = 1 - orientation
+    indptr, indices, eids = g.csr(orientation)
+    fu, fv, fe = _feat(u), _feat(v), _feat(e)
+    r, d = C.c_int64(), C.c_int64()
+    st = REF.ref_binary_reduce(strategy, orientation, g.n, g.n, _ptr(indptr), _ptr(indices),
+                               _ptr(eids), *cfg, fu, fv, fe, threads, None, C.byref(r),
+                               C.byref(d))
+    _check(st, "ref_binary_reduce")
+    out = np.empty((r.value, d.value), np.float32)
+    _check(REF.ref_binary_reduce(strategy, orientation, g.n, g.n, _ptr(indptr), _ptr(indices),
+                                 _ptr(eids), *cfg, fu, fv, fe, threads, out.ctypes.data,
+                                 C.byref(r), C.byref(d)), "ref_binary_reduce")
+    return out
+
+
+def ref_oracle_aggregate(g, cfg, u=None, v=None, e=None):
+    fu, fv, fe = _feat(u), _feat(v), _feat(e)
+    r, d = C.c_int64(), C.c_int64()
+    _check(REF.ref_oracle_aggregate(g.n, g.m, _ptr(g.src), _ptr(g.dst), *cfg, fu, fv, fe, None,
+                                    C.byref(r), C.byref(d)), "ref_oracle_aggregate")
+    out = np.empty((r.value, d.value), np.float32)
+    _check(REF.ref_oracle_aggregate(g.n, g.m, _ptr(g.src), _ptr(g.dst), *cfg, fu, fv, fe,
+                                    out.ctypes.data, C.byref(r), C.byref(d)))
+    return out
