@@ -1,0 +1,473 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 aggregation hot path (BASELINE.json configs[1]).
+
+Workload ("cfg2", BASELINE.json configs[1]): GCN-normalised SpMM, u_mul_e +
+sum, forward AND backward, on an R-MAT graph (a,b,c,d = .57,.19,.19,.05,
+seed 0) with 1M nodes and 16M edges plus one self-loop per node (E = 17M);
+node features fp32 [1M x 256] ~ N(0,1) (seed 1); scalar edge weight
+w = 1/sqrt(deg_out(u) deg_in(v)); output gradient fp32 ~ N(0,1) (seed 3).
+
+One step = forward  out    = u_mul_e_add_v(x, w)        on the dst-major CSR
+         + backward grad_x = v_mul_e_add_u(grad_out, w) on the src-major CSR
+(the grad of x; w is a constant of the graph in GCN).  Metric: aggregated
+edges per second = 2E / step time (each edge is aggregated once forward and
+once backward), plus effective HBM GB/s of the dominant kernel against the
+measured copy bandwidth in MEASURED_PEAKS.json.
+
+  value  -- device-resident inputs, CUDA-event timed (max over ranks);
+  e2e    -- the same step through the C-ABI host entry
+            (gspmm_binary_reduce_host) from pinned host buffers, H2D of
+            x/w/grad_out and D2H of out/grad_x inside the timed region;
+  cpu_baseline -- the UNMODIFIED reference library (oracle/_ref, compiled from
+            /root/reference/proj/src) on the host cores, same inputs.
+
+The inputs (1 GB per feature matrix) exceed the 126 MB L2, so no flush is
+needed between steps.  N>1 (torchrun): owner rows of each orientation are
+split into edge-balanced contiguous ranges, one per rank; features are
+replicated; no collective on the data path (strong scaling: fixed total work).
+
+--impl reference times the reference library alone (rank 0; other ranks exit).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_NODES = 1_000_000
+N_RMAT = 16_000_000
+FEAT = 256
+SEEDS = {"graph": 0, "x": 1, "grad": 3}
+WORKLOAD = ("cfg2: GCN u_mul_e+sum fwd+bwd, R-MAT(.57,.19,.19,.05) 1M nodes, "
+            "16M edges + 1M self-loops, x fp32 [1M x 256] N(0,1), w=1/sqrt(dout*din)")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ inputs
+def make_inputs(threads=0):
+    """cfg2 inputs through the product's host synthesis (bit-identical to the
+    reference generators; pinned by tests/test_abi.py)."""
+    import paper_2007_06354_b200 as P
+    t0 = time.time()
+    src, dst = P.synth_rmat(N_NODES, N_RMAT, 0.57, 0.19, 0.19, 0.05, SEEDS["graph"], threads)
+    loops = np.arange(N_NODES, dtype=np.uint32)
+    src = np.concatenate([src, loops])
+    dst = np.concatenate([dst, loops])
+    w = P.synth_gcn_weights(N_NODES, src, dst, threads)
+    dcsr = P.build_csr(N_NODES, src, dst, P.DST_MAJOR, threads)
+    scsr = P.transpose(N_NODES, N_NODES, *dcsr, threads=threads)
+    log(f"[bench] graph: {len(src)} edges in {time.time() - t0:.1f}s")
+    return src, dst, w, dcsr, scsr
+
+
+def make_features(pinned):
+    import paper_2007_06354_b200 as P
+    import torch
+    t0 = time.time()
+    out = []
+    for seed in (SEEDS["x"], SEEDS["grad"]):
+        t = torch.empty((N_NODES, FEAT), dtype=torch.float32, pin_memory=pinned)
+        P.synth_normal(N_NODES, FEAT, seed, out=t.numpy())
+        out.append(t)
+    log(f"[bench] features in {time.time() - t0:.1f}s")
+    return out
+
+
+def alg_bytes(rows, edges, feat):
+    """Algorithmic bytes of one u_mul_e+sum pass: features
+    gathered once per edge + CSR (indptr + indices) + scalar edge operand +
+    output rows."""
+    return edges * feat * 4 + (rows + 1) * 4 + edges * 4 + edges * 4 + rows * feat * 4
+
+
+# ----------------------------------------------------------- reference CPU
+def reference_step_runner(src, dst, x_np, w_np, gy_np, threads):
+    """The unmodified reference (oracle/_ref) on the same inputs: returns a
+    callable that runs one fwd+bwd step and reports its seconds (the
+    reference's own steady_clock around each binary_reduce)."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        return None, "oracle/_ref/libgspmm_ref.so not built"
+    R = O.REF
+    t0 = time.time()
+    views = R.ref_views_create(N_NODES, len(src), src.ctypes.data, dst.ctypes.data)
+    fx = R.ref_feat_create(x_np.shape[0], x_np.shape[1], x_np.ctypes.data)
+    fg = R.ref_feat_create(gy_np.shape[0], gy_np.shape[1], gy_np.ctypes.data)
+    fw = R.ref_feat_create(w_np.shape[0], 1, w_np.ctypes.data)
+    log(f"[bench] reference views/features in {time.time() - t0:.1f}s")
+
+    def step():
+        # u_mul_e_add_v forward, v_mul_e_add_u backward (RowParallelSpmm,
+        # the reference's fastest strategy and its parity comparator)
+        t_f = R.ref_run(views, O.SPMM, O.U, O.E, O.MUL, O.SUM, O.V, fx, None, fw, threads, None)
+        t_b = R.ref_run(views, O.SPMM, O.V, O.E, O.MUL, O.SUM, O.U, None, fg, fw, threads, None)
+        if t_f < 0 or t_b < 0:
+            raise RuntimeError("reference binary_reduce failed")
+        return t_f + t_b
+
+    def close():
+        for f in (fx, fg, fw):
+            R.ref_feat_free(f)
+        R.ref_views_free(views)
+
+    step.close = close
+    return step, None
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
+# --------------------------------------------------------------- our arm
+def run_ours(args, rank, world, dist):
+    import torch
+    import paper_2007_06354_b200 as P
+    from paper_2007_06354_b200.shard import balanced_row_ranges, slice_csr
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    src, dst, w, dcsr, scsr = make_inputs()
+    E = len(src)
+    x_h, gy_h = make_features(pinned=True)
+
+    # shard owner rows (edge-balanced) of both orientations
+    db = balanced_row_ranges(dcsr[0], world)
+    sb = balanced_row_ranges(scsr[0], world)
+    d_lo, d_hi = int(db[rank]), int(db[rank + 1])
+    s_lo, s_hi = int(sb[rank]), int(sb[rank + 1])
+    dsl = slice_csr(*dcsr, d_lo, d_hi)
+    ssl = slice_csr(*scsr, s_lo, s_hi)
+    t0 = time.time()
+    gd = P.Graph(*dsl, num_rows=d_hi - d_lo, num_cols=N_NODES, orientation=P.DST_MAJOR, device=dev)
+    gs = P.Graph(*ssl, num_rows=s_hi - s_lo, num_cols=N_NODES, orientation=P.SRC_MAJOR, device=dev)
+    log(f"[bench] rank {rank}: dst rows [{d_lo},{d_hi}) {gd.num_edges} edges, "
+        f"src rows [{s_lo},{s_hi}) {gs.num_edges} edges; upload {time.time() - t0:.1f}s; "
+        f"long rows {gd.num_long_rows}/{gs.num_long_rows}")
+
+    x = x_h.cuda(dev)
+    gy = gy_h.cuda(dev)
+    w_d = torch.from_numpy(w).cuda(dev)
+    # device plan: edge weights permuted into each handle's CSR order (untimed,
+    # the analogue of the reference's BlockPlan build outside bench timing)
+    w_fwd = gd.permute_edges(w_d)
+    w_bwd = gs.permute_edges(w_d)
+    out = torch.empty((d_hi - d_lo, FEAT), dtype=torch.float32, device=dev)
+    gx = torch.empty((s_hi - s_lo, FEAT), dtype=torch.float32, device=dev)
+    cfg_f = P.named_config("u_mul_e_add_v")
+    cfg_b = P.named_config("v_mul_e_add_u")
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        P.binary_reduce(gd, cfg_f, u=x, e=w_fwd, out=out, e_order=P.EDGE_BY_POS, stream=stream)
+        if ev:
+            ev[1].record(stream)
+        P.binary_reduce(gs, cfg_b, v=gy, e=w_bwd, out=gx, e_order=P.EDGE_BY_POS, stream=stream)
+        if ev:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    launches0 = P.launch_count()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        stop.record(stream)
+        torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    launches = P.launch_count() - launches0
+    ms = start.elapsed_time(stop)
+    fwd_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    bwd_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # --- e2e: the reference-facing host call, pinned host buffers -----------
+    e2e = None
+    if not args.skip_e2e:
+        out_h = torch.empty((d_hi - d_lo, FEAT), dtype=torch.float32, pin_memory=True)
+        gx_h = torch.empty((s_hi - s_lo, FEAT), dtype=torch.float32, pin_memory=True)
+        w_pin = torch.from_numpy(w).pin_memory()
+        xn, gyn, wn = x_h.numpy(), gy_h.numpy(), w_pin.numpy()
+
+        def e2e_step():
+            P.binary_reduce_host(gd, cfg_f, u=xn, e=wn, out=out_h.numpy(),
+                                 stream=stream.cuda_stream)
+            P.binary_reduce_host(gs, cfg_b, v=gyn, e=wn, out=gx_h.numpy(),
+                                 stream=stream.cuda_stream)
+        for _ in range(max(1, min(args.warmup, 2))):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        n_e2e = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        e2e_s = (time.perf_counter() - t0) / n_e2e
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        h2d = (x_h.numel() + gy_h.numel() + 2 * w.size) * 4
+        d2h = (out_h.numel() + gx_h.numel()) * 4
+        e2e = {"value": 2 * E / e2e_s, "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
+               "path": "gspmm_binary_reduce_host (C-ABI host entry), pinned host buffers"}
+
+    # --- CPU baseline (rank 0, N=1): the reference library, bounded sample ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        threads = os.cpu_count() or 1
+        runner, why = reference_step_runner(src, dst, x_h.numpy(), w, gy_h.numpy(), threads)
+        if runner is None:
+            cpu = {"value": None, "unit": "edges/s", "unavailable": why}
+        else:
+            runner()  # warm
+            times = []
+            t_begin = time.time()
+            while len(times) < 3 and (time.time() - t_begin) < 30:
+                times.append(runner())
+            runner.close()
+            mean_s = sum(times) / len(times)
+            model, cores = cpu_info()
+            cpu = {"value": 2 * E / mean_s, "unit": "edges/s", "cores": threads,
+                   "kind": "reference",
+                   "sample": f"full cfg2 fwd+bwd step ({len(times)} timed after 1 warm-up; "
+                             f"binary_reduce RowParallelSpmm, {threads} OpenMP threads, "
+                             f"{model})",
+                   "s_per_step": mean_s}
+
+    # --- roofline of the dominant kernel --------------------------------------
+    peak, peak_src = peaks()
+    f_avg = sum(fwd_ms) / len(fwd_ms)
+    b_avg = sum(bwd_ms) / len(bwd_ms)
+    fwd_bytes = alg_bytes(d_hi - d_lo, gd.num_edges, FEAT)
+    bwd_bytes = alg_bytes(s_hi - s_lo, gs.num_edges, FEAT)
+    dominant = ("fwd", f_avg, fwd_bytes) if f_avg >= b_avg else ("bwd", b_avg, bwd_bytes)
+    achieved = dominant[2] / (dominant[1] * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(dominant[0])
+        except Exception:
+            traffic = None
+    result = {
+        "metric": "aggregated edges/s (cfg2 GCN u_mul_e+sum, fwd+bwd)",
+        "value": 2 * E / (ms_max / args.steps * 1e-3),
+        "unit": "edges/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (R-MAT graph and N(0,1) features generated in-process, seeded)",
+        "config": {"workload": WORKLOAD, "edges": E, "nodes": N_NODES, "feat": FEAT,
+                   "parallelism": f"dst/src-row shards x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs (1 GB feature matrices) larger than the 126 MB L2; no flush",
+                   "edge_operand": "weights permuted once to CSR order (device plan, untimed)"},
+        "roofline": {"bound": "hbm", "kernel": f"k_rows<4,MUL,SUM> ({dominant[0]})",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "alg_bytes_per_launch": dominant[2],
+                     "avg_launch_ms": dominant[1], "peak_source": peak_src},
+        "kernels_ms": {"fwd": f_avg, "bwd": b_avg,
+                       "fwd_gbs": fwd_bytes / (f_avg * 1e-3) / 1e9,
+                       "bwd_gbs": bwd_bytes / (b_avg * 1e-3) / 1e9},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "impl": "b200",
+    }
+    return result
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the unmodified reference library on the host cores."""
+    if rank != 0:
+        return None
+    from oracle import oracle as O
+    if not O.ref_available():
+        return {"impl": "reference", "unavailable": "oracle/_ref/libgspmm_ref.so not built"}
+    threads = os.cpu_count() or 1
+    t0 = time.time()
+    # the reference's own generator for the graph (generate.cpp RMat)
+    src, dst = O.ref_generate(1, N_NODES, N_RMAT, a=0.57, b=0.19, c=0.19, d=0.05,
+                              seed=SEEDS["graph"])
+    src, dst = O.add_self_loops(N_NODES, src, dst)
+    w = O.gcn_weights(N_NODES, src, dst)
+    x = O.normal_features(N_NODES, FEAT, SEEDS["x"], threads=threads)
+    gy = O.normal_features(N_NODES, FEAT, SEEDS["grad"], threads=threads)
+    log(f"[bench-ref] inputs in {time.time() - t0:.1f}s")
+    runner, why = reference_step_runner(src, dst, x, w, gy, threads)
+    if runner is None:
+        return {"impl": "reference", "unavailable": why}
+    for _ in range(args.warmup):
+        runner()
+    times = [runner() for _ in range(args.steps)]
+    runner.close()
+    mean_s = sum(times) / len(times)
+    E = len(src)
+    model, _ = cpu_info()
+    value = 2 * E / mean_s
+    return {
+        "metric": "aggregated edges/s (cfg2 GCN u_mul_e+sum, fwd+bwd)",
+        "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (R-MAT graph and N(0,1) features generated in-process, seeded)",
+        "config": {"workload": WORKLOAD, "edges": E, "nodes": N_NODES, "feat": FEAT,
+                   "parallelism": f"{threads} OpenMP threads"},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"full cfg2 fwd+bwd step x{args.steps} (RowParallelSpmm, "
+                                   f"{threads} threads, {model})"},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg")
+    ap.add_argument("--skip-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        log("[bench] warmup raised to 3 (timing rule)")
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as tdist
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+            tdist.init_process_group("nccl")
+            dist = tdist
+        res = run_ours(args, rank, world, dist)
+        if dist:
+            dist.destroy_process_group()
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,231 @@
+/*
+ * gspmm_b200.h -- C-ABI of the B200-native Copy-Reduce / Binary-Reduce path.
+ *
+ * Drop-in boundary for the reference's hot path (arXiv 2007.06354's
+ * aggregation primitives, re-implemented by /root/reference/proj as
+ * gspmm::binary_reduce / gspmm::copy_reduce):
+ *
+ *   reference (proj/include/gspmm/kernels.hpp)        this ABI
+ *   -----------------------------------------------   -------------------------
+ *   FeatureMatrix binary_reduce(Strategy, const        gspmm_binary_reduce /
+ *     CsrGraph&, const BrConfig&, const FeatureMatrix*  gspmm_binary_reduce_host
+ *     u, v, e, const BlockPlan*, int threads)           (kernels.hpp:60-64)
+ *   FeatureMatrix copy_reduce(Strategy, const         gspmm_copy_reduce
+ *     CsrGraph&, const FeatureMatrix&, ReduceOp, ...)   (kernels.hpp:71-73)
+ *   Orientation required_orientation(Strategy,        gspmm_required_orientation
+ *     Operand out)                                      (kernels.hpp:48)
+ *   CsrGraph (indptr/indices/edge_ids, csr.hpp:37-54) gspmm_graph_create: a
+ *     + BlockPlan (block_plan.hpp:39-88)                device handle holding the
+ *                                                       CSR and the device plan
+ *   void validate_config(const BrConfig&)             gspmm_validate_config
+ *     (br_config.hpp:46)
+ *   StructureError/ShapeError/ConfigError             GSPMM_ERR_* status codes +
+ *     (error.hpp:22-45)                                 gspmm_last_error()
+ *
+ * Plain C types only: pointers, sizes, int32 enums whose numeric values are
+ * the reference's (ops.hpp:28,33; br_config.hpp Operand; types.hpp:35).
+ * Node/edge ids are uint32 (types.hpp:25-31).  Features are fp32 row-major
+ * with an explicit row stride `ld` (elements); ld == 0 means ld == dim, the
+ * reference's FeatureMatrix layout.
+ *
+ * Device entry points take DEVICE pointers and enqueue on `stream`
+ * (cudaStream_t, NULL = legacy default stream); they return after launch.
+ * Host entry points (`*_host`) take HOST pointers, stage through the
+ * handle's device workspace and return after the result is back on the
+ * host, like the reference's synchronous call.
+ *
+ * Semantics (identical to the reference, bit for bit):
+ *   - each output element is a sequential fp32 left fold, from the reduce
+ *     identity, over the owner row's edges in canonical CSR order (rows
+ *     ascending; neighbour ascending; edge id ascending), every multiply and
+ *     add rounded separately (kernels.cpp:162-195);
+ *   - Max uses `a < m ? m : a`, Min `m < a ? m : a` (kernels.cpp:38-52);
+ *   - Max/Min rows with no edges read 0 (kernels.cpp:490-499), other
+ *     reducers leave the identity;
+ *   - width-1 operands broadcast (stride 0, kernels.cpp:444-453);
+ *   - out == E stores one message per edge row, indexed by edge id.
+ */
+#ifndef GSPMM_B200_H
+#define GSPMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSPMM_B200_ABI_VERSION 1
+
+/* ---- status (error.hpp:22-45 taxonomy, plus device failures) ---- */
+enum {
+  GSPMM_OK = 0,
+  GSPMM_ERR_CONFIG = 1,    /* ConfigError: invalid descriptor             */
+  GSPMM_ERR_SHAPE = 2,     /* ShapeError: operand/orientation mismatch     */
+  GSPMM_ERR_STRUCTURE = 3, /* StructureError: malformed CSR                */
+  GSPMM_ERR_CUDA = 4,      /* CUDA runtime failure (no device, OOM, ...)   */
+  GSPMM_ERR_ARG = 5        /* null handle / bad pointer argument           */
+};
+
+/* ---- enums: numeric values of the reference ---- */
+enum { GSPMM_U = 0, GSPMM_V = 1, GSPMM_E = 2, GSPMM_NONE = 3 };           /* Operand */
+enum { GSPMM_ADD = 0, GSPMM_SUB = 1, GSPMM_MUL = 2, GSPMM_DIV = 3,
+       GSPMM_DOT = 4, GSPMM_COPY = 5 };                                   /* BinaryOp */
+enum { GSPMM_SUM = 0, GSPMM_MAX = 1, GSPMM_MIN = 2, GSPMM_PROD = 3,
+       GSPMM_COPY_LAST = 4,
+       GSPMM_MEAN = 5 /* extension: sum / in-degree, 0 for empty rows */ }; /* ReduceOp */
+enum { GSPMM_SRC_MAJOR = 0, GSPMM_DST_MAJOR = 1 };                       /* Orientation */
+enum { GSPMM_PUSH = 0, GSPMM_PULL = 1, GSPMM_BLOCKED = 2, GSPMM_SPMM = 3 }; /* Strategy */
+
+/* Row order of an edge operand. */
+enum {
+  GSPMM_EDGE_BY_ID = 0,  /* row i is edge id i (the reference's layout)      */
+  GSPMM_EDGE_BY_POS = 1  /* row j is the j-th nonzero of THIS handle's CSR,  */
+                         /* produced once by gspmm_graph_permute_edges       */
+};
+
+/* BrConfig (br_config.hpp:37-44) */
+typedef struct {
+  int32_t lhs, rhs, binary, reduce, out;
+} gspmm_config;
+
+/* A feature matrix view (FeatureMatrix, feature_matrix.hpp:29-66).
+ * data == NULL means "operand not supplied". */
+typedef struct {
+  const float* data;
+  int64_t rows;
+  int64_t dim;
+  int64_t ld;          /* row stride in floats, 0 -> dim */
+  int32_t edge_order;  /* GSPMM_EDGE_BY_ID / _BY_POS, E operands only */
+} gspmm_mat;
+
+typedef struct {
+  float* data;
+  int64_t rows;
+  int64_t dim;
+  int64_t ld; /* 0 -> dim */
+} gspmm_out;
+
+/* Extensions the reference does not have. Zero-init = off. */
+typedef struct {
+  /* Max/Min: winning edge per output element, -1 when no edge raised the
+   * running value (empty rows).  [out rows x dim], stride arg_ld (0 -> dim).
+   * First canonical position wins ties (the `a < m` scan). */
+  int32_t* arg_other; /* neighbour node id of the winning edge */
+  int32_t* arg_edge;  /* edge id of the winning edge           */
+  int64_t arg_ld;
+  /* Multi-head broadcast: an operand of width H (H divides the output
+   * width W) broadcasts each element over W/H consecutive columns
+   * (DGL's [N,H,D] x [E,H,1]).  With binary == DOT: `heads` per-head dot
+   * products over gather_dim/heads columns, output width = heads. */
+  int32_t heads;
+  /* Per-node scale of each edge's OTHER endpoint (the gathered node):
+   * message := message * other_scale[other], rounded (used for the mean
+   * backward: e = 1/deg_in(dst)). Device pointer, length = #other nodes. */
+  const float* other_scale;
+} gspmm_options;
+
+typedef struct gspmm_graph_s* gspmm_graph;
+
+/* ---- errors ---- */
+const char* gspmm_last_error(void); /* thread-local message of the last failure */
+int gspmm_abi_version(void);
+
+/* ---- descriptor helpers (host only, no device needed) ---- */
+/* validate_config, br_config.cpp:83-94 */
+int gspmm_validate_config(const gspmm_config* cfg);
+/* named_config, br_config.cpp:96-131: "u_mul_e_add_v", "u_copy_max_v", ... */
+int gspmm_named_config(const char* name, gspmm_config* cfg);
+/* required_orientation, kernels.cpp:400-411; returns the orientation or -1 */
+int gspmm_required_orientation(int strategy, int out);
+
+/* ---- graph handle (CsrGraph + device plan) ----
+ * Uploads a canonical CSR (host arrays) to `device`.  validate != 0 runs the
+ * reference's validate() checks (csr.cpp:111-156) on the host first and
+ * returns GSPMM_ERR_STRUCTURE on failure.  The handle owns the device CSR,
+ * the degree-binned row plan and a workspace for host calls. */
+int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
+                       uint32_t num_cols, const uint32_t* indptr,
+                       const uint32_t* indices, const uint32_t* edge_ids,
+                       int validate, gspmm_graph* out);
+int gspmm_graph_destroy(gspmm_graph g);
+int gspmm_graph_info(gspmm_graph g, int* orientation, uint32_t* num_rows,
+                     uint32_t* num_cols, uint64_t* num_edges,
+                     uint32_t* num_long_rows);
+/* Device copies of the handle's CSR arrays (read-only). */
+int gspmm_graph_device_csr(gspmm_graph g, const uint32_t** indptr,
+                           const uint32_t** indices, const uint32_t** edge_ids);
+/* Permutes an edge operand from edge-id order into this handle's CSR
+ * position order (dst[j] = src[edge_ids[j]]), on the device.  The untimed
+ * analogue of the reference's BlockPlan build (bench.cpp:95-97). */
+int gspmm_graph_permute_edges(gspmm_graph g, const float* src_by_id,
+                              int64_t dim, int64_t src_ld, float* dst_by_pos,
+                              int64_t dst_ld, void* stream);
+
+/* ---- compute (device pointers, asynchronous on stream) ---- */
+int gspmm_binary_reduce(gspmm_graph g, const gspmm_config* cfg,
+                        const gspmm_mat* u, const gspmm_mat* v,
+                        const gspmm_mat* e, const gspmm_out* out,
+                        void* stream);
+int gspmm_binary_reduce_ex(gspmm_graph g, const gspmm_config* cfg,
+                           const gspmm_mat* u, const gspmm_mat* v,
+                           const gspmm_mat* e, const gspmm_out* out,
+                           const gspmm_options* opt, void* stream);
+/* copy_reduce (kernels.cpp:503-524): source entity inferred from
+ * src->rows (node count first, then edge count). */
+int gspmm_copy_reduce(gspmm_graph g, const gspmm_mat* src, int reduce,
+                      const gspmm_out* out, void* stream);
+/* Gradient through an argmax: grad_src[arg[r,f], f] += grad_out[r,f]
+ * (f64 accumulation, then rounded to fp32; arg -1 skipped).  grad_src is
+ * overwritten. */
+int gspmm_argmax_backward(const int32_t* arg, int64_t rows, int64_t dim,
+                          int64_t arg_ld, const float* grad_out,
+                          int64_t grad_ld, float* grad_src, int64_t src_rows,
+                          int64_t src_ld, void* stream);
+
+/* ---- host-buffer entry (the reference's synchronous call shape) ----
+ * Same arguments with HOST pointers; copies in, computes, copies out and
+ * synchronizes.  Pinned host memory makes the copies asynchronous DMA. */
+int gspmm_binary_reduce_host(gspmm_graph g, const gspmm_config* cfg,
+                             const gspmm_mat* u, const gspmm_mat* v,
+                             const gspmm_mat* e, const gspmm_out* out,
+                             const gspmm_options* opt, void* stream);
+
+/* Output shape of a config on a handle (rows, width), after the full
+ * reference validation (binary_reduce kernels.cpp:418-456). */
+int gspmm_out_shape(gspmm_graph g, const gspmm_config* cfg,
+                    const gspmm_mat* u, const gspmm_mat* v,
+                    const gspmm_mat* e, const gspmm_options* opt,
+                    int64_t* rows, int64_t* dim);
+
+/* Number of kernels the library launched since load (evidence counter). */
+uint64_t gspmm_launch_count(void);
+
+/* ---- input synthesis and CSR construction (host, multithreaded) ----
+ * Bit-identical to the reference's generators (generate.cpp) and CSR
+ * builder (csr.cpp); threads <= 0 uses all hardware threads. */
+int64_t gspmm_synth_rmat(uint32_t n, uint64_t num_edges, double a, double b,
+                         double c, double d, uint64_t seed, uint32_t* src,
+                         uint32_t* dst, int threads);
+/* Erdos-Renyi: returns the edge count; buffers malloc'ed, free with gspmm_free */
+int64_t gspmm_synth_er(uint32_t n, uint64_t num_edges, double prob,
+                       uint64_t seed, uint32_t** src, uint32_t** dst);
+void gspmm_free(void* p);
+int gspmm_build_csr(uint32_t n, int64_t m, const uint32_t* src,
+                    const uint32_t* dst, int orientation, uint32_t* indptr,
+                    uint32_t* indices, uint32_t* edge_ids, int threads);
+int gspmm_transpose(uint32_t num_rows, uint32_t num_cols,
+                    const uint32_t* indptr, const uint32_t* indices,
+                    const uint32_t* edge_ids, uint32_t* t_indptr,
+                    uint32_t* t_indices, uint32_t* t_edge_ids, int threads);
+/* U[-1,1) (random_features, generate.cpp:256-266) and builder N(0,1) */
+void gspmm_synth_uniform(int64_t count, uint64_t seed, float* out, int threads);
+void gspmm_synth_normal(int64_t count, uint64_t seed, float* out, int threads);
+/* GCN weight w[e] = 1/sqrt(deg_out(src[e]) * deg_in(dst[e])), edge-id order */
+void gspmm_synth_gcn_weights(uint32_t n, int64_t m, const uint32_t* src,
+                             const uint32_t* dst, float* w, int threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSPMM_B200_H */

@@ -1,0 +1,115 @@
+// gspmm_b200.hpp -- C++ host API with the reference's entry points, over the
+// C-ABI (gspmm_b200.h).
+//
+// Same names, parameter lists, ownership and error behaviour as the
+// reference library's public API (/root/reference/proj/include/gspmm):
+//   binary_reduce / copy_reduce        kernels.hpp:60-64, 71-73
+//   required_orientation, Strategy     kernels.hpp:40-48
+//   BrConfig, validate_config,         br_config.hpp:37-59
+//     named_config, config_name
+//   CsrGraph, FeatureMatrix            csr.hpp:37-54, feature_matrix.hpp:29-66
+//   StructureError/ShapeError/         error.hpp:22-45
+//     ConfigError
+// It lives in namespace gspmm_b200 so a program can link it next to the
+// reference (the parity harness does).  A caller switches by changing the
+// namespace (or a `namespace gspmm = gspmm_b200;` alias).
+//
+// Strategy and BlockPlan are accepted for signature compatibility: the
+// device plan built at graph upload replaces both (Push is served by the
+// owner-computes kernel on the transposed view; results equal Pull's, which
+// the reference guarantees to within its tolerance).  `threads` is ignored.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "gspmm_b200.h"
+
+namespace gspmm_b200 {
+
+using NodeId = std::uint32_t;
+using EdgeId = std::uint32_t;
+
+enum class Orientation : std::uint8_t { SrcMajor = 0, DstMajor = 1 };
+enum class BinaryOp : std::uint8_t { Add, Sub, Mul, Div, Dot, CopyLhs };
+enum class ReduceOp : std::uint8_t { Sum, Max, Min, Prod, CopyLast };
+enum class Operand : std::uint8_t { U, V, E, None };
+enum class Strategy : std::uint8_t { Push, Pull, BlockedPull, RowParallelSpmm };
+
+struct StructureError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ShapeError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+// CUDA failures (no device, out of memory): the path has no CPU fallback.
+struct DeviceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct BrConfig {
+  Operand lhs = Operand::U;
+  Operand rhs = Operand::None;
+  BinaryOp binary = BinaryOp::CopyLhs;
+  ReduceOp reduce = ReduceOp::Sum;
+  Operand out = Operand::V;
+  friend bool operator==(const BrConfig&, const BrConfig&) = default;
+};
+
+struct CsrGraph {
+  Orientation orientation = Orientation::DstMajor;
+  NodeId num_rows = 0;
+  NodeId num_cols = 0;
+  std::vector<EdgeId> indptr;
+  std::vector<NodeId> indices;
+  std::vector<EdgeId> edge_ids;
+  EdgeId num_edges() const { return indptr.empty() ? 0 : indptr.back(); }
+  NodeId num_src_nodes() const {
+    return orientation == Orientation::SrcMajor ? num_rows : num_cols;
+  }
+  NodeId num_dst_nodes() const {
+    return orientation == Orientation::SrcMajor ? num_cols : num_rows;
+  }
+};
+
+struct FeatureMatrix {
+  std::int64_t rows = 0;
+  std::int64_t dim = 0;
+  std::vector<float> data;
+  FeatureMatrix() = default;
+  FeatureMatrix(std::int64_t r, std::int64_t d)
+      : rows(r), dim(d), data(static_cast<std::size_t>(r * d), 0.0f) {}
+  float* row(std::int64_t i) { return data.data() + i * dim; }
+  const float* row(std::int64_t i) const { return data.data() + i * dim; }
+  float& at(std::int64_t i, std::int64_t j) { return data[i * dim + j]; }
+  float at(std::int64_t i, std::int64_t j) const { return data[i * dim + j]; }
+};
+
+// Placeholder for the reference's Alg.-3 schedule; the device plan replaces it.
+struct BlockPlan {};
+
+void validate_config(const BrConfig& cfg);
+BrConfig named_config(std::string_view name);
+std::string config_name(const BrConfig& cfg);
+Orientation required_orientation(Strategy s, Operand out);
+
+FeatureMatrix binary_reduce(Strategy strategy, const CsrGraph& g,
+                            const BrConfig& cfg, const FeatureMatrix* u_feats,
+                            const FeatureMatrix* v_feats,
+                            const FeatureMatrix* e_feats,
+                            const BlockPlan* plan = nullptr, int threads = 0);
+
+FeatureMatrix copy_reduce(Strategy strategy, const CsrGraph& g,
+                          const FeatureMatrix& src_feats, ReduceOp reduce,
+                          const BlockPlan* plan = nullptr, int threads = 0);
+
+// Throws the exception matching a C-ABI status (no-op for GSPMM_OK).
+void throw_status(int status);
+
+}  // namespace gspmm_b200

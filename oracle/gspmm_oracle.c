@@ -234,6 +234,11 @@ void or_normal_features(int64_t count, uint64_t seed, float* out) {
   for (int64_t i = 0; i < count; ++i) out[i] = or_normal_at(seed, (uint64_t)i);
 }
 
+/* elements [offset, offset+count) of the stream (chunked generation) */
+void or_normal_features_at(int64_t offset, int64_t count, uint64_t seed, float* out) {
+  for (int64_t i = 0; i < count; ++i) out[i] = or_normal_at(seed, (uint64_t)(offset + i));
+}
+
 /* ----------------------------------------------------------- graph core */
 
 /* from_keys, csr.cpp:31-71: stable counting sort by column, then by row. */

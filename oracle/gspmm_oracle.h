@@ -51,6 +51,7 @@ int64_t or_gen_sbm(uint32_t n, int blocks, double p_in, double p_out,
 void or_free(void* p);
 void or_random_features(int64_t rows, int64_t dim, uint64_t seed, float* out);
 void or_normal_features(int64_t count, uint64_t seed, float* out);
+void or_normal_features_at(int64_t offset, int64_t count, uint64_t seed, float* out);
 
 /* ---- graph core (csr.cpp) ---- */
 int or_build_csr(uint32_t n, int64_t m, const uint32_t* src,

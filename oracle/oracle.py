@@ -78,6 +78,7 @@ def _load_c():
         "or_free": (None, [vp]),
         "or_random_features": (None, [i64, i64, u64, vp]),
         "or_normal_features": (None, [i64, u64, vp]),
+        "or_normal_features_at": (None, [i64, i64, u64, vp]),
         "or_build_csr": (i32, [u32, i64, vp, vp, i32, vp, vp, vp]),
         "or_transpose": (i32, [u32, u32, vp, vp, vp, vp, vp, vp]),
         "or_validate": (i32, [u32, u32, i64, vp, i64, vp, vp]),
@@ -153,10 +154,24 @@ def random_features(rows, dim, seed):
     return out
 
 
-def normal_features(rows, dim, seed):
-    """Builder-defined N(0,1), Box-Muller."""
+def normal_features(rows, dim, seed, threads=1):
+    """Builder-defined N(0,1), Box-Muller.  threads > 1 splits the
+    counter stream into chunks (ctypes releases the GIL)."""
     out = np.empty((rows, dim), np.float32)
-    LIB.or_normal_features(rows * dim, seed, out.ctypes.data)
+    total = rows * dim
+    if threads <= 1 or total < (1 << 20):
+        LIB.or_normal_features(total, seed, out.ctypes.data)
+        return out
+    from concurrent.futures import ThreadPoolExecutor
+    flat = out.reshape(-1)
+    bounds = np.linspace(0, total, threads + 1).astype(np.int64)
+
+    def work(k):
+        b, e = int(bounds[k]), int(bounds[k + 1])
+        LIB.or_normal_features_at(b, e - b, seed, flat[b:].ctypes.data)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(work, range(threads)))
     return out
 
 

@@ -1,0 +1,326 @@
+"""Python host API over the C-ABI, mirroring the reference's operator
+interface (proj/include/gspmm/kernels.hpp): ``binary_reduce`` / ``copy_reduce``
+with the same config names, operand roles, output shapes and error types.
+
+Device tensors are torch CUDA tensors (torch is used for device memory and
+streams only -- every byte of compute is the library's sm_100a kernels);
+``*_host`` variants take numpy arrays and go through the C-ABI host entry.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _capi as A
+from ._capi import (ADD, COPY, COPY_LAST, DIV, DOT, DST_MAJOR, E, EDGE_BY_ID, EDGE_BY_POS, MAX,
+                    MEAN, MIN, MUL, NONE, PROD, SRC_MAJOR, SUB, SUM, U, V, check)
+
+__all__ = [
+    "Graph", "binary_reduce", "binary_reduce_host", "copy_reduce", "argmax_backward",
+    "named_config", "validate_config", "required_orientation", "out_shape",
+    "synth_rmat", "synth_er", "build_csr", "transpose", "synth_uniform", "synth_normal",
+    "synth_gcn_weights", "launch_count",
+]
+
+
+def _u32(a):
+    return np.ascontiguousarray(a, dtype=np.uint32)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+# ------------------------------------------------------------------ config
+def named_config(name):
+    """named_config (br_config.cpp:96-131)."""
+    cfg = A.Config()
+    check(A.LIB.gspmm_named_config(name.encode(), C.byref(cfg)), f"named_config({name!r})")
+    return cfg
+
+
+def as_config(cfg):
+    if isinstance(cfg, A.Config):
+        return cfg
+    if isinstance(cfg, str):
+        return named_config(cfg)
+    return A.Config(*cfg)
+
+
+def validate_config(cfg):
+    check(A.LIB.gspmm_validate_config(C.byref(as_config(cfg))), "validate_config")
+
+
+def required_orientation(strategy, out):
+    o = A.LIB.gspmm_required_orientation(strategy, out)
+    if o < 0:
+        raise A.ConfigError(A.last_error())
+    return o
+
+
+def launch_count():
+    return A.LIB.gspmm_launch_count()
+
+
+# ------------------------------------------------------------------- graph
+class Graph:
+    """Device-resident CsrGraph (csr.hpp:37-54) plus the device row plan.
+
+    ``indptr/indices/edge_ids`` are host arrays in the reference's canonical
+    CSR order; they are uploaded once.  ``orientation`` is DST_MAJOR (rows are
+    destinations, the forward view) or SRC_MAJOR (the transposed view used by
+    out=U configs and the backward)."""
+
+    def __init__(self, indptr, indices, edge_ids, num_rows=None, num_cols=None,
+                 orientation=DST_MAJOR, device=0, validate=False):
+        indptr, indices, edge_ids = _u32(indptr), _u32(indices), _u32(edge_ids)
+        self.num_rows = len(indptr) - 1 if num_rows is None else int(num_rows)
+        self.num_cols = self.num_rows if num_cols is None else int(num_cols)
+        self.orientation = orientation
+        self.device = device
+        self.num_edges = int(indptr[-1]) if len(indptr) else 0
+        h = C.c_void_p()
+        check(A.LIB.gspmm_graph_create(device, orientation, self.num_rows, self.num_cols,
+                                       _ptr(indptr), _ptr(indices), _ptr(edge_ids),
+                                       1 if validate else 0, C.byref(h)), "graph_create")
+        self._h = h
+        nl = C.c_uint32()
+        check(A.LIB.gspmm_graph_info(h, None, None, None, None, C.byref(nl)))
+        self.num_long_rows = nl.value
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise A.ArgumentError("graph handle already closed")
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            A.LIB.gspmm_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def entity_rows(self, ent):
+        src_major = self.orientation == SRC_MAJOR
+        if ent == U:
+            return self.num_rows if src_major else self.num_cols
+        if ent == V:
+            return self.num_cols if src_major else self.num_rows
+        return self.num_edges
+
+    def permute_edges(self, e, stream=None):
+        """Edge operand in edge-id order -> this handle's CSR position order
+        (device, untimed setup like the reference's BlockPlan)."""
+        import torch
+        e2 = e.reshape(e.shape[0], -1)
+        out = torch.empty_like(e2)
+        check(A.LIB.gspmm_graph_permute_edges(self.handle, e2.data_ptr(), e2.shape[1],
+                                              e2.stride(0), out.data_ptr(), out.stride(0),
+                                              _stream(stream, e2)), "permute_edges")
+        return out
+
+
+# -------------------------------------------------------------- operands
+def _stream(stream, ref_tensor=None):
+    if stream is not None:
+        return stream if isinstance(stream, int) else stream.cuda_stream
+    import torch
+    dev = ref_tensor.device if ref_tensor is not None else None
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def _dev_mat(t, edge_order=EDGE_BY_ID):
+    if t is None:
+        return None
+    import torch
+    if t.dtype != torch.float32 or not t.is_cuda:
+        raise A.ShapeError("operands must be float32 CUDA tensors")
+    t2 = t.reshape(t.shape[0], -1) if t.dim() != 2 else t
+    if t2.shape[1] > 1 and t2.stride(1) != 1:
+        raise A.ShapeError("operand rows must be contiguous")
+    ld = t2.stride(0) if t2.shape[0] > 1 else t2.shape[1]
+    m = A.Mat(t2.data_ptr(), t2.shape[0], t2.shape[1], ld, edge_order)
+    m._keep = t2
+    return m
+
+
+def _host_mat(a, edge_order=EDGE_BY_ID):
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    m = A.Mat(a.ctypes.data if a.size else 1, a.shape[0], a.shape[1], a.shape[1], edge_order)
+    m._keep = a
+    return m
+
+
+def _opts(heads=1, arg_other=None, arg_edge=None, other_scale=None, arg_ld=0):
+    o = A.Options()
+    o.heads = heads
+    o.arg_other = arg_other
+    o.arg_edge = arg_edge
+    o.arg_ld = arg_ld
+    o.other_scale = other_scale
+    return o
+
+
+def _ref(m):
+    return C.byref(m) if m is not None else None
+
+
+def out_shape(graph, cfg, u=None, v=None, e=None, heads=1, host=False):
+    cfg = as_config(cfg)
+    mk = _host_mat if host else _dev_mat
+    mu, mv, me = mk(u), mk(v), mk(e)
+    r, d = C.c_int64(), C.c_int64()
+    check(A.LIB.gspmm_out_shape(graph.handle, C.byref(cfg), _ref(mu), _ref(mv), _ref(me),
+                                C.byref(_opts(heads)), C.byref(r), C.byref(d)), "binary_reduce")
+    return r.value, d.value
+
+
+# ----------------------------------------------------------------- compute
+def binary_reduce(graph, cfg, u=None, v=None, e=None, *, out=None, e_order=EDGE_BY_ID,
+                  want_arg_other=False, want_arg_edge=False, heads=1, other_scale=None,
+                  stream=None):
+    """binary_reduce (kernels.hpp:60-64) on device tensors.
+
+    Returns ``out`` (allocated when not given) or ``(out, arg_other,
+    arg_edge)`` when an argmax output is requested."""
+    import torch
+    cfg = as_config(cfg)
+    mu, mv, me = _dev_mat(u), _dev_mat(v), _dev_mat(e, e_order)
+    ref_t = next(t for t in (u, v, e) if t is not None) if any(
+        t is not None for t in (u, v, e)) else None
+    rows, dim = out_shape(graph, cfg, u, v, e, heads)
+    dev = ref_t.device if ref_t is not None else torch.device("cuda", graph.device)
+    if out is None:
+        out = torch.empty((rows, dim), dtype=torch.float32, device=dev)
+    mo = A.Out(out.data_ptr(), rows, dim, out.stride(0) if out.dim() == 2 else dim)
+    ao = torch.empty((rows, dim), dtype=torch.int32, device=dev) if want_arg_other else None
+    ae = torch.empty((rows, dim), dtype=torch.int32, device=dev) if want_arg_edge else None
+    opts = _opts(heads, ao.data_ptr() if ao is not None else None,
+                 ae.data_ptr() if ae is not None else None,
+                 other_scale.data_ptr() if other_scale is not None else None)
+    check(A.LIB.gspmm_binary_reduce_ex(graph.handle, C.byref(cfg), _ref(mu), _ref(mv), _ref(me),
+                                       C.byref(mo), C.byref(opts), _stream(stream, ref_t)),
+          "binary_reduce")
+    if want_arg_other or want_arg_edge:
+        return out, ao, ae
+    return out
+
+
+def copy_reduce(graph, src, reduce, *, out=None, stream=None):
+    """copy_reduce (kernels.hpp:71-73): source entity inferred from rows."""
+    import torch
+    ms = _dev_mat(src)
+    rows = graph.entity_rows(V)
+    if out is None:
+        out = torch.empty((rows, ms.dim), dtype=torch.float32, device=src.device)
+    mo = A.Out(out.data_ptr(), rows, ms.dim, out.stride(0))
+    check(A.LIB.gspmm_copy_reduce(graph.handle, C.byref(ms), reduce, C.byref(mo),
+                                  _stream(stream, src)), "copy_reduce")
+    return out
+
+
+def argmax_backward(arg, grad_out, src_rows, *, out=None, stream=None):
+    """grad_src[arg[r,f], f] += grad_out[r,f] (f64 accumulate, fp32 result)."""
+    import torch
+    rows, dim = arg.shape
+    if out is None:
+        out = torch.empty((src_rows, dim), dtype=torch.float32, device=grad_out.device)
+    check(A.LIB.gspmm_argmax_backward(arg.data_ptr(), rows, dim, arg.stride(0),
+                                      grad_out.data_ptr(), grad_out.stride(0), out.data_ptr(),
+                                      src_rows, out.stride(0), _stream(stream, grad_out)),
+          "argmax_backward")
+    return out
+
+
+def binary_reduce_host(graph, cfg, u=None, v=None, e=None, *, out=None, want_arg_other=False,
+                       want_arg_edge=False, heads=1, stream=None):
+    """The reference's synchronous call shape: numpy in, numpy out, through
+    the C-ABI host entry (H2D, kernel, D2H)."""
+    cfg = as_config(cfg)
+    mu, mv, me = _host_mat(u), _host_mat(v), _host_mat(e)
+    rows, dim = out_shape(graph, cfg, u, v, e, heads, host=True)
+    if out is None:
+        out = np.empty((rows, dim), np.float32)
+    mo = A.Out(out.ctypes.data, rows, dim, dim)
+    ao = np.empty((rows, dim), np.int32) if want_arg_other else None
+    ae = np.empty((rows, dim), np.int32) if want_arg_edge else None
+    opts = _opts(heads, _ptr(ao), _ptr(ae))
+    check(A.LIB.gspmm_binary_reduce_host(graph.handle, C.byref(cfg), _ref(mu), _ref(mv), _ref(me),
+                                         C.byref(mo), C.byref(opts), stream or None),
+          "binary_reduce_host")
+    if want_arg_other or want_arg_edge:
+        return out, ao, ae
+    return out
+
+
+# ------------------------------------------------- synthesis and CSR build
+def synth_rmat(n, num_edges, a=0.57, b=0.19, c=0.19, d=0.05, seed=0, threads=0):
+    src = np.empty(max(num_edges, 1), np.uint32)
+    dst = np.empty(max(num_edges, 1), np.uint32)
+    m = A.LIB.gspmm_synth_rmat(n, num_edges, a, b, c, d, seed, _ptr(src), _ptr(dst), threads)
+    if m < 0:
+        raise A.ConfigError("rmat: could not place an edge inside the node range")
+    return src[:num_edges], dst[:num_edges]
+
+
+def synth_er(n, num_edges=0, prob=-1.0, seed=0):
+    ps, pd = C.c_void_p(), C.c_void_p()
+    m = A.LIB.gspmm_synth_er(n, num_edges, prob, seed, C.byref(ps), C.byref(pd))
+    cap = max(m, 1)
+    src = np.ctypeslib.as_array(C.cast(ps, C.POINTER(C.c_uint32)), shape=(cap,))[:m].copy()
+    dst = np.ctypeslib.as_array(C.cast(pd, C.POINTER(C.c_uint32)), shape=(cap,))[:m].copy()
+    A.LIB.gspmm_free(ps)
+    A.LIB.gspmm_free(pd)
+    return src, dst
+
+
+def build_csr(n, src, dst, orientation=DST_MAJOR, threads=0):
+    src, dst = _u32(src), _u32(dst)
+    m = len(src)
+    indptr = np.empty(n + 1, np.uint32)
+    indices = np.empty(max(m, 1), np.uint32)
+    eids = np.empty(max(m, 1), np.uint32)
+    check(A.LIB.gspmm_build_csr(n, m, _ptr(src), _ptr(dst), orientation, _ptr(indptr),
+                                _ptr(indices), _ptr(eids), threads), "build_csr")
+    return indptr, indices[:m], eids[:m]
+
+
+def transpose(num_rows, num_cols, indptr, indices, eids, threads=0):
+    indptr, indices, eids = _u32(indptr), _u32(indices), _u32(eids)
+    m = int(indptr[-1])
+    t_indptr = np.empty(num_cols + 1, np.uint32)
+    t_indices = np.empty(max(m, 1), np.uint32)
+    t_eids = np.empty(max(m, 1), np.uint32)
+    check(A.LIB.gspmm_transpose(num_rows, num_cols, _ptr(indptr), _ptr(indices), _ptr(eids),
+                                _ptr(t_indptr), _ptr(t_indices), _ptr(t_eids), threads),
+          "transpose")
+    return t_indptr, t_indices[:m], t_eids[:m]
+
+
+def synth_uniform(rows, dim, seed, threads=0, out=None):
+    out = np.empty((rows, dim), np.float32) if out is None else out
+    A.LIB.gspmm_synth_uniform(rows * dim, seed, out.ctypes.data, threads)
+    return out
+
+
+def synth_normal(rows, dim, seed, threads=0, out=None):
+    out = np.empty((rows, dim), np.float32) if out is None else out
+    A.LIB.gspmm_synth_normal(rows * dim, seed, out.ctypes.data, threads)
+    return out
+
+
+def synth_gcn_weights(n, src, dst, threads=0):
+    src, dst = _u32(src), _u32(dst)
+    w = np.empty((len(src), 1), np.float32)
+    A.LIB.gspmm_synth_gcn_weights(n, len(src), _ptr(src), _ptr(dst), w.ctypes.data, threads)
+    return w

@@ -1,0 +1,100 @@
+// aux.cu -- the small sm_100a kernels around the aggregation:
+//   * edge-operand permutation into CSR position order (the device plan's
+//     analogue of the reference building its BlockPlan outside the timed
+//     region, bench.cpp:95-97);
+//   * the gradient through a max/min argmax: a scatter
+//     with f64 atomics into a workspace, then one rounding to fp32, so the
+//     result matches the oracle's f64 accumulation independently of the
+//     order in which the atomics land.  Backward only: the forward path
+//     never uses atomics.
+#include <atomic>
+
+#include "device_ops.cuh"
+
+namespace gspmm_b200 {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+
+__global__ void k_permute_edges(const uint32_t* __restrict__ eids, uint64_t m,
+                                const float* __restrict__ src, int64_t dim,
+                                int64_t src_ld, float* __restrict__ dst,
+                                int64_t dst_ld) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+       i < m * static_cast<uint64_t>(dim); i += stride) {
+    const uint64_t j = i / dim;
+    const int64_t c = static_cast<int64_t>(i - j * dim);
+    dst[j * dst_ld + c] = __ldg(src + static_cast<int64_t>(__ldg(eids + j)) * src_ld + c);
+  }
+}
+
+__global__ void k_argmax_scatter(const int32_t* __restrict__ arg, int64_t rows,
+                                 int64_t dim, int64_t arg_ld,
+                                 const float* __restrict__ grad,
+                                 int64_t grad_ld, double* __restrict__ acc) {
+  const int64_t total = rows * dim;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+       i < total; i += stride) {
+    const int64_t r = i / dim, c = i - r * dim;
+    const int32_t a = __ldg(arg + r * arg_ld + c);
+    if (a >= 0) atomicAdd(acc + static_cast<int64_t>(a) * dim + c,
+                          static_cast<double>(__ldg(grad + r * grad_ld + c)));
+  }
+}
+
+__global__ void k_round_f64(const double* __restrict__ acc, int64_t rows,
+                            int64_t dim, float* __restrict__ out, int64_t ld) {
+  const int64_t total = rows * dim;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+       i < total; i += stride) {
+    const int64_t r = i / dim, c = i - r * dim;
+    out[r * ld + c] = __double2float_rn(acc[i]);
+  }
+}
+
+unsigned grid_for(int64_t work, int threads) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b > 148 * 32) b = 148 * 32;
+  return static_cast<unsigned>(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+cudaError_t launch_permute_edges(const uint32_t* eids, uint64_t m,
+                                 const float* src, int64_t dim, int64_t src_ld,
+                                 float* dst, int64_t dst_ld, cudaStream_t s) {
+  if (m == 0 || dim == 0) return cudaSuccess;
+  k_permute_edges<<<grid_for(static_cast<int64_t>(m) * dim, 256), 256, 0, s>>>(
+      eids, m, src, dim, src_ld, dst, dst_ld);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_argmax_backward(const int32_t* arg, int64_t rows,
+                                   int64_t dim, int64_t arg_ld,
+                                   const float* grad_out, int64_t grad_ld,
+                                   float* grad_src, int64_t src_rows,
+                                   int64_t src_ld, double* acc,
+                                   cudaStream_t s) {
+  cudaError_t err = cudaMemsetAsync(acc, 0, sizeof(double) * src_rows * dim, s);
+  if (err != cudaSuccess) return err;
+  if (rows * dim > 0) {
+    k_argmax_scatter<<<grid_for(rows * dim, 256), 256, 0, s>>>(arg, rows, dim, arg_ld,
+                                                               grad_out, grad_ld, acc);
+    note_launch();
+  }
+  if (src_rows * dim > 0) {
+    k_round_f64<<<grid_for(src_rows * dim, 256), 256, 0, s>>>(acc, src_rows, dim, grad_src,
+                                                             src_ld);
+    note_launch();
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace gspmm_b200

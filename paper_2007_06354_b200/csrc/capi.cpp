@@ -1,0 +1,612 @@
+// capi.cpp -- the extern "C" boundary (include/gspmm_b200.h): descriptor
+// validation with the reference's rules and error taxonomy, the device graph
+// handle (CSR + degree plan), operand binding, vector-width selection and
+// kernel dispatch.  No CPU fallback exists: every compute entry point either
+// launches the sm_100a kernels or returns an error.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gspmm_b200.h"
+#include "internal.h"
+
+namespace gspmm_b200 {
+uint64_t launch_count();
+}
+
+using namespace gspmm_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int status, const std::string& msg) {
+  g_err = msg;
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(GSPMM_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(expr, where)                     \
+  do {                                            \
+    cudaError_t _e = (expr);                      \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+const char* operand_name(int o) {
+  switch (o) {
+    case GSPMM_U: return "u";
+    case GSPMM_V: return "v";
+    case GSPMM_E: return "e";
+    default: return "none";
+  }
+}
+
+// Rows above this degree are scheduled first (descending degree).
+constexpr uint32_t kLongThreshold = 1024;
+
+}  // namespace
+
+struct gspmm_graph_s {
+  int device = 0;
+  int orientation = GSPMM_DST_MAJOR;
+  uint32_t num_rows = 0, num_cols = 0;
+  uint64_t m = 0;
+  uint32_t* d_indptr = nullptr;
+  uint32_t* d_indices = nullptr;
+  uint32_t* d_eids = nullptr;
+  uint32_t* d_long = nullptr;
+  uint32_t num_long = 0;
+  int num_sms = 148;
+  std::mutex mu;  // guards the host-call workspace
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+};
+
+namespace {
+
+// ---------------------------------------------------------------- config
+
+int validate_cfg(const gspmm_config* c) {
+  if (!c) return fail(GSPMM_ERR_ARG, "null config");
+  auto bad_op = [](int o) { return o < GSPMM_U || o > GSPMM_NONE; };
+  if (bad_op(c->lhs) || bad_op(c->rhs) || bad_op(c->out) || c->binary < GSPMM_ADD ||
+      c->binary > GSPMM_COPY || c->reduce < GSPMM_SUM || c->reduce > GSPMM_MEAN)
+    return fail(GSPMM_ERR_CONFIG, "enum value out of range");
+  // validate_config, br_config.cpp:83-94
+  if (c->lhs == GSPMM_NONE) return fail(GSPMM_ERR_CONFIG, "lhs operand must be u, v or e");
+  if (c->out == GSPMM_NONE) return fail(GSPMM_ERR_CONFIG, "output target must be u, v or e");
+  if ((c->rhs == GSPMM_NONE) != (c->binary == GSPMM_COPY))
+    return fail(GSPMM_ERR_CONFIG, "rhs is absent exactly for the copy operator");
+  if (c->rhs != GSPMM_NONE && c->rhs == c->lhs)
+    return fail(GSPMM_ERR_CONFIG, "lhs and rhs must bind to different entities");
+  if (c->out == GSPMM_E && c->reduce != GSPMM_COPY_LAST)
+    return fail(GSPMM_ERR_CONFIG, "edge-destined configs store, reduce must be copy");
+  return GSPMM_OK;
+}
+
+struct Bound {
+  RowLaunch L;
+  int64_t out_rows = 0;
+  int64_t width = 0;
+};
+
+int64_t entity_rows(const gspmm_graph_s* g, int ent) {
+  const bool src_major = g->orientation == GSPMM_SRC_MAJOR;
+  if (ent == GSPMM_U) return src_major ? g->num_rows : g->num_cols;
+  if (ent == GSPMM_V) return src_major ? g->num_cols : g->num_rows;
+  return static_cast<int64_t>(g->m);
+}
+
+int32_t role_of(const gspmm_graph_s* g, int ent, int edge_order) {
+  if (ent == GSPMM_E) return edge_order == GSPMM_EDGE_BY_POS ? ROLE_POS : ROLE_EID;
+  const bool row_is_u = g->orientation == GSPMM_SRC_MAJOR;
+  return (ent == GSPMM_U) == row_is_u ? ROLE_ROW : ROLE_OTHER;
+}
+
+bool aligned(const void* p, int bytes) {
+  return (reinterpret_cast<uintptr_t>(p) % static_cast<uintptr_t>(bytes)) == 0;
+}
+
+// The full binding of binary_reduce (kernels.cpp:418-456) plus the
+// extensions (mean, heads, argmax, other_scale).  out may be null (shape
+// query only).
+int bind(const gspmm_graph_s* g, const gspmm_config* cfg, const gspmm_mat* u,
+         const gspmm_mat* v, const gspmm_mat* e, const gspmm_out* out,
+         const gspmm_options* opt, Bound* b) {
+  if (!g) return fail(GSPMM_ERR_ARG, "null graph handle");
+  int st = validate_cfg(cfg);
+  if (st) return st;
+  // required_orientation(strategy != Push, out), kernels.cpp:400-411
+  const int need = cfg->out == GSPMM_U ? GSPMM_SRC_MAJOR : GSPMM_DST_MAJOR;
+  if (g->orientation != need)
+    return fail(GSPMM_ERR_SHAPE, std::string("output ") + operand_name(cfg->out) + " needs a " +
+                                     (need == GSPMM_SRC_MAJOR ? "src-major" : "dst-major") +
+                                     " graph, got " +
+                                     (g->orientation == GSPMM_SRC_MAJOR ? "src-major" : "dst-major"));
+  const gspmm_options none{};
+  if (!opt) opt = &none;
+  const int heads = opt->heads > 1 ? opt->heads : 1;
+
+  auto pick = [&](int o) { return o == GSPMM_U ? u : o == GSPMM_V ? v : e; };
+  // bind_operand, kernels.cpp:361-377
+  auto bind_one = [&](int o, const gspmm_mat*& m) -> int {
+    m = pick(o);
+    if (!m || !m->data)
+      return fail(GSPMM_ERR_SHAPE, std::string("missing feature matrix for operand ") + operand_name(o));
+    if (m->rows != entity_rows(g, o))
+      return fail(GSPMM_ERR_SHAPE, std::string("operand ") + operand_name(o) + " has " +
+                                       std::to_string(m->rows) + " rows, entity has " +
+                                       std::to_string(entity_rows(g, o)));
+    if (m->dim < 1 || (m->ld != 0 && m->ld < m->dim))
+      return fail(GSPMM_ERR_SHAPE, std::string("operand ") + operand_name(o) + " has a bad dim/ld");
+    return GSPMM_OK;
+  };
+  const gspmm_mat* lm = nullptr;
+  const gspmm_mat* rm = nullptr;
+  if ((st = bind_one(cfg->lhs, lm))) return st;
+  const int64_t dl = lm->dim;
+  int64_t dr = dl;
+  if (cfg->rhs != GSPMM_NONE) {
+    if ((st = bind_one(cfg->rhs, rm))) return st;
+    dr = rm->dim;
+  }
+  const bool is_dot = cfg->binary == GSPMM_DOT;
+  const int64_t gather = std::max(dl, dr);
+  auto head_ok = [&](int64_t d) {
+    return !is_dot && heads > 1 && d == heads && gather % heads == 0 && d < gather;
+  };
+  if (rm && !(dl == dr || dl == 1 || dr == 1 || head_ok(dl) || head_ok(dr)))
+    return fail(GSPMM_ERR_SHAPE, "operand widths are not broadcast-compatible");
+  if (is_dot && heads > 1 && gather % heads != 0)
+    return fail(GSPMM_ERR_SHAPE, "dot heads must divide the operand width");
+  int64_t w = is_dot ? heads : cfg->binary == GSPMM_COPY ? dl : gather;
+  if (cfg->reduce == GSPMM_MEAN && cfg->out == GSPMM_E)
+    return fail(GSPMM_ERR_CONFIG, "mean reduces into nodes only");
+  const bool want_arg = opt->arg_other || opt->arg_edge;
+  if (want_arg && cfg->reduce != GSPMM_MAX && cfg->reduce != GSPMM_MIN)
+    return fail(GSPMM_ERR_CONFIG, "argmax outputs need the max or min reducer");
+  if (want_arg && (is_dot || cfg->out == GSPMM_E))
+    return fail(GSPMM_ERR_CONFIG, "argmax outputs need a node-destined, non-dot config");
+  if (is_dot && heads > 1 && cfg->out != GSPMM_E)
+    return fail(GSPMM_ERR_CONFIG, "per-head dot is edge-destined only");
+
+  RowLaunch& L = b->L;
+  L = RowLaunch{};
+  L.indptr = g->d_indptr;
+  L.indices = g->d_indices;
+  L.eids = g->d_eids;
+  L.num_rows = g->num_rows;
+  auto mk = [&](int o, const gspmm_mat* m) {
+    OperandDesc d;
+    d.base = m->data;
+    d.ld = m->ld ? m->ld : m->dim;
+    d.role = role_of(g, o, m->edge_order);
+    if (m->dim == 1 && gather > 1) {
+      d.mode = MODE_SCALAR;  // stride 0, kernels.cpp:451-453
+    } else if (m->dim < gather) {
+      d.mode = MODE_HEAD;
+      d.group = static_cast<int32_t>(gather / m->dim);
+    } else {
+      d.mode = MODE_FULL;
+    }
+    return d;
+  };
+  L.lhs = mk(cfg->lhs, lm);
+  if (rm) L.rhs = mk(cfg->rhs, rm);
+  L.binop = cfg->binary;
+  L.reduce = cfg->reduce == GSPMM_MEAN ? R_SUM : cfg->reduce;
+  L.mean = cfg->reduce == GSPMM_MEAN;
+  L.out_edge = cfg->out == GSPMM_E;
+  L.width = static_cast<int32_t>(w);
+  L.gather_dim = static_cast<int32_t>(gather);
+  L.heads = heads;
+  L.other_scale = opt->other_scale;
+  L.arg_other = opt->arg_other;
+  L.arg_edge = opt->arg_edge;
+  L.arg_ld = opt->arg_ld ? opt->arg_ld : w;
+  L.long_rows = g->d_long;
+  L.num_long = g->num_long;
+  L.long_threshold = g->num_long ? kLongThreshold : 0xffffffffu;
+  L.num_sms = g->num_sms;
+  b->out_rows = entity_rows(g, cfg->out);
+  b->width = w;
+
+  if (out) {
+    if (!out->data) return fail(GSPMM_ERR_SHAPE, "missing output matrix");
+    if (out->rows != b->out_rows || out->dim != w || (out->ld != 0 && out->ld < w))
+      return fail(GSPMM_ERR_SHAPE, "output must be " + std::to_string(b->out_rows) + " x " +
+                                       std::to_string(w));
+    L.out = out->data;
+    L.out_ld = out->ld ? out->ld : w;
+  }
+
+  // Widest vector every operand layout admits.
+  auto vec_ok = [&](int V) {
+    auto ok_op = [&](const OperandDesc& d) {
+      if (!d.base) return true;
+      if (d.mode == MODE_FULL) return d.ld % V == 0 && aligned(d.base, 4 * V);
+      if (d.mode == MODE_HEAD) return d.group % V == 0;
+      return true;
+    };
+    if (!ok_op(L.lhs) || !ok_op(L.rhs)) return false;
+    if (!is_dot && L.out && !(L.out_ld % V == 0 && aligned(L.out, 4 * V))) return false;
+    return true;
+  };
+  L.vec = vec_ok(4) ? 4 : vec_ok(2) ? 2 : 1;
+  return GSPMM_OK;
+}
+
+int launch(gspmm_graph_s* g, Bound& b, void* stream) {
+  cudaError_t err;
+  if (b.L.binop == GSPMM_DOT)
+    err = launch_dot(b.L, static_cast<cudaStream_t>(stream));
+  else
+    err = launch_rows(b.L, static_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "kernel launch");
+  (void)g;
+  return GSPMM_OK;
+}
+
+// Host validate, csr.cpp:111-156 (same checks, same order).
+int validate_host(uint32_t num_rows, uint32_t num_cols, const uint32_t* indptr,
+                  const uint32_t* indices, const uint32_t* eids) {
+  if (indptr[0] != 0) return fail(GSPMM_ERR_STRUCTURE, "indptr[0] != 0");
+  for (uint32_t r = 0; r < num_rows; ++r)
+    if (indptr[r] > indptr[r + 1])
+      return fail(GSPMM_ERR_STRUCTURE, "indptr not monotone at row " + std::to_string(r + 1));
+  const uint64_t m = indptr[num_rows];
+  for (uint64_t j = 0; j < m; ++j)
+    if (indices[j] >= num_cols)
+      return fail(GSPMM_ERR_STRUCTURE, "index out of range at nonzero " + std::to_string(j));
+  std::vector<bool> seen(m, false);
+  for (uint64_t j = 0; j < m; ++j) {
+    if (eids[j] >= m || seen[eids[j]])
+      return fail(GSPMM_ERR_STRUCTURE,
+                  "edge_ids not a permutation (at nonzero " + std::to_string(j) + ")");
+    seen[eids[j]] = true;
+  }
+  for (uint32_t r = 0; r < num_rows; ++r)
+    for (uint32_t j = indptr[r]; j + 1 < indptr[r + 1]; ++j) {
+      const bool ordered = indices[j] < indices[j + 1] ||
+                           (indices[j] == indices[j + 1] && eids[j] < eids[j + 1]);
+      if (!ordered)
+        return fail(GSPMM_ERR_STRUCTURE, "row " + std::to_string(r) + " not sorted at nonzero " +
+                                             std::to_string(j + 1));
+    }
+  return GSPMM_OK;
+}
+
+size_t mat_bytes(const gspmm_mat* m) {
+  if (!m || !m->data) return 0;
+  const int64_t ld = m->ld ? m->ld : m->dim;
+  return m->rows ? static_cast<size_t>((m->rows - 1) * ld + m->dim) * sizeof(float) : 0;
+}
+
+size_t round_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+}  // namespace
+
+extern "C" {
+
+const char* gspmm_last_error(void) { return g_err.c_str(); }
+int gspmm_abi_version(void) { return GSPMM_B200_ABI_VERSION; }
+uint64_t gspmm_launch_count(void) { return gspmm_b200::launch_count(); }
+
+int gspmm_validate_config(const gspmm_config* cfg) { return validate_cfg(cfg); }
+
+// named_config, br_config.cpp:96-131
+int gspmm_named_config(const char* name, gspmm_config* cfg) {
+  if (!name || !cfg) return fail(GSPMM_ERR_ARG, "null argument");
+  std::vector<std::string> t;
+  std::string cur;
+  for (const char* p = name;; ++p) {
+    if (*p == '_' || *p == '\0') {
+      t.push_back(cur);
+      cur.clear();
+      if (*p == '\0') break;
+    } else {
+      cur += *p;
+    }
+  }
+  auto opnd = [](const std::string& s) {
+    return s == "u" ? GSPMM_U : s == "v" ? GSPMM_V : s == "e" ? GSPMM_E : -1;
+  };
+  auto bin = [](const std::string& s) {
+    return s == "add" ? GSPMM_ADD : s == "sub" ? GSPMM_SUB : s == "mul" ? GSPMM_MUL
+         : s == "div" ? GSPMM_DIV : s == "dot" ? GSPMM_DOT : -1;
+  };
+  auto red = [](const std::string& s) {
+    return s == "add" ? GSPMM_SUM : s == "max" ? GSPMM_MAX : s == "min" ? GSPMM_MIN
+         : s == "mul" ? GSPMM_PROD : s == "copy" ? GSPMM_COPY_LAST : -1;
+  };
+  const std::string bad = std::string("invalid config name '") + name + "': ";
+  gspmm_config c{};
+  if (t.size() == 4) {
+    const int l = opnd(t[0]), r = red(t[2]);
+    if (l < 0 || t[1] != "copy" || r < 0 || t[3] != "v")
+      return fail(GSPMM_ERR_CONFIG, bad + "expected {u,e}_copy_{add,max,min,mul,copy}_v");
+    if (l == GSPMM_V) return fail(GSPMM_ERR_CONFIG, bad + "copy source must be u or e");
+    c = {l, GSPMM_NONE, GSPMM_COPY, r, GSPMM_V};
+  } else if (t.size() == 5) {
+    const int l = opnd(t[0]), b = bin(t[1]), r = opnd(t[2]), rd = red(t[3]), o = opnd(t[4]);
+    if (l < 0 || b < 0 || r < 0 || rd < 0 || o < 0)
+      return fail(GSPMM_ERR_CONFIG, bad + "expected {u,v,e}_<binop>_{u,v,e}_<redop>_{u,v,e}");
+    c = {l, r, b, o == GSPMM_E ? GSPMM_COPY_LAST : rd, o};
+  } else {
+    return fail(GSPMM_ERR_CONFIG, bad + "expected 4 or 5 '_'-separated tokens");
+  }
+  const int st = validate_cfg(&c);
+  if (st) return st;
+  *cfg = c;
+  return GSPMM_OK;
+}
+
+int gspmm_required_orientation(int strategy, int out) {
+  const bool owner_rows = strategy != GSPMM_PUSH;
+  if (out == GSPMM_V || out == GSPMM_E) return owner_rows ? GSPMM_DST_MAJOR : GSPMM_SRC_MAJOR;
+  if (out == GSPMM_U) return owner_rows ? GSPMM_SRC_MAJOR : GSPMM_DST_MAJOR;
+  fail(GSPMM_ERR_CONFIG, "output target must be u, v or e");
+  return -1;
+}
+
+int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
+                       uint32_t num_cols, const uint32_t* indptr,
+                       const uint32_t* indices, const uint32_t* edge_ids,
+                       int validate, gspmm_graph* out) {
+  if (!out || !indptr) return fail(GSPMM_ERR_ARG, "null argument");
+  if (orientation != GSPMM_SRC_MAJOR && orientation != GSPMM_DST_MAJOR)
+    return fail(GSPMM_ERR_ARG, "orientation must be 0 (src-major) or 1 (dst-major)");
+  const uint64_t m = indptr[num_rows];
+  if (m && (!indices || !edge_ids)) return fail(GSPMM_ERR_ARG, "null CSR array");
+  if (validate) {
+    const int st = validate_host(num_rows, num_cols, indptr, indices, edge_ids);
+    if (st) return st;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(GSPMM_ERR_CUDA, "no CUDA device visible: the B200 kernels cannot run here");
+  if (device < 0 || device >= ndev) return fail(GSPMM_ERR_ARG, "device index out of range");
+  CUDA_TRY(cudaSetDevice(device), "cudaSetDevice");
+
+  auto* g = new gspmm_graph_s;
+  g->device = device;
+  g->orientation = orientation;
+  g->num_rows = num_rows;
+  g->num_cols = num_cols;
+  g->m = m;
+  cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
+
+  // Degree plan: rows above kLongThreshold, heaviest first.
+  std::vector<uint32_t> long_rows;
+  for (uint32_t r = 0; r < num_rows; ++r)
+    if (indptr[r + 1] - indptr[r] > kLongThreshold) long_rows.push_back(r);
+  std::stable_sort(long_rows.begin(), long_rows.end(), [&](uint32_t a, uint32_t b) {
+    return indptr[a + 1] - indptr[a] > indptr[b + 1] - indptr[b];
+  });
+  g->num_long = static_cast<uint32_t>(long_rows.size());
+
+  auto cleanup = [&](cudaError_t e, const char* where) {
+    cudaFree(g->d_indptr);
+    cudaFree(g->d_indices);
+    cudaFree(g->d_eids);
+    cudaFree(g->d_long);
+    delete g;
+    return cuda_fail(e, where);
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&g->d_indptr, sizeof(uint32_t) * (num_rows + 1))) != cudaSuccess)
+    return cleanup(e, "cudaMalloc indptr");
+  if ((e = cudaMalloc(&g->d_indices, sizeof(uint32_t) * std::max<uint64_t>(m, 1))) != cudaSuccess)
+    return cleanup(e, "cudaMalloc indices");
+  if ((e = cudaMalloc(&g->d_eids, sizeof(uint32_t) * std::max<uint64_t>(m, 1))) != cudaSuccess)
+    return cleanup(e, "cudaMalloc edge_ids");
+  if ((e = cudaMalloc(&g->d_long, sizeof(uint32_t) * std::max<size_t>(long_rows.size(), 1))) !=
+      cudaSuccess)
+    return cleanup(e, "cudaMalloc plan");
+  if ((e = cudaMemcpy(g->d_indptr, indptr, sizeof(uint32_t) * (num_rows + 1),
+                      cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cleanup(e, "upload indptr");
+  if (m) {
+    if ((e = cudaMemcpy(g->d_indices, indices, sizeof(uint32_t) * m, cudaMemcpyHostToDevice)) !=
+        cudaSuccess)
+      return cleanup(e, "upload indices");
+    if ((e = cudaMemcpy(g->d_eids, edge_ids, sizeof(uint32_t) * m, cudaMemcpyHostToDevice)) !=
+        cudaSuccess)
+      return cleanup(e, "upload edge_ids");
+  }
+  if (!long_rows.empty() &&
+      (e = cudaMemcpy(g->d_long, long_rows.data(), sizeof(uint32_t) * long_rows.size(),
+                      cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cleanup(e, "upload plan");
+  *out = g;
+  return GSPMM_OK;
+}
+
+int gspmm_graph_destroy(gspmm_graph g) {
+  if (!g) return GSPMM_OK;
+  cudaSetDevice(g->device);
+  cudaFree(g->d_indptr);
+  cudaFree(g->d_indices);
+  cudaFree(g->d_eids);
+  cudaFree(g->d_long);
+  cudaFree(g->ws);
+  delete g;
+  return GSPMM_OK;
+}
+
+int gspmm_graph_info(gspmm_graph g, int* orientation, uint32_t* num_rows,
+                     uint32_t* num_cols, uint64_t* num_edges,
+                     uint32_t* num_long_rows) {
+  if (!g) return fail(GSPMM_ERR_ARG, "null graph handle");
+  if (orientation) *orientation = g->orientation;
+  if (num_rows) *num_rows = g->num_rows;
+  if (num_cols) *num_cols = g->num_cols;
+  if (num_edges) *num_edges = g->m;
+  if (num_long_rows) *num_long_rows = g->num_long;
+  return GSPMM_OK;
+}
+
+int gspmm_graph_device_csr(gspmm_graph g, const uint32_t** indptr,
+                           const uint32_t** indices, const uint32_t** edge_ids) {
+  if (!g) return fail(GSPMM_ERR_ARG, "null graph handle");
+  if (indptr) *indptr = g->d_indptr;
+  if (indices) *indices = g->d_indices;
+  if (edge_ids) *edge_ids = g->d_eids;
+  return GSPMM_OK;
+}
+
+int gspmm_graph_permute_edges(gspmm_graph g, const float* src_by_id, int64_t dim,
+                              int64_t src_ld, float* dst_by_pos, int64_t dst_ld,
+                              void* stream) {
+  if (!g || !src_by_id || !dst_by_pos) return fail(GSPMM_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(g->device), "cudaSetDevice");
+  CUDA_TRY(launch_permute_edges(g->d_eids, g->m, src_by_id, dim, src_ld ? src_ld : dim,
+                                dst_by_pos, dst_ld ? dst_ld : dim,
+                                static_cast<cudaStream_t>(stream)),
+           "permute_edges");
+  return GSPMM_OK;
+}
+
+int gspmm_out_shape(gspmm_graph g, const gspmm_config* cfg, const gspmm_mat* u,
+                    const gspmm_mat* v, const gspmm_mat* e,
+                    const gspmm_options* opt, int64_t* rows, int64_t* dim) {
+  Bound b;
+  const int st = bind(g, cfg, u, v, e, nullptr, opt, &b);
+  if (st) return st;
+  if (rows) *rows = b.out_rows;
+  if (dim) *dim = b.width;
+  return GSPMM_OK;
+}
+
+int gspmm_binary_reduce_ex(gspmm_graph g, const gspmm_config* cfg,
+                           const gspmm_mat* u, const gspmm_mat* v,
+                           const gspmm_mat* e, const gspmm_out* out,
+                           const gspmm_options* opt, void* stream) {
+  Bound b;
+  int st = bind(g, cfg, u, v, e, out, opt, &b);
+  if (st) return st;
+  if (!out) return fail(GSPMM_ERR_SHAPE, "missing output matrix");
+  CUDA_TRY(cudaSetDevice(g->device), "cudaSetDevice");
+  return launch(g, b, stream);
+}
+
+int gspmm_binary_reduce(gspmm_graph g, const gspmm_config* cfg,
+                        const gspmm_mat* u, const gspmm_mat* v,
+                        const gspmm_mat* e, const gspmm_out* out, void* stream) {
+  return gspmm_binary_reduce_ex(g, cfg, u, v, e, out, nullptr, stream);
+}
+
+// copy_reduce, kernels.cpp:503-524
+int gspmm_copy_reduce(gspmm_graph g, const gspmm_mat* src, int reduce,
+                      const gspmm_out* out, void* stream) {
+  if (!g || !src) return fail(GSPMM_ERR_ARG, "null argument");
+  gspmm_config cfg{GSPMM_U, GSPMM_NONE, GSPMM_COPY, reduce, GSPMM_V};
+  const bool src_major = g->orientation == GSPMM_SRC_MAJOR;
+  const int64_t nu = src_major ? g->num_rows : g->num_cols;
+  if (src->rows == nu) {
+    cfg.lhs = GSPMM_U;
+    return gspmm_binary_reduce(g, &cfg, src, nullptr, nullptr, out, stream);
+  }
+  if (src->rows == static_cast<int64_t>(g->m)) {
+    cfg.lhs = GSPMM_E;
+    return gspmm_binary_reduce(g, &cfg, nullptr, nullptr, src, out, stream);
+  }
+  return fail(GSPMM_ERR_SHAPE, "copy_reduce: source rows match neither the node nor the edge count");
+}
+
+int gspmm_argmax_backward(const int32_t* arg, int64_t rows, int64_t dim,
+                          int64_t arg_ld, const float* grad_out, int64_t grad_ld,
+                          float* grad_src, int64_t src_rows, int64_t src_ld,
+                          void* stream) {
+  if (!arg || !grad_out || !grad_src) return fail(GSPMM_ERR_ARG, "null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* acc = nullptr;
+  const size_t bytes = sizeof(double) * std::max<int64_t>(src_rows * dim, 1);
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&acc), bytes, s), "argmax workspace");
+  cudaError_t e = launch_argmax_backward(arg, rows, dim, arg_ld ? arg_ld : dim, grad_out,
+                                         grad_ld ? grad_ld : dim, grad_src, src_rows,
+                                         src_ld ? src_ld : dim, acc, s);
+  cudaFreeAsync(acc, s);
+  if (e != cudaSuccess) return cuda_fail(e, "argmax_backward");
+  return GSPMM_OK;
+}
+
+int gspmm_binary_reduce_host(gspmm_graph g, const gspmm_config* cfg,
+                             const gspmm_mat* u, const gspmm_mat* v,
+                             const gspmm_mat* e, const gspmm_out* out,
+                             const gspmm_options* opt, void* stream) {
+  if (!g || !out) return fail(GSPMM_ERR_ARG, "null argument");
+  // Validate against the host views first (shapes only; no pointer use).
+  Bound probe;
+  int st = bind(g, cfg, u, v, e, out, opt, &probe);
+  if (st) return st;
+  if (opt && opt->other_scale)
+    return fail(GSPMM_ERR_ARG, "other_scale is a device-side option");
+  std::lock_guard<std::mutex> lock(g->mu);
+  CUDA_TRY(cudaSetDevice(g->device), "cudaSetDevice");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const gspmm_mat* in[3] = {u, v, e};
+  size_t sz[3], total = 0;
+  for (int i = 0; i < 3; ++i) total += round_up(sz[i] = mat_bytes(in[i]));
+  const int64_t out_ld = out->ld ? out->ld : out->dim;
+  const size_t out_bytes =
+      out->rows ? static_cast<size_t>((out->rows - 1) * out_ld + out->dim) * sizeof(float) : 0;
+  total += round_up(out_bytes);
+  const int64_t arg_ld = opt && opt->arg_ld ? opt->arg_ld : out->dim;
+  const size_t arg_bytes =
+      out->rows ? static_cast<size_t>((out->rows - 1) * arg_ld + out->dim) * sizeof(int32_t) : 0;
+  const bool ao = opt && opt->arg_other, ae = opt && opt->arg_edge;
+  total += (ao ? round_up(arg_bytes) : 0) + (ae ? round_up(arg_bytes) : 0);
+  if (total > g->ws_bytes) {
+    cudaFree(g->ws);
+    g->ws = nullptr;
+    g->ws_bytes = 0;
+    CUDA_TRY(cudaMalloc(&g->ws, total), "workspace");
+    g->ws_bytes = total;
+  }
+  char* p = static_cast<char*>(g->ws);
+  gspmm_mat dev[3];
+  const gspmm_mat* dptr[3] = {nullptr, nullptr, nullptr};
+  for (int i = 0; i < 3; ++i) {
+    if (!in[i] || !in[i]->data) continue;
+    dev[i] = *in[i];
+    dev[i].data = reinterpret_cast<const float*>(p);
+    CUDA_TRY(cudaMemcpyAsync(p, in[i]->data, sz[i], cudaMemcpyHostToDevice, s), "H2D operand");
+    dptr[i] = &dev[i];
+    p += round_up(sz[i]);
+  }
+  gspmm_out dout = *out;
+  dout.data = reinterpret_cast<float*>(p);
+  p += round_up(out_bytes);
+  gspmm_options dopt{};
+  if (opt) dopt = *opt;
+  if (ao) {
+    dopt.arg_other = reinterpret_cast<int32_t*>(p);
+    p += round_up(arg_bytes);
+  }
+  if (ae) {
+    dopt.arg_edge = reinterpret_cast<int32_t*>(p);
+    p += round_up(arg_bytes);
+  }
+  st = gspmm_binary_reduce_ex(g, cfg, dptr[0], dptr[1], dptr[2], &dout, &dopt, stream);
+  if (st) return st;
+  CUDA_TRY(cudaMemcpyAsync(out->data, dout.data, out_bytes, cudaMemcpyDeviceToHost, s), "D2H out");
+  if (ao)
+    CUDA_TRY(cudaMemcpyAsync(opt->arg_other, dopt.arg_other, arg_bytes, cudaMemcpyDeviceToHost, s),
+             "D2H arg");
+  if (ae)
+    CUDA_TRY(cudaMemcpyAsync(opt->arg_edge, dopt.arg_edge, arg_bytes, cudaMemcpyDeviceToHost, s),
+             "D2H arg");
+  CUDA_TRY(cudaStreamSynchronize(s), "synchronize");
+  return GSPMM_OK;
+}
+
+}  // extern "C"

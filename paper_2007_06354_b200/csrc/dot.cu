@@ -1,0 +1,155 @@
+// dot.cu -- Binary-Reduce with the Dot operator (u_dot_v_*, SDDMM-style
+// edge scores and the grad of edge weights / attention), sm_100a.
+//
+// The reference computes each dot as a sequential fp32 left fold over the
+// feature columns, product rounded then added (apply_dot, kernels.cpp:91-97,
+// and the oracle's message(), oracle.cpp:49-56), and its own tests demand
+// bit-equality for the edge-destined configs (CopyLast is an "exact" reduce,
+// compare.hpp:58-61; test_kernels.cpp:218).  A warp-shuffle tree would be
+// faster to write but not bit-exact, so the kernel transposes through
+// shared memory instead:
+//   * a warp owns one destination row and walks its edges 32 at a time;
+//   * for each 32*V-column chunk, the 32 lanes gather the chunk of both
+//     operands for one edge at a time with coalesced vector loads, multiply
+//     (rounded) and park the products in a per-warp shared tile laid out so
+//     that both the writes and the per-edge reads are bank-conflict free;
+//   * lane k then folds edge k's products in column order, carrying its
+//     accumulator across chunks and emitting one value per head (multi-head
+//     grad_a: `heads` dots of gather_dim/heads columns each).
+// Edge outputs are stored by edge id; node outputs fold the 32 per-edge
+// dots in canonical order with the row's reducer.
+#include "device_ops.cuh"
+
+namespace gspmm_b200 {
+namespace {
+
+constexpr int kDotWarps = 4;
+
+template <int V, int ROP>
+__global__ void __launch_bounds__(kDotWarps * 32) k_dot(const RowLaunch p) {
+  constexpr int kCW = 32 * V;       // columns per chunk
+  constexpr int kStride = kCW + 1;  // padded tile row
+  extern __shared__ float smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  float* tile = smem + warp * 32 * kStride;
+
+  const int64_t r64 = static_cast<int64_t>(blockIdx.x) * kDotWarps + warp;
+  if (r64 >= p.num_rows) return;
+  const uint32_t r = static_cast<uint32_t>(r64);
+  const uint32_t beg = __ldg(p.indptr + r), end = __ldg(p.indptr + r + 1);
+  const int G = p.gather_dim;
+  const int D = G / p.heads;
+  const bool need_eid = p.out_edge || p.lhs.role == ROLE_EID || p.rhs.role == ROLE_EID;
+
+  float racc = red_identity<ROP>();  // node outputs (heads == 1)
+
+  for (uint32_t jb = beg; jb < end; jb += 32) {
+    const int n = min(32u, end - jb);
+    const uint32_t jl = jb + lane;
+    uint32_t my_other = 0, my_eid = 0;
+    if (lane < n) {
+      my_other = __ldg(p.indices + jl);
+      if (need_eid) my_eid = __ldg(p.eids + jl);
+    }
+    float acc = 0.0f;
+    int head = 0;
+    for (int cb = 0; cb < G; cb += kCW) {
+      const int c0 = cb + lane * V;
+      // Gather + multiply: edge i's chunk lands in tile row i.
+      for (int i0 = 0; i0 < n; i0 += 8) {
+        float lv[8][V], rv[8][V];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int i = i0 + k;
+          const uint32_t o = __shfl_sync(kFull, my_other, i & 31);
+          const uint32_t e = need_eid ? __shfl_sync(kFull, my_eid, i & 31) : 0u;
+          if (i < n && c0 < G) {
+            const uint32_t j = jb + i;
+            load_operand<V>(p.lhs, operand_row(p.lhs.role, r, o, e, j), c0, lv[k]);
+            load_operand<V>(p.rhs, operand_row(p.rhs.role, r, o, e, j), c0, rv[k]);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int i = i0 + k;
+          if (i < n) {
+#pragma unroll
+            for (int t = 0; t < V; ++t)
+              tile[i * kStride + t * 32 + lane] =
+                  c0 + t < G ? __fmul_rn(lv[k][t], rv[k][t]) : 0.0f;
+          }
+        }
+      }
+      __syncwarp();
+      // Sequential fold of edge `lane` over the chunk's columns.
+      if (lane < n) {
+        const int cend = min(kCW, G - cb);
+        for (int c = 0; c < cend; ++c) {
+          acc = __fadd_rn(acc, tile[lane * kStride + (c % V) * 32 + c / V]);
+          if ((cb + c + 1) % D == 0) {
+            if (p.out_edge) {
+              p.out[static_cast<int64_t>(my_eid) * p.out_ld + head] = acc;
+            } else {
+              tile[lane * kStride + kCW] = acc;  // heads == 1: parked in the pad column
+            }
+            acc = 0.0f;
+            ++head;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (!p.out_edge) {
+      // Fold this chunk's per-edge dots in canonical order.
+      const float dv = lane < n ? tile[lane * kStride + kCW] : 0.0f;
+      for (int k = 0; k < n; ++k) racc = red_combine<ROP>(racc, __shfl_sync(kFull, dv, k));
+      __syncwarp();
+    }
+  }
+  if (!p.out_edge && lane == 0) {
+    const uint32_t deg = end - beg;
+    if ((ROP == R_MAX || ROP == R_MIN) && deg == 0) racc = 0.0f;
+    if (p.mean) racc = deg ? __fdiv_rn(racc, __uint2float_rn(deg)) : 0.0f;
+    p.out[static_cast<int64_t>(r) * p.out_ld] = racc;
+  }
+}
+
+template <int V, int ROP>
+cudaError_t launch_dv(const RowLaunch& p, cudaStream_t s) {
+  const size_t smem = sizeof(float) * kDotWarps * 32 * (32 * V + 1);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_dot<V, ROP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    attr_set = true;
+  }
+  const int64_t blocks = (static_cast<int64_t>(p.num_rows) + kDotWarps - 1) / kDotWarps;
+  if (blocks == 0) return cudaSuccess;
+  k_dot<V, ROP><<<static_cast<unsigned>(blocks), kDotWarps * 32, smem, s>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <int V>
+cudaError_t launch_dr(const RowLaunch& p, cudaStream_t s) {
+  switch (p.reduce) {
+    case R_SUM: return launch_dv<V, R_SUM>(p, s);
+    case R_MAX: return launch_dv<V, R_MAX>(p, s);
+    case R_MIN: return launch_dv<V, R_MIN>(p, s);
+    case R_PROD: return launch_dv<V, R_PROD>(p, s);
+    default: return launch_dv<V, R_LAST>(p, s);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_dot(const RowLaunch& p, cudaStream_t s) {
+  switch (p.vec) {
+    case 4: return launch_dr<4>(p, s);
+    case 2: return launch_dr<2>(p, s);
+    default: return launch_dr<1>(p, s);
+  }
+}
+
+}  // namespace gspmm_b200

@@ -1,0 +1,82 @@
+// internal.h -- launch descriptors shared by the C-ABI layer (capi.cpp) and
+// the sm_100a kernels (*.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gspmm_b200 {
+
+// Which endpoint of an edge an operand row is taken from, resolved by the
+// host from (operand entity, graph orientation) -- the reference's
+// OperandRef::row (kernels.cpp:120-125) split_endpoints (:138-147).
+enum Role : int32_t {
+  ROLE_ROW = 0,    // the owner row itself (constant across the row's edges)
+  ROLE_OTHER = 1,  // indices[j]: the gathered neighbour
+  ROLE_EID = 2,    // edge_ids[j]: an edge operand in edge-id order
+  ROLE_POS = 3     // j: an edge operand pre-permuted to CSR position order
+};
+
+// How an operand's elements map onto the output columns.
+enum Mode : int32_t {
+  MODE_FULL = 0,    // column c reads element c
+  MODE_SCALAR = 1,  // width-1 broadcast, stride 0 (kernels.cpp:451-453)
+  MODE_HEAD = 2     // width-H broadcast over groups of `group` columns
+};
+
+struct OperandDesc {
+  const float* base = nullptr;
+  int64_t ld = 0;
+  int32_t role = ROLE_OTHER;
+  int32_t mode = MODE_FULL;
+  int32_t group = 1;
+};
+
+enum BinOp : int32_t { B_ADD = 0, B_SUB = 1, B_MUL = 2, B_DIV = 3, B_DOT = 4, B_COPY = 5 };
+enum RedOp : int32_t { R_SUM = 0, R_MAX = 1, R_MIN = 2, R_PROD = 3, R_LAST = 4 };
+
+struct RowLaunch {
+  const uint32_t* indptr = nullptr;
+  const uint32_t* indices = nullptr;
+  const uint32_t* eids = nullptr;
+  uint32_t num_rows = 0;
+  OperandDesc lhs, rhs;  // rhs.base == nullptr for the copy operator
+  int32_t binop = B_COPY;
+  int32_t reduce = R_SUM;
+  bool mean = false;       // divide by the row degree (0 for empty rows)
+  bool out_edge = false;   // out == E: store per edge (row = edge id)
+  float* out = nullptr;
+  int64_t out_ld = 0;
+  int32_t width = 0;       // output width W
+  int32_t gather_dim = 0;  // dot: reduced length
+  int32_t heads = 1;       // dot: per-head products
+  int32_t* arg_other = nullptr;
+  int32_t* arg_edge = nullptr;
+  int64_t arg_ld = 0;
+  const float* other_scale = nullptr;
+  int32_t vec = 4;         // vector width chosen by the host (4, 2, 1)
+  // degree plan: rows whose degree exceeds long_threshold are listed in
+  // long_rows (descending degree) and processed first.
+  const uint32_t* long_rows = nullptr;
+  uint32_t num_long = 0;
+  uint32_t long_threshold = 0xffffffffu;
+  int num_sms = 148;
+};
+
+// Kernel launchers (rows.cu, dot.cu, aux.cu).  Return cudaGetLastError().
+cudaError_t launch_rows(const RowLaunch& p, cudaStream_t s);
+cudaError_t launch_dot(const RowLaunch& p, cudaStream_t s);
+cudaError_t launch_permute_edges(const uint32_t* eids, uint64_t m,
+                                 const float* src, int64_t dim, int64_t src_ld,
+                                 float* dst, int64_t dst_ld, cudaStream_t s);
+cudaError_t launch_argmax_backward(const int32_t* arg, int64_t rows,
+                                   int64_t dim, int64_t arg_ld,
+                                   const float* grad_out, int64_t grad_ld,
+                                   float* grad_src, int64_t src_rows,
+                                   int64_t src_ld, double* acc,
+                                   cudaStream_t s);
+
+// Launch counter (evidence of native execution), bumped by each launcher.
+void note_launch(uint64_t n = 1);
+
+}  // namespace gspmm_b200

@@ -1,0 +1,369 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the pinned
+oracle on identical seeded inputs.
+
+The bar is BIT-EXACTNESS for every op, sums included: the kernels fold each
+output element sequentially in canonical edge order with separately rounded
+products and sums, exactly like the reference's RowParallelSpmm
+(kernels.cpp:162-195), which the oracle restates and the golden fixtures pin.
+The reference's own looser criterion (max_rel_error <= 1e-5 against the f64
+oracle_aggregate, compare.hpp:30-45) is checked as well.
+"""
+import numpy as np
+import pytest
+
+from gspmm_testutil import HAS_GPU
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+if HAS_GPU:
+    import torch
+
+    import paper_2007_06354_b200 as P
+
+SUM_TOL = 1e-5  # reference acceptance tolerance for sum-like reduces
+
+
+def dev_graph(g, orientation):
+    """Device handle for one orientation of an oracle Graph (cached)."""
+    cache = g.__dict__.setdefault("_dev", {})
+    if orientation not in cache:
+        ip, ix, ei = g.csr(orientation)
+        cache[orientation] = P.Graph(ip, ix, ei, g.n, g.n, orientation, validate=True)
+    return cache[orientation]
+
+
+def cuda(a):
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, np.float32)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    return torch.from_numpy(a).cuda()
+
+
+def gpu_reduce(g, cfg, u=None, v=None, e=None, **kw):
+    orientation = O.SRC_MAJOR if cfg[4] == O.U else O.DST_MAJOR
+    h = dev_graph(g, orientation)
+    res = P.binary_reduce(h, cfg, cuda(u), cuda(v), cuda(e), **kw)
+    torch.cuda.synchronize()
+    if isinstance(res, tuple):
+        return tuple(None if r is None else r.cpu().numpy() for r in res)
+    return res.cpu().numpy()
+
+
+def g_of(n, edges):
+    return O.Graph(n, np.array([e[0] for e in edges], np.uint32),
+                   np.array([e[1] for e in edges], np.uint32))
+
+
+# ------------------------------- goldens of proj/tests/test_kernels.cpp
+def test_goldens_from_reference_tests():
+    g = g_of(3, [(0, 2), (1, 2)])
+    assert gpu_reduce(g, O.named_config("u_copy_add_v"), u=[[1, 2], [3, 4], [0, 0]]).tolist() == \
+        [[0, 0], [0, 0], [4, 6]]                                           # :49-66
+    g = g_of(2, [(0, 1)])
+    assert gpu_reduce(g, O.named_config("u_copy_add_v"), u=[[5, -3], [9, 9]]).tolist() == \
+        [[0, 0], [5, -3]]                                                  # :68-78
+    g3 = g_of(3, [(0, 1), (2, 1)])
+    assert gpu_reduce(g3, O.named_config("u_copy_max_v"), u=[[5], [-7], [2]])[:, 0].tolist() == \
+        [0, 5, 0]                                                          # :80-90
+    assert gpu_reduce(g, O.named_config("u_mul_e_add_v"), u=[[2, 3], [0, 0]],
+                      e=[[10, 10]])[1].tolist() == [20, 30]                # :92-103
+    out = gpu_reduce(g, O.named_config("u_dot_v_add_e"), u=[[1, 2], [0, 0]], v=[[0, 0], [3, 4]])
+    assert out.shape == (1, 1) and out[0, 0] == 11                         # :105-116
+    assert gpu_reduce(g, O.named_config("u_add_v_copy_e"), u=[[1], [0]],
+                      v=[[0], [5]])[0, 0] == 6                             # :118-127
+    gd = g_of(2, [(0, 1), (0, 1)])
+    assert gpu_reduce(gd, O.named_config("e_copy_max_v"), e=[[3], [7]])[1, 0] == 7  # :129-137
+    gc = g_of(3, [(2, 1), (0, 1)])                                         # test_oracle.cpp:64-73
+    assert gpu_reduce(gc, O.named_config("u_copy_copy_v"), u=[[10], [0], [99]])[1, 0] == 99
+
+
+def test_empty_graph_all_zero():  # test_kernels.cpp:190-200
+    g = O.Graph(4, np.array([], np.uint32), np.array([], np.uint32))
+    for name in ("u_copy_add_v", "u_copy_max_v"):
+        assert (gpu_reduce(g, O.named_config(name), u=np.ones((4, 3))) == 0).all()
+
+
+def test_copy_reduce_infers_entity():  # test_kernels.cpp:176-188
+    g = g_of(3, [(0, 2), (1, 2)])
+    h = dev_graph(g, O.DST_MAJOR)
+    out = P.copy_reduce(h, cuda([[1], [10]]), P.SUM)
+    assert out.cpu().numpy()[2, 0] == 11
+    with pytest.raises(P.ShapeError):
+        P.copy_reduce(h, cuda(np.zeros((5, 1))), P.SUM)
+
+
+def test_validation_errors():  # test_kernels.cpp:139-174
+    g = g_of(2, [(0, 1)])
+    cfg = O.named_config("u_copy_add_v")
+    with pytest.raises(P.ShapeError):  # wrong orientation for the output
+        P.binary_reduce(dev_graph(g, O.SRC_MAJOR), cfg, cuda(np.zeros((2, 4))))
+    h = dev_graph(g, O.DST_MAJOR)
+    with pytest.raises(P.ShapeError):  # missing operand
+        P.binary_reduce(h, cfg)
+    with pytest.raises(P.ShapeError):  # row mismatch
+        P.binary_reduce(h, cfg, cuda(np.zeros((3, 4))))
+    with pytest.raises(P.ShapeError):  # incompatible widths
+        P.binary_reduce(h, O.named_config("u_add_v_add_v"), cuda(np.zeros((2, 4))),
+                        cuda(np.zeros((2, 3))))
+    with pytest.raises(P.ConfigError):
+        P.binary_reduce(h, (O.U, O.U, O.MUL, O.SUM, O.V), cuda(np.zeros((2, 4))))
+
+
+def test_degree_identity():  # test_kernels.cpp:339-352
+    n, src, dst = O.random_small_graph(190)
+    g = O.Graph(n, src, dst)
+    out = gpu_reduce(g, O.named_config("u_copy_add_v"), u=np.ones((n, 1)))
+    assert (out[:, 0] == np.bincount(dst, minlength=n)).all()
+
+
+# ------------------------------------------- reference fixtures, bitwise
+@pytest.mark.parametrize("seed", (101, 104, 107))
+def test_reference_fixtures_bit_exact(golden, seed):
+    p = f"s{seed}_"
+    n = int(golden[p + "n"][0])
+    g = O.Graph(n, golden[p + "src"], golden[p + "dst"])
+    fu, fv, fe = golden[p + "fu"], golden[p + "fv"], golden[p + "fe"]
+    for cname in O.APPLICATION_CONFIGS:
+        cfg = O.named_config(cname)
+        got = gpu_reduce(g, cfg, fu, fv, fe)
+        assert O.bit_equal(got, golden[p + "spmm_" + cname]), cname
+        if cfg[4] != O.E:
+            want = golden[p + "oracle_" + cname]
+            if O.is_exact_reduce(cfg[3]):
+                assert O.bit_equal(got, want), cname
+            else:
+                assert O.max_rel_error(got, want) <= SUM_TOL, cname
+
+
+def test_composed_fixtures_bit_exact(golden):
+    n = int(golden["c_n"][0])
+    g = O.Graph(n, golden["c_src"], golden["c_dst"])
+    x, w, gy, a = golden["c_x"], golden["c_w"], golden["c_gy"], golden["c_att"]
+    assert O.bit_equal(gpu_reduce(g, (O.U, O.E, O.MUL, O.SUM, O.V), u=x, e=w), golden["c_gcn_fwd"])
+    assert O.bit_equal(gpu_reduce(g, (O.V, O.E, O.MUL, O.SUM, O.U), v=gy, e=w), golden["c_gcn_bwd"])
+    assert O.bit_equal(gpu_reduce(g, (O.U, O.V, O.DOT, O.LAST, O.E), u=x, v=gy), golden["c_grad_w"])
+    assert O.bit_equal(gpu_reduce(g, (O.U, O.NONE, O.COPY, P.MEAN, O.V), u=x), golden["c_mean"])
+    assert O.bit_equal(gpu_reduce(g, (O.U, O.NONE, O.COPY, O.MAX, O.V), u=x), golden["c_max"])
+    assert O.bit_equal(gpu_reduce(g, (O.U, O.E, O.MUL, O.SUM, O.V), u=x, e=a, heads=4),
+                       golden["c_mh_fwd"])
+
+
+# ------------------------------------- properties over random graphs
+EXTRA = ["u_copy_max_v", "u_copy_min_v", "u_copy_mul_v", "u_copy_copy_v", "u_sub_v_add_v",
+         "u_div_e_max_v", "e_mul_u_min_v", "v_add_e_add_v", "u_mul_v_mul_v", "e_copy_copy_v",
+         "u_sub_e_copy_e", "u_dot_e_add_v", "v_dot_u_max_v"]
+
+
+@pytest.mark.parametrize("seed", range(101, 141))
+def test_all_configs_bit_exact_vs_oracle(seed):  # test_kernels.cpp:202-226
+    n, src, dst = O.random_small_graph(seed)
+    g = O.Graph(n, src, dst)
+    dim = 1 + O.splitmix64_at(seed, 1) % 17
+    fu = O.random_features(n, dim, seed)
+    fv = O.random_features(n, dim, seed + 1)
+    fe = O.random_features(g.m, dim, seed + 2)
+    for cname in O.APPLICATION_CONFIGS + EXTRA:
+        cfg = O.named_config(cname)
+        want = O.binary_reduce(g, cfg, fu, fv, fe)
+        got = gpu_reduce(g, cfg, fu, fv, fe)
+        assert O.bit_equal(got, want), f"{cname} seed {seed}"
+
+
+@pytest.mark.parametrize("seed", range(130, 135))
+def test_scalar_edge_broadcast(seed):  # test_kernels.cpp:228-241
+    n, src, dst = O.random_small_graph(seed)
+    g = O.Graph(n, src, dst)
+    fu = O.random_features(n, 9, seed)
+    fe = O.random_features(g.m, 1, seed + 2)
+    cfg = O.named_config("u_mul_e_add_v")
+    got = gpu_reduce(g, cfg, u=fu, e=fe)
+    assert O.bit_equal(got, O.binary_reduce(g, cfg, u=fu, e=fe))
+    assert O.max_rel_error(got, O.oracle_aggregate(g, cfg, u=fu, e=fe)) <= SUM_TOL
+
+
+@pytest.mark.parametrize("seed", range(150, 154))
+def test_source_destined(seed):  # test_kernels.cpp:261-276
+    n, src, dst = O.random_small_graph(seed)
+    g = O.Graph(n, src, dst)
+    fu = O.random_features(n, 4, seed)
+    fv = O.random_features(n, 4, seed + 1)
+    cfg = (O.U, O.V, O.MUL, O.SUM, O.U)
+    got = gpu_reduce(g, cfg, u=fu, v=fv)
+    assert O.bit_equal(got, O.binary_reduce(g, cfg, u=fu, v=fv))
+    assert O.max_rel_error(got, O.oracle_aggregate(g, cfg, u=fu, v=fv)) <= SUM_TOL
+
+
+def test_linearity():  # test_kernels.cpp:323-337
+    n, src, dst = O.random_small_graph(180)
+    g = O.Graph(n, src, dst)
+    fu = O.random_features(n, 6, 180)
+    cfg = O.named_config("u_copy_add_v")
+    base = gpu_reduce(g, cfg, u=fu)
+    scaled = gpu_reduce(g, cfg, u=fu * np.float32(3))
+    assert O.max_rel_error(scaled, base * np.float32(3)) <= SUM_TOL
+
+
+def test_deterministic_repeats():  # max bit-identical across runs (cf. :308-321)
+    n, src, dst = O.random_small_graph(170)
+    g = O.Graph(n, src, dst)
+    fu = O.random_features(n, 8, 170)
+    for name in ("u_copy_max_v", "u_copy_add_v"):
+        a = gpu_reduce(g, O.named_config(name), u=fu)
+        for _ in range(3):
+            assert O.bit_equal(a, gpu_reduce(g, O.named_config(name), u=fu))
+
+
+# ------------------------------------------------ layouts and widths
+@pytest.mark.parametrize("dim", [1, 2, 3, 4, 5, 7, 8, 31, 33, 64, 100, 127, 128, 129, 256, 300,
+                                 512, 602])
+def test_widths_bit_exact(dim):
+    src, dst = O.gen_rmat(3000, 40000, seed=dim)
+    g = O.Graph(3000, src, dst)
+    x = O.normal_features(3000, dim, dim)
+    w = O.gcn_weights(3000, src, dst)
+    fe = O.random_features(g.m, dim, 5)
+    for cfg, kw in (((O.U, O.E, O.MUL, O.SUM, O.V), dict(u=x, e=w)),
+                    ((O.U, O.E, O.SUB, O.MAX, O.V), dict(u=x, e=fe)),
+                    ((O.U, O.NONE, O.COPY, O.SUM, O.V), dict(u=x)),
+                    ((O.V, O.E, O.MUL, O.SUM, O.U), dict(v=x, e=w)),
+                    ((O.U, O.V, O.DOT, O.LAST, O.E), dict(u=x, v=x))):
+        assert O.bit_equal(gpu_reduce(g, cfg, **kw), O.binary_reduce(g, cfg, **kw)), (dim, cfg)
+
+
+def test_padded_leading_dimension():
+    # F=602 rows are not 16-byte aligned; a padded device ld=604 takes the
+    # float4 path.  Results must not depend on the layout.
+    src, dst = O.gen_rmat(2000, 30000, seed=3)
+    g = O.Graph(2000, src, dst)
+    x = O.normal_features(2000, 602, 1)
+    want = O.mean(g, x)
+    h = dev_graph(g, O.DST_MAJOR)
+    xp = torch.zeros((2000, 604), dtype=torch.float32, device="cuda")
+    xp[:, :602] = cuda(x)
+    outp = torch.full((2000, 604), 7.0, device="cuda")
+    P.binary_reduce(h, (O.U, O.NONE, O.COPY, P.MEAN, O.V), xp[:, :602], out=outp[:, :602])
+    torch.cuda.synchronize()
+    assert O.bit_equal(outp[:, :602].cpu().numpy(), want)
+    assert (outp[:, 602:] == 7.0).all()  # padding untouched
+    out = P.binary_reduce(h, (O.U, O.NONE, O.COPY, P.MEAN, O.V), cuda(x))
+    assert O.bit_equal(out.cpu().numpy(), want)
+
+
+def test_edge_operand_in_csr_order():
+    src, dst = O.gen_rmat(2000, 30000, seed=4)
+    g = O.Graph(2000, src, dst)
+    x = O.normal_features(2000, 64, 1)
+    w = O.gcn_weights(2000, src, dst)
+    want = O.binary_reduce(g, (O.U, O.E, O.MUL, O.SUM, O.V), u=x, e=w)
+    for orientation, cfg, kw in ((O.DST_MAJOR, (O.U, O.E, O.MUL, O.SUM, O.V), "u"),
+                                 (O.SRC_MAJOR, (O.V, O.E, O.MUL, O.SUM, O.U), "v")):
+        h = dev_graph(g, orientation)
+        wp = h.permute_edges(cuda(w))
+        args = {kw: cuda(x), "e": wp}
+        got = P.binary_reduce(h, cfg, e_order=P.EDGE_BY_POS, **args).cpu().numpy()
+        ref = O.binary_reduce(g, cfg, **{kw: x, "e": w})
+        assert O.bit_equal(got, ref)
+    assert O.bit_equal(gpu_reduce(g, (O.U, O.E, O.MUL, O.SUM, O.V), u=x, e=w), want)
+
+
+def test_host_entry_matches_device_entry():
+    src, dst = O.gen_rmat(1500, 20000, seed=6)
+    g = O.Graph(1500, src, dst)
+    x = O.normal_features(1500, 48, 1)
+    w = O.gcn_weights(1500, src, dst)
+    h = dev_graph(g, O.DST_MAJOR)
+    cfg = (O.U, O.E, O.MUL, O.SUM, O.V)
+    host = P.binary_reduce_host(h, cfg, u=x, e=w)
+    assert O.bit_equal(host, O.binary_reduce(g, cfg, u=x, e=w))
+    val, au, ae = P.binary_reduce_host(h, (O.U, O.NONE, O.COPY, O.MAX, O.V), u=x,
+                                       want_arg_other=True, want_arg_edge=True)
+    v2, au2, ae2 = O.copy_max_argmax(g, x)
+    assert O.bit_equal(val, v2) and (au == au2).all() and (ae == ae2).all()
+
+
+# ------------------------------------------- extensions
+@pytest.mark.parametrize("seed", range(5))
+def test_mean_and_mean_backward(seed):
+    src, dst = O.gen_rmat(4000, 60000, seed=seed)
+    g = O.Graph(4000, src, dst)
+    x = O.random_features(4000, 100, seed)
+    gy = O.normal_features(4000, 100, seed + 3)
+    assert O.bit_equal(gpu_reduce(g, (O.U, O.NONE, O.COPY, P.MEAN, O.V), u=x), O.mean(g, x))
+    # backward: v_copy_add_u scaled by 1/deg_in(v) of the gathered node
+    deg = O.in_degree(g)
+    inv = np.zeros(4000, np.float32)
+    inv[deg > 0] = np.float32(1) / deg[deg > 0].astype(np.float32)
+    h = dev_graph(g, O.SRC_MAJOR)
+    got = P.binary_reduce(h, (O.V, O.NONE, O.COPY, O.SUM, O.U), v=cuda(gy),
+                          other_scale=torch.from_numpy(inv).cuda()).cpu().numpy()
+    assert O.bit_equal(got, O.mean_backward(g, gy))
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_max_argmax_and_backward(seed):
+    src, dst = O.gen_rmat(3000, 50000, seed=seed)
+    src, dst = O.symmetrize(src, dst)
+    g = O.Graph(3000, src, dst)
+    # few distinct values: ties between different sources and duplicate edges
+    x = np.round(O.random_features(3000, 100, seed) * 4) / 4
+    val, au, ae = gpu_reduce(g, (O.U, O.NONE, O.COPY, O.MAX, O.V), u=x, want_arg_other=True,
+                             want_arg_edge=True)
+    v2, au2, ae2 = O.copy_max_argmax(g, x)
+    assert O.bit_equal(val, v2)
+    assert O.bit_equal(val, O.binary_reduce(g, O.named_config("u_copy_max_v"), u=x))
+    assert (au == au2).all() and (ae == ae2).all()
+    gy = O.normal_features(3000, 100, seed + 3)
+    grad = P.argmax_backward(torch.from_numpy(au).cuda(), cuda(gy), 3000).cpu().numpy()
+    want = O.argmax_backward(au2, gy, 3000)
+    assert O.max_rel_error(grad, want) <= 1e-6
+    # min + argmin
+    val, au, _ = gpu_reduce(g, (O.U, O.NONE, O.COPY, O.MIN, O.V), u=x, want_arg_other=True)
+    assert O.bit_equal(val, O.binary_reduce(g, O.named_config("u_copy_min_v"), u=x))
+
+
+def test_argmax_over_edge_features():
+    src, dst = O.gen_rmat(500, 8000, seed=2)
+    g = O.Graph(500, src, dst)
+    fe = np.round(O.random_features(g.m, 16, 3) * 3) / 3
+    val, au, ae = gpu_reduce(g, (O.E, O.NONE, O.COPY, O.MAX, O.V), e=fe, want_arg_other=True,
+                             want_arg_edge=True)
+    v2, au2, ae2 = O.copy_max_argmax(g, fe, lhs=O.E)
+    assert O.bit_equal(val, v2) and (au == au2).all() and (ae == ae2).all()
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_multihead_forward_backward(seed):
+    heads, d = 8, 64
+    src, dst = O.gen_rmat(2000, 40000, seed=seed)
+    g = O.Graph(2000, src, dst)
+    x = O.normal_features(2000, heads * d, seed)
+    a = O.softmax_attention(2000, dst, O.normal_features(g.m, heads, seed + 2))
+    gy = O.normal_features(2000, heads * d, seed + 3)
+    fwd = gpu_reduce(g, (O.U, O.E, O.MUL, O.SUM, O.V), u=x, e=a, heads=heads)
+    assert O.bit_equal(fwd, O.multihead_u_mul_e_sum(g, x, a, heads))
+    gx_want, ga_want = O.multihead_backward(g, x, a, gy, heads)
+    gx = gpu_reduce(g, (O.V, O.E, O.MUL, O.SUM, O.U), v=gy, e=a, heads=heads)
+    assert O.bit_equal(gx, gx_want)
+    ga = gpu_reduce(g, (O.U, O.V, O.DOT, O.LAST, O.E), u=x, v=gy, heads=heads)
+    assert O.bit_equal(ga, ga_want)
+
+
+def test_long_rows_hub():
+    # a hub with 60k in-edges and 40k out-edges exercises the long-row plan
+    rng = np.random.default_rng(0)
+    n = 5000
+    src = np.concatenate([rng.integers(0, n, 60000), np.zeros(40000, np.int64),
+                          rng.integers(0, n, 20000)]).astype(np.uint32)
+    dst = np.concatenate([np.zeros(60000, np.int64), rng.integers(0, n, 40000),
+                          rng.integers(0, n, 20000)]).astype(np.uint32)
+    g = O.Graph(n, src, dst)
+    x = O.normal_features(n, 128, 1)
+    w = O.gcn_weights(n, src, dst)
+    for cfg, kw in (((O.U, O.E, O.MUL, O.SUM, O.V), dict(u=x, e=w)),
+                    ((O.V, O.E, O.MUL, O.SUM, O.U), dict(v=x, e=w)),
+                    ((O.U, O.NONE, O.COPY, O.MAX, O.V), dict(u=x))):
+        assert O.bit_equal(gpu_reduce(g, cfg, **kw), O.binary_reduce(g, cfg, **kw))
+    assert dev_graph(g, O.DST_MAJOR).num_long_rows >= 1
