@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -14,6 +15,7 @@
 
 #include "gspmm_b200.h"
 #include "internal.h"
+#include "stream.h"
 
 namespace gspmm_b200 {
 uint64_t launch_count();
@@ -49,8 +51,18 @@ const char* operand_name(int o) {
   }
 }
 
-// Rows above this degree are scheduled first (descending degree).
-constexpr uint32_t kLongThreshold = 1024;
+// Device plan defaults: edges per row segment, and the degree above which a
+// row is a LONG row (split into narrow column slices across many warps).
+// Overridable for experiments with GSPMM_SEG_EDGES / GSPMM_LONG_EDGES.
+constexpr uint32_t kSegEdges = 1024;
+constexpr uint32_t kLongEdges = 4096;
+
+uint32_t env_u32(const char* name, uint32_t dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  const long x = std::strtol(v, nullptr, 10);
+  return x > 0 ? static_cast<uint32_t>(x) : dflt;
+}
 
 }  // namespace
 
@@ -64,6 +76,12 @@ struct gspmm_graph_s {
   uint32_t* d_eids = nullptr;
   uint32_t* d_long = nullptr;
   uint32_t num_long = 0;
+  uint32_t long_threshold = 0;
+  uint2* d_segs = nullptr;
+  uint32_t num_segs = 0;
+  uint32_t* d_counter = nullptr;  // [0] segment units, [1] long-row units
+  cudaStream_t side = nullptr;     // long-row kernel runs here concurrently
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int num_sms = 148;
   std::mutex mu;  // guards the host-call workspace
   void* ws = nullptr;
@@ -214,7 +232,7 @@ int bind(const gspmm_graph_s* g, const gspmm_config* cfg, const gspmm_mat* u,
   L.arg_ld = opt->arg_ld ? opt->arg_ld : w;
   L.long_rows = g->d_long;
   L.num_long = g->num_long;
-  L.long_threshold = g->num_long ? kLongThreshold : 0xffffffffu;
+  L.long_threshold = g->num_long ? g->long_threshold : 0xffffffffu;
   L.num_sms = g->num_sms;
   b->out_rows = entity_rows(g, cfg->out);
   b->width = w;
@@ -244,14 +262,129 @@ int bind(const gspmm_graph_s* g, const gspmm_config* cfg, const gspmm_mat* u,
   return GSPMM_OK;
 }
 
+// Which planned kernel runs this binding?  Both planned kernels take the
+// gathered full-width operand as lhs and at most a small (scalar /
+// per-head) edge or neighbour operand as rhs; everything else goes to the
+// simple register kernel (rows.cu).  0 = rows.cu, 1 = gather.cu (default),
+// 2 = stream.cu (TMA-staged, GSPMM_KERNEL=tma).
+int plan_kernel(const RowLaunch& L, int* rhs_width) {
+  static const char* kname = std::getenv("GSPMM_KERNEL");
+  static const int forced = !kname ? -1
+                            : std::strcmp(kname, "rows") == 0 ? 0
+                            : std::strcmp(kname, "tma") == 0 ? 2 : 1;
+  if (forced == 0 || std::getenv("GSPMM_DISABLE_STREAM") != nullptr) return 0;
+  if (L.binop == GSPMM_DOT || L.out_edge || !L.out) return 0;
+  if (L.reduce == R_PROD || L.reduce == R_LAST) return 0;  // rare: rows.cu
+  if (L.lhs.mode != MODE_FULL || L.lhs.role == ROLE_ROW) return 0;
+  if (L.lhs.ld % 4 || !aligned(L.lhs.base, 16)) return 0;
+  if (L.out_ld % 4 || !aligned(L.out, 16)) return 0;
+  *rhs_width = 0;
+  const int k = forced == 2 ? 2 : 1;
+  if (L.rhs.base) {
+    if (L.rhs.role == ROLE_ROW || L.rhs.mode == MODE_FULL) return 0;
+    // lanes fold float4 column groups: a head must cover whole groups
+    if (L.rhs.mode == MODE_HEAD && L.rhs.group % 4) return 0;
+    const int h = L.rhs.mode == MODE_SCALAR ? 1 : L.width / L.rhs.group;
+    if (k == 2) {  // TMA variant stages the small operand with cp.async
+      if (L.other_scale) return 0;
+      if (h != 1 && h != 2 && h != 4 && h != 8 && h != 16) return 0;
+      if (h >= 2 && (L.rhs.ld % h || !aligned(L.rhs.base, h >= 4 ? 16 : 8))) return 0;
+      if (h >= 4 && L.rhs.ld % 4) return 0;
+    }
+    *rhs_width = h;
+  }
+  return k;
+}
+
 int launch(gspmm_graph_s* g, Bound& b, void* stream) {
   cudaError_t err;
-  if (b.L.binop == GSPMM_DOT)
-    err = launch_dot(b.L, static_cast<cudaStream_t>(stream));
-  else
-    err = launch_rows(b.L, static_cast<cudaStream_t>(stream));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rw = 0;
+  int kind = 0;
+  if (b.L.binop == GSPMM_DOT) {
+    err = launch_dot(b.L, s);
+  } else if ((kind = plan_kernel(b.L, &rw)) != 0) {
+    StreamLaunch p;
+    p.row = b.L;
+    p.segs = g->d_segs;
+    p.n_segs = g->num_segs;
+    p.long_rows = g->d_long;
+    p.n_long = g->num_long;
+    p.counter = g->d_counter;
+    p.rhs_width = rw;
+    const int W = b.L.width;
+    p.seg_sw = W <= 256 ? W : 256;
+    p.seg_slices = static_cast<uint32_t>((W + p.seg_sw - 1) / p.seg_sw);
+    static const uint32_t tma_min = env_u32("GSPMM_TMA_MIN_BYTES", 512);
+    p.tma_min_bytes = tma_min;
+    static const char* trace_path = std::getenv("GSPMM_UNIT_TRACE");
+    // development aid: per-unit timing of one launch, appended to a file
+    auto traced = [&](StreamLaunch q, cudaStream_t st, auto&& fn) -> cudaError_t {
+      if (!trace_path || !*trace_path) return fn(q, st);
+      unsigned long long* d = nullptr;
+      const size_t bytes = sizeof(unsigned long long) * 4 * std::max<uint32_t>(q.n_units, 1);
+      cudaError_t e2 = cudaMalloc(&d, bytes);
+      if (e2 != cudaSuccess) return e2;
+      cudaMemsetAsync(d, 0, bytes, st);
+      q.trace = d;
+      e2 = fn(q, st);
+      std::vector<unsigned long long> h(bytes / sizeof(unsigned long long));
+      cudaMemcpyAsync(h.data(), d, bytes, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      cudaFree(d);
+      if (FILE* f = std::fopen(trace_path, "ab")) {
+        const unsigned long long hdr[4] = {0xC0FFEEull, q.n_units, q.n_long_units,
+                                           static_cast<unsigned long long>(q.mode)};
+        std::fwrite(hdr, sizeof(hdr), 1, f);
+        std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+        std::fclose(f);
+      }
+      return e2;
+    };
+    if (kind == 2) {
+      // TMA variant: long rows as 32-column slices inside the same kernel
+      p.long_sw = W <= 32 ? W : 32;
+      p.long_slices = static_cast<uint32_t>((W + p.long_sw - 1) / p.long_sw);
+      p.n_long_units = p.n_long * p.long_slices;
+      p.n_units = p.n_long_units + p.n_segs * p.seg_slices;
+      err = traced(p, s, [](const StreamLaunch& q, cudaStream_t st) { return launch_stream(q, st); });
+    } else {
+      // Long rows (one per CTA, <= 256-column slices) run on the handle's
+      // side stream concurrently with the row segments: fork / join with
+      // events so the call stays ordered on the caller's stream.
+      StreamLaunch pl = p;
+      pl.mode = 1;
+      pl.long_sw = W <= 256 ? W : 256;
+      pl.long_slices = static_cast<uint32_t>((W + pl.long_sw - 1) / pl.long_sw);
+      pl.n_long_units = pl.n_long * pl.long_slices;
+      pl.n_units = pl.n_long_units;
+      pl.counter = g->d_counter + 1;
+      p.mode = 0;
+      p.n_long_units = 0;
+      p.n_units = p.n_segs * p.seg_slices;
+      auto run_gather = [](const StreamLaunch& q, cudaStream_t st) { return launch_gather(q, st); };
+      err = cudaSuccess;
+      if (pl.n_units) {
+        if (!g->side) {
+          CUDA_TRY(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking), "side stream");
+          CUDA_TRY(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming), "event");
+          CUDA_TRY(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming), "event");
+        }
+        CUDA_TRY(cudaEventRecord(g->ev_fork, s), "fork");
+        CUDA_TRY(cudaStreamWaitEvent(g->side, g->ev_fork, 0), "fork");
+        err = traced(pl, g->side, run_gather);
+        if (err == cudaSuccess) err = cudaEventRecord(g->ev_join, g->side);
+      }
+      if (err == cudaSuccess && p.n_units) err = traced(p, s, run_gather);
+      if (pl.n_units) {
+        cudaError_t ej = cudaStreamWaitEvent(s, g->ev_join, 0);
+        if (err == cudaSuccess) err = ej;
+      }
+    }
+  } else {
+    err = launch_rows(b.L, s);
+  }
   if (err != cudaSuccess) return cuda_fail(err, "kernel launch");
-  (void)g;
   return GSPMM_OK;
 }
 
@@ -384,20 +517,46 @@ int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
   g->m = m;
   cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
 
-  // Degree plan: rows above kLongThreshold, heaviest first.
+  // Device plan: long rows (heaviest first) and edge-balanced segments of
+  // consecutive non-long rows.
+  const uint32_t seg_edges = env_u32("GSPMM_SEG_EDGES", kSegEdges);
+  g->long_threshold = env_u32("GSPMM_LONG_EDGES", kLongEdges);
   std::vector<uint32_t> long_rows;
-  for (uint32_t r = 0; r < num_rows; ++r)
-    if (indptr[r + 1] - indptr[r] > kLongThreshold) long_rows.push_back(r);
+  std::vector<uint2> segs;
+  {
+    uint32_t begin = 0;
+    uint64_t acc = 0;
+    for (uint32_t r = 0; r < num_rows; ++r) {
+      const uint32_t deg = indptr[r + 1] - indptr[r];
+      if (deg > g->long_threshold) {
+        long_rows.push_back(r);
+        if (r > begin) segs.push_back(make_uint2(begin, r));
+        begin = r + 1;
+        acc = 0;
+        continue;
+      }
+      acc += deg;
+      if (acc >= seg_edges) {
+        segs.push_back(make_uint2(begin, r + 1));
+        begin = r + 1;
+        acc = 0;
+      }
+    }
+    if (num_rows > begin) segs.push_back(make_uint2(begin, num_rows));
+  }
   std::stable_sort(long_rows.begin(), long_rows.end(), [&](uint32_t a, uint32_t b) {
     return indptr[a + 1] - indptr[a] > indptr[b + 1] - indptr[b];
   });
   g->num_long = static_cast<uint32_t>(long_rows.size());
+  g->num_segs = static_cast<uint32_t>(segs.size());
 
   auto cleanup = [&](cudaError_t e, const char* where) {
     cudaFree(g->d_indptr);
     cudaFree(g->d_indices);
     cudaFree(g->d_eids);
     cudaFree(g->d_long);
+    cudaFree(g->d_segs);
+    cudaFree(g->d_counter);
     delete g;
     return cuda_fail(e, where);
   };
@@ -426,6 +585,15 @@ int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
       (e = cudaMemcpy(g->d_long, long_rows.data(), sizeof(uint32_t) * long_rows.size(),
                       cudaMemcpyHostToDevice)) != cudaSuccess)
     return cleanup(e, "upload plan");
+  if ((e = cudaMalloc(&g->d_segs, sizeof(uint2) * std::max<size_t>(segs.size(), 1))) !=
+      cudaSuccess)
+    return cleanup(e, "cudaMalloc segments");
+  if (!segs.empty() &&
+      (e = cudaMemcpy(g->d_segs, segs.data(), sizeof(uint2) * segs.size(),
+                      cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cleanup(e, "upload segments");
+  if ((e = cudaMalloc(&g->d_counter, 2 * sizeof(uint32_t))) != cudaSuccess)
+    return cleanup(e, "cudaMalloc counter");
   *out = g;
   return GSPMM_OK;
 }
@@ -437,6 +605,13 @@ int gspmm_graph_destroy(gspmm_graph g) {
   cudaFree(g->d_indices);
   cudaFree(g->d_eids);
   cudaFree(g->d_long);
+  cudaFree(g->d_segs);
+  cudaFree(g->d_counter);
+  if (g->side) {
+    cudaStreamDestroy(g->side);
+    cudaEventDestroy(g->ev_fork);
+    cudaEventDestroy(g->ev_join);
+  }
   cudaFree(g->ws);
   delete g;
   return GSPMM_OK;

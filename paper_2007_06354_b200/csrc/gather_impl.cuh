@@ -1,0 +1,557 @@
+// gather_impl.cuh -- the production owner-computes row kernel (sm_100a),
+// instantiated per binary operator in gather_{copy,mul,arith}.cu.
+//
+// Same semantics as rows.cu / stream.cu (the reference's RowParallelSpmm
+// left fold, kernels.cpp:162-195, bit for bit), built from measurements on
+// B200 (scripts/mb_gather.cu, profiles/):
+//
+//   * random source-row gathers run fastest as 128-bit LDGs into registers
+//     (7.2 TB/s for 1 KB rows, 5.0 TB/s for 400 B rows) -- faster than one
+//     TMA bulk copy per row (5.9 / 1.8 TB/s), whose per-SM request rate caps
+//     small rows; so rows are gathered with LDG.128 into a register
+//     ping-pong: the next batch's loads are in flight while the current
+//     batch is folded;
+//   * persistent CTAs pull WORK UNITS (the device plan: edge-balanced
+//     segments of consecutive rows, and column slices of long rows) from a
+//     global counter, first units interleaved across SMs;
+//   * WIDE units: lanes own 4 (or 8) output columns, one edge per warp load
+//     instruction (512 B or 1 KB);  NARROW units (32-column slices of long
+//     rows): lane = (edge group g, column quad i), four edges per warp load
+//     instruction; the four edges are then folded in order by the column
+//     owners through warp shuffles -- the fold stays sequential per column;
+//   * neighbour ids / scalar edge operands arrive as coalesced 32-edge
+//     windows prefetched one window (NARROW: two) ahead and broadcast with
+//     shuffles; row ends likewise;
+//   * fused epilogue: zero-degree fixup, mean, argmax; each output row is
+//     written exactly once.
+#pragma once
+#include <type_traits>
+#include "device_ops.cuh"
+#include "stream.h"
+#include "tma.cuh"
+
+namespace gspmm_b200 {
+namespace gather_detail {
+
+constexpr int kThreads = 256;
+
+struct UnitCtx {
+  uint32_t r0, r1, e0, e1;
+  int c0, cw;
+};
+
+// Row-boundary state of a unit: windows of indptr (lane k <-> rb + 1 + k).
+struct RowCursor {
+  uint32_t rb, rwin, rnxt, r, row_start, row_end, r1;
+  __device__ __forceinline__ void init(const uint32_t* indptr, uint32_t r0_, uint32_t r1_,
+                                       uint32_t e0, int lane) {
+    rb = r0_;
+    r1 = r1_;
+    rwin = 0;
+    rnxt = 0;
+    if (r0_ + 1 + lane <= r1_) rwin = __ldg(indptr + r0_ + 1 + lane);
+    if (r0_ + 33 + lane <= r1_) rnxt = __ldg(indptr + r0_ + 33 + lane);
+    r = r0_;
+    row_start = e0;
+    row_end = __shfl_sync(kFull, rwin, 0);
+  }
+  __device__ __forceinline__ void advance(const uint32_t* indptr, int lane) {
+    ++r;
+    row_start = row_end;
+    if (r - rb >= 32u) {
+      rb += 32u;
+      rwin = rnxt;
+      rnxt = 0;
+      if (rb + 33 + lane <= r1) rnxt = __ldg(indptr + rb + 33 + lane);
+    }
+    row_end = __shfl_sync(kFull, rwin, static_cast<int>(r - rb) & 31);
+  }
+};
+
+template <int VPL, int ROP, bool ARG>
+struct Acc {
+  float a[VPL][4];
+  uint32_t arg[VPL][4];
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        a[v][t] = red_identity<ROP>();
+        arg[v][t] = 0xffffffffu;
+      }
+  }
+  __device__ __forceinline__ void fold(int v, const float (&m)[4], uint32_t j) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if constexpr (ARG) {
+        if (red_wins<ROP>(a[v][t], m[t])) {
+          a[v][t] = m[t];
+          arg[v][t] = j;
+        }
+      } else {
+        a[v][t] = red_combine<ROP>(a[v][t], m[t]);
+      }
+    }
+  }
+  // Epilogue of owner row r over columns [c0 + c, ...) of this lane.
+  __device__ __forceinline__ void store(const RowLaunch& L, uint32_t r, uint32_t deg, int c0,
+                                        int cw, int v, int c) {
+    if (c >= cw) return;
+    float o[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      float x = a[v][t];
+      if constexpr (ROP == R_MAX || ROP == R_MIN) {
+        if (deg == 0) x = 0.0f;
+      }
+      if (L.mean) x = deg ? __fdiv_rn(x, __uint2float_rn(deg)) : 0.0f;
+      o[t] = x;
+    }
+    float* orow = L.out + static_cast<int64_t>(r) * L.out_ld + c0;
+    if (c + 4 <= cw) {
+      store_vec<4>(orow + c, o);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (c + t < cw) orow[c + t] = o[t];
+    }
+    if constexpr (ARG) {
+      const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + c;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (c + t >= cw) break;
+        const bool none = arg[v][t] == 0xffffffffu;
+        if (L.arg_other)
+          L.arg_other[ab + t] = none ? -1 : static_cast<int32_t>(__ldg(L.indices + arg[v][t]));
+        if (L.arg_edge)
+          L.arg_edge[ab + t] = none ? -1 : static_cast<int32_t>(__ldg(L.eids + arg[v][t]));
+      }
+    }
+  }
+};
+
+// Small per-edge operand value for output columns starting at c (absolute).
+__device__ __forceinline__ float small_value(const RowLaunch& L, int rw, uint32_t other,
+                                             uint32_t eid, uint32_t j, int cabs) {
+  const int64_t rr = operand_row(L.rhs.role, 0, other, eid, j);
+  const int h = rw == 1 ? 0 : cabs / L.rhs.group;
+  return __ldg(L.rhs.base + rr * L.rhs.ld + h);
+}
+
+// ------------------------------------------------------------------ WIDE
+// One edge per warp load instruction; lanes own columns lane*4 + v*128.
+// Batches of U edges: all U rows' loads are issued, then folded in edge
+// order as runs of the current row (the finalize code exists once).
+template <int VPL, int U, int BOP, int ROP, bool ARG, bool SMALL>
+__device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, int rw,
+                                          bool scale_on, bool need_eid, int lane) {
+  const float* lbase = L.lhs.base + u.c0 + lane * 4;
+  const int64_t lld = L.lhs.ld;
+  const int32_t lrole = L.lhs.role;
+  bool col_ok[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) col_ok[v] = lane * 4 + v * 128 < u.cw;
+  const bool rs_pos = SMALL && rw == 1 && L.rhs.role == ROLE_POS;
+
+  RowCursor rc;
+  rc.init(L.indptr, u.r0, u.r1, u.e0, lane);
+  Acc<VPL, ROP, ARG> acc;
+  acc.reset();
+
+  // id windows: lane k <-> edge e0 + 32w + k; the next window is in flight
+  uint32_t win_o = 0, win_e = 0, nxt_o = 0, nxt_e = 0;
+  float win_r = 0.0f, nxt_r = 0.0f;  // scalar rhs in CSR order rides along
+  auto load_win = [&](uint32_t w, uint32_t& o, uint32_t& e, float& rs) {
+    const uint32_t j = u.e0 + 32u * w + lane;
+    if (j < u.e1) {
+      o = __ldg(L.indices + j);
+      if (need_eid) e = __ldg(L.eids + j);
+      if (rs_pos) rs = __ldg(L.rhs.base + static_cast<int64_t>(j) * L.rhs.ld);
+    }
+  };
+  const uint32_t n_edges = u.e1 - u.e0;
+  load_win(0, win_o, win_e, win_r);
+  load_win(1, nxt_o, nxt_e, nxt_r);
+  constexpr int kPerWin = 32 / U;
+  const uint32_t n_batches = (n_edges + U - 1) / U;
+
+  uint32_t j = u.e0;
+  for (uint32_t b = 0; b < n_batches; ++b) {
+    if (b != 0 && (b % kPerWin) == 0) {  // entering the next id window
+      win_o = nxt_o;
+      win_e = nxt_e;
+      win_r = nxt_r;
+      load_win(b / kPerWin + 1, nxt_o, nxt_e, nxt_r);
+    }
+    const uint32_t jb = u.e0 + b * U;
+    const uint32_t n = min(static_cast<uint32_t>(U), u.e1 - jb);
+    float4 x[U][VPL];
+    float r[U][VPL];  // small operand per edge and vector (or the scale)
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int sl = static_cast<int>((b % kPerWin) * U) + k;
+      const uint32_t o = __shfl_sync(kFull, win_o, sl);
+      const uint32_t e = need_eid ? __shfl_sync(kFull, win_e, sl) : 0u;
+      float rs = 0.0f;
+      if (rs_pos) rs = __shfl_sync(kFull, win_r, sl);
+      if (static_cast<uint32_t>(k) < n) {
+        const int64_t lr = operand_row(lrole, 0, o, e, jb + k);
+        const float* src = lbase + lr * lld;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          if (col_ok[v]) x[k][v] = __ldg(reinterpret_cast<const float4*>(src + v * 128));
+        if constexpr (SMALL) {
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) {
+            if (rs_pos) r[k][v] = rs;
+            else if (rw > 0)
+              r[k][v] = col_ok[v] ? small_value(L, rw, o, e, jb + k, u.c0 + lane * 4 + v * 128)
+                                  : 0.0f;
+            else if (scale_on) r[k][v] = __ldg(L.other_scale + o);
+          }
+        }
+      }
+    }
+    uint32_t k0 = 0;
+    while (k0 < n) {
+      while (j == rc.row_end) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          acc.store(L, rc.r, rc.row_end - rc.row_start, u.c0, u.cw, v, lane * 4 + v * 128);
+        acc.reset();
+        rc.advance(L.indptr, lane);
+      }
+      const uint32_t k1 = k0 + min(n - k0, rc.row_end - j);
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        if (static_cast<uint32_t>(k) < k0 || static_cast<uint32_t>(k) >= k1) continue;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          if (!col_ok[v]) continue;
+          const float xs[4] = {x[k][v].x, x[k][v].y, x[k][v].z, x[k][v].w};
+          float m[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            if constexpr (SMALL) {
+              if (rw > 0) m[t] = bin_apply<BOP>(xs[t], r[k][v]);
+              else m[t] = __fmul_rn(bin_apply<BOP>(xs[t], 0.0f), r[k][v]);  // copy * scale
+            } else {
+              m[t] = bin_apply<BOP>(xs[t], 0.0f);
+            }
+          }
+          acc.fold(v, m, u.e0 + b * U + k);
+        }
+      }
+      j += k1 - k0;
+      k0 = k1;
+    }
+  }
+  // the current row and trailing empty rows
+  while (rc.r < u.r1) {
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+      acc.store(L, rc.r, rc.row_end - rc.row_start, u.c0, u.cw, v, lane * 4 + v * 128);
+    acc.reset();
+    if (rc.r + 1 < u.r1) {
+      rc.advance(L.indptr, lane);
+    } else {
+      ++rc.r;
+    }
+  }
+}
+
+// -------------------------------------------------------------- LONG ROWS
+// One long row (a column slice of <= 256 floats of it) per CTA: the 16 warps
+// gather a round of R edges with LDG.128 into registers while the previous
+// round, staged in shared memory, is folded by the column owners (thread t
+// owns column t) in canonical edge order.  A lone warp cannot keep enough
+// bytes in flight for a 66k-329k-edge row (one owner must see every edge in
+// order); a CTA keeps ~128 KB in flight for it.
+constexpr int kLongThreads = 512;
+
+template <int VPL>
+struct LongGeom {
+  static constexpr int U = VPL == 1 ? 16 : 8;          // edges per warp per round
+  static constexpr int R = (kLongThreads / 32) * U;    // edges per round
+  static constexpr int kMaxSmall = 16;                  // staged small floats per edge
+  static constexpr size_t smem_bytes(int slot_f) {
+    return sizeof(float) * (static_cast<size_t>(R) * slot_f + static_cast<size_t>(R) * kMaxSmall);
+  }
+};
+
+template <int VPL, int BOP, int ROP, bool ARG, bool SMALL>
+__global__ void __launch_bounds__(kLongThreads, 1) k_long(const StreamLaunch p) {
+  using G = LongGeom<VPL>;
+  constexpr int U = G::U, R = G::R;
+  extern __shared__ __align__(16) float sm[];
+  __shared__ uint32_t s_unit;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const RowLaunch& L = p.row;
+  const int rw = SMALL ? p.rhs_width : 0;
+  const bool scale_on = SMALL && L.other_scale != nullptr;
+  const int rws = SMALL ? (rw > 0 ? rw : 1) : 0;  // staged small floats per edge
+  const bool need_eid = L.lhs.role == ROLE_EID || (rw && L.rhs.role == ROLE_EID);
+
+  for (;;) {
+    if (tid == 0) s_unit = atomicAdd(p.counter, 1u);
+    __syncthreads();
+    const uint32_t unit = s_unit;
+    __syncthreads();
+    if (unit >= p.n_units) break;
+    const unsigned long long t0 = p.trace ? globaltimer_ns() : 0ull;
+    const uint32_t li = unit / p.long_slices;
+    const uint32_t slc = unit - li * p.long_slices;
+    const uint32_t r = __ldg(p.long_rows + li);
+    const int c0 = static_cast<int>(slc) * p.long_sw;
+    const int cw = min(p.long_sw, L.width - c0);
+    const int slot_f = (cw + 3) & ~3;
+    float* buf = sm;
+    float* sbuf = sm + static_cast<size_t>(R) * slot_f;
+    const uint32_t e0 = __ldg(L.indptr + r), e1 = __ldg(L.indptr + r + 1);
+    const uint32_t n = e1 - e0;
+    const uint32_t rounds = (n + R - 1) / R;
+    const float* lbase = L.lhs.base + c0 + lane * 4;
+    bool col_ok[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) col_ok[v] = lane * 4 + v * 128 < cw;
+
+    // ids of this warp's U edges of a round: lane k < U <-> edge k
+    auto load_ids = [&](uint32_t rd, uint32_t& o, uint32_t& e) {
+      const uint32_t j = e0 + rd * R + warp * U + lane;
+      if (lane < U && j < e1) {
+        o = __ldg(L.indices + j);
+        if (need_eid) e = __ldg(L.eids + j);
+      }
+    };
+    float4 x[U][VPL];
+    float sv[G::kMaxSmall];  // lane k < U: small operand of edge k
+    auto issue = [&](uint32_t rd, uint32_t o_win, uint32_t e_win) {
+      const uint32_t jb = e0 + rd * R + warp * U;
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const uint32_t o = __shfl_sync(kFull, o_win, k);
+        const uint32_t e = need_eid ? __shfl_sync(kFull, e_win, k) : 0u;
+        if (jb + k < e1) {
+          const float* src = lbase + operand_row(L.lhs.role, 0, o, e, jb + k) * L.lhs.ld;
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            if (col_ok[v]) x[k][v] = __ldg(reinterpret_cast<const float4*>(src + v * 128));
+        }
+      }
+      if constexpr (SMALL) {
+        const uint32_t j = jb + lane;
+        if (lane < U && j < e1) {
+          if (rw > 0) {
+            const float* src = L.rhs.base + operand_row(L.rhs.role, 0, o_win, e_win, j) * L.rhs.ld;
+#pragma unroll
+            for (int h = 0; h < G::kMaxSmall; ++h)
+              if (h < rw) sv[h] = __ldg(src + h);
+          } else if (scale_on) {
+            sv[0] = __ldg(L.other_scale + o_win);
+          }
+        }
+      }
+    };
+    auto stage = [&](uint32_t rd) {
+      const uint32_t jb = e0 + rd * R + warp * U;
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        if (jb + k < e1) {
+          float* dst = buf + static_cast<size_t>(warp * U + k) * slot_f + lane * 4;
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            if (col_ok[v]) *reinterpret_cast<float4*>(dst + v * 128) = x[k][v];
+        }
+      }
+      if constexpr (SMALL) {
+        if (lane < U && jb + lane < e1) {
+#pragma unroll
+          for (int h = 0; h < G::kMaxSmall; ++h)
+            if (h < rws) sbuf[(warp * U + lane) * rws + h] = sv[h];
+        }
+      }
+    };
+
+    // the fold: thread tid < cw owns column c0 + tid
+    float acc = red_identity<ROP>();
+    uint32_t arg = 0xffffffffu;
+    const int hcol = (SMALL && rw > 1) ? (c0 + tid) / L.rhs.group : 0;
+    uint32_t ida = 0, idea = 0, idb = 0, ideb = 0;
+    load_ids(0, ida, idea);
+    load_ids(1, idb, ideb);
+    issue(0, ida, idea);
+    stage(0);
+    __syncthreads();
+    for (uint32_t k = 0; k < rounds; ++k) {
+      if (k + 1 < rounds) {
+        issue(k + 1, idb, ideb);  // loads in flight during the fold below
+        load_ids(k + 2, idb, ideb);
+      }
+      if (tid < cw) {
+        const uint32_t cnt = min(static_cast<uint32_t>(R), n - k * R);
+        const float* col = buf + tid;
+        for (uint32_t e = 0; e < cnt; ++e) {
+          float m = col[static_cast<size_t>(e) * slot_f];
+          if constexpr (SMALL) {
+            if (rw > 0) m = bin_apply<BOP>(m, sbuf[e * rws + hcol]);
+            else m = __fmul_rn(bin_apply<BOP>(m, 0.0f), sbuf[e]);
+          } else {
+            m = bin_apply<BOP>(m, 0.0f);
+          }
+          if constexpr (ARG) {
+            if (red_wins<ROP>(acc, m)) {
+              acc = m;
+              arg = e0 + k * R + e;
+            }
+          } else {
+            acc = red_combine<ROP>(acc, m);
+          }
+        }
+      }
+      __syncthreads();
+      if (k + 1 < rounds) stage(k + 1);
+      __syncthreads();
+    }
+    if (tid < cw) {
+      float a = acc;
+      if constexpr (ROP == R_MAX || ROP == R_MIN) {
+        if (n == 0) a = 0.0f;
+      }
+      if (L.mean) a = n ? __fdiv_rn(a, __uint2float_rn(n)) : 0.0f;
+      L.out[static_cast<int64_t>(r) * L.out_ld + c0 + tid] = a;
+      if constexpr (ARG) {
+        const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + tid;
+        const bool none = arg == 0xffffffffu;
+        if (L.arg_other)
+          L.arg_other[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.indices + arg));
+        if (L.arg_edge) L.arg_edge[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.eids + arg));
+      }
+    }
+    if (p.trace && tid == 0) {
+      unsigned long long* t = p.trace + 4ull * unit;
+      t[0] = t0;
+      t[1] = globaltimer_ns();
+      t[2] = (static_cast<unsigned long long>(smid()) << 32) | 0xffffu;
+      t[3] = n;
+    }
+    __syncthreads();
+  }
+}
+
+// -------------------------------------------------------------- segments
+template <int VPL, int U, int BOP, int ROP, bool ARG, bool SMALL>
+__global__ void __launch_bounds__(kThreads, 2) k_gather(const StreamLaunch p) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int warps = kThreads / 32;
+  const RowLaunch& L = p.row;
+  const int rw = SMALL ? p.rhs_width : 0;
+  const bool scale_on = SMALL && L.other_scale != nullptr;
+  const bool need_eid = L.lhs.role == ROLE_EID || (rw && L.rhs.role == ROLE_EID);
+
+  const uint32_t n_static = gridDim.x * warps;
+  uint32_t next_unit = blockIdx.x + gridDim.x * static_cast<uint32_t>(warp);
+  for (;;) {
+    const uint32_t unit = next_unit;
+    if (unit >= p.n_units) break;
+    if (lane == 0) next_unit = atomicAdd(p.counter, 1u) + n_static;
+    next_unit = __shfl_sync(kFull, next_unit, 0);
+    const unsigned long long t0 = p.trace ? globaltimer_ns() : 0ull;
+
+    UnitCtx u;
+    const uint32_t si = unit / p.seg_slices;
+    const uint32_t sl = unit - si * p.seg_slices;
+    const uint2 seg = __ldg(p.segs + si);
+    u.r0 = seg.x;
+    u.r1 = seg.y;
+    u.c0 = static_cast<int>(sl) * p.seg_sw;
+    u.cw = min(p.seg_sw, L.width - u.c0);
+    u.e0 = __ldg(L.indptr + u.r0);
+    u.e1 = __ldg(L.indptr + u.r1);
+    wide_unit<VPL, U, BOP, ROP, ARG, SMALL>(L, u, rw, scale_on, need_eid, lane);
+    if (p.trace && lane == 0) {
+      unsigned long long* t = p.trace + 4ull * unit;
+      t[0] = t0;
+      t[1] = globaltimer_ns();
+      t[2] = (static_cast<unsigned long long>(smid()) << 32) | static_cast<unsigned>(warp);
+      t[3] = u.e1 - u.e0;
+    }
+  }
+}
+
+// p.mode: 0 = row segments (k_gather), 1 = long rows (k_long)
+template <int VPL, int BOP, int ROP, bool ARG, bool SMALL>
+cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  const int sms = p.row.num_sms > 0 ? p.row.num_sms : 148;
+  if (p.mode == 1) {
+    const int slot_f = (p.long_sw + 3) & ~3;
+    const size_t smem = LongGeom<VPL>::smem_bytes(slot_f);
+    static int configured = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured != dev) {
+      e = cudaFuncSetAttribute(k_long<VPL, BOP, ROP, ARG, SMALL>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(LongGeom<VPL>::smem_bytes(VPL == 1 ? 128 : 256)));
+      if (e != cudaSuccess) return e;
+      configured = dev;
+    }
+    const unsigned grid = p.n_units < static_cast<uint32_t>(sms) ? p.n_units
+                                                                  : static_cast<unsigned>(sms);
+    k_long<VPL, BOP, ROP, ARG, SMALL><<<grid, kLongThreads, smem, s>>>(p);
+  } else {
+    constexpr int U = VPL == 1 ? 16 : 8;
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
+                                                    k_gather<VPL, U, BOP, ROP, ARG, SMALL>,
+                                                    kThreads, 0);
+      if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    k_gather<VPL, U, BOP, ROP, ARG, SMALL><<<sms * blocks_per_sm, kThreads, 0, s>>>(p);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <int VPL, int BOP>
+cudaError_t launch_red(const StreamLaunch& p, cudaStream_t s) {
+  const bool arg = p.row.arg_other || p.row.arg_edge;
+  auto small = [&](auto rop, auto argt) {
+    constexpr int R = decltype(rop)::value;
+    constexpr bool A = decltype(argt)::value;
+    if constexpr (BOP == B_COPY) {
+      return p.row.other_scale ? launch_k<VPL, BOP, R, A, true>(p, s)
+                               : launch_k<VPL, BOP, R, A, false>(p, s);
+    } else {
+      return launch_k<VPL, BOP, R, A, true>(p, s);
+    }
+  };
+  using F = std::false_type;
+  using T = std::true_type;
+  switch (p.row.reduce) {
+    case R_SUM: return small(std::integral_constant<int, R_SUM>{}, F{});
+    case R_MAX: return arg ? small(std::integral_constant<int, R_MAX>{}, T{})
+                           : small(std::integral_constant<int, R_MAX>{}, F{});
+    default: return arg ? small(std::integral_constant<int, R_MIN>{}, T{})
+                        : small(std::integral_constant<int, R_MIN>{}, F{});
+  }
+}
+
+template <int BOP>
+cudaError_t launch_bop(const StreamLaunch& p, cudaStream_t s) {
+  const int sw = p.mode == 1 ? p.long_sw : p.seg_sw;
+  return sw > 128 ? launch_red<2, BOP>(p, s) : launch_red<1, BOP>(p, s);
+}
+
+}  // namespace gather_detail
+
+// per-operator entry points (one translation unit each)
+cudaError_t launch_gather_copy(const StreamLaunch& p, cudaStream_t s);
+cudaError_t launch_gather_mul(const StreamLaunch& p, cudaStream_t s);
+cudaError_t launch_gather_arith(const StreamLaunch& p, cudaStream_t s);
+
+}  // namespace gspmm_b200

@@ -11,7 +11,9 @@ oracle_aggregate, compare.hpp:30-45) is checked as well.
 import numpy as np
 import pytest
 
-from gspmm_testutil import HAS_GPU
+import os
+
+from gspmm_testutil import HAS_GPU, ROOT
 from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -367,3 +369,59 @@ def test_long_rows_hub():
                     ((O.U, O.NONE, O.COPY, O.MAX, O.V), dict(u=x))):
         assert O.bit_equal(gpu_reduce(g, cfg, **kw), O.binary_reduce(g, cfg, **kw))
     assert dev_graph(g, O.DST_MAJOR).num_long_rows >= 1
+
+
+@pytest.mark.parametrize("seg,long_", [(1, 2), (7, 16), (64, 100), (3, 100000)])
+def test_plan_granularity_does_not_change_results(seg, long_, monkeypatch):
+    # tiny segments / long-row thresholds force every unit boundary case of
+    # the streaming kernel (rows split across units, empty rows at unit
+    # edges, long rows sliced into 32-column units) -- results stay bitwise
+    monkeypatch.setenv("GSPMM_SEG_EDGES", str(seg))
+    monkeypatch.setenv("GSPMM_LONG_EDGES", str(long_))
+    src, dst = O.gen_rmat(1500, 25000, seed=seg)
+    src, dst = O.add_self_loops(1500, src, dst)
+    g = O.Graph(1500, src, dst)
+    for dim in (4, 100, 256, 300):
+        x = O.normal_features(1500, dim, dim)
+        w = O.gcn_weights(1500, src, dst)
+        cases = [((O.U, O.E, O.MUL, O.SUM, O.V), dict(u=x, e=w)),
+                 ((O.V, O.E, O.MUL, O.SUM, O.U), dict(v=x, e=w)),
+                 ((O.U, O.NONE, O.COPY, O.MAX, O.V), dict(u=x)),
+                 ((O.U, O.NONE, O.COPY, P.MEAN, O.V), dict(u=x))]
+        for cfg, kw in cases:
+            got = gpu_reduce(g, cfg, **kw)
+            want = O.mean(g, x) if cfg[3] == P.MEAN else O.binary_reduce(g, cfg, **kw)
+            assert O.bit_equal(got, want), (seg, long_, dim, cfg)
+        g.__dict__.pop("_dev", None)  # rebuild handles with the next plan
+
+
+def test_register_path_matches_stream_path():
+    # the register-staged fallback (rows.cu) and the TMA-staged kernel
+    # (stream.cu) must agree bitwise; run the fallback in a subprocess
+    import subprocess
+    import sys
+    code = r"""
+import sys; sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+import numpy as np, torch
+import paper_2007_06354_b200 as P
+from oracle import oracle as O
+src, dst = O.gen_rmat(3000, 60000, seed=9)
+g = O.Graph(3000, src, dst)
+x = O.normal_features(3000, 256, 1); w = O.gcn_weights(3000, src, dst)
+h = P.Graph(*g.dst_major, orientation=P.DST_MAJOR)
+out = P.binary_reduce(h, 'u_mul_e_add_v', u=torch.from_numpy(x).cuda(), e=torch.from_numpy(w).cuda())
+np.save(sys.argv[2], out.cpu().numpy())
+"""
+    import tempfile
+    outs = []
+    for disable in (False, True):
+        env = dict(os.environ)
+        env.pop("GSPMM_DISABLE_STREAM", None)
+        if disable:
+            env["GSPMM_DISABLE_STREAM"] = "1"
+        path = tempfile.mktemp(suffix=".npy")
+        r = subprocess.run([sys.executable, "-c", code, ROOT, path], env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    assert O.bit_equal(outs[0], outs[1])
