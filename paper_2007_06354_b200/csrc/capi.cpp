@@ -51,9 +51,9 @@ const char* operand_name(int o) {
   }
 }
 
-// Device plan defaults: edges per row segment, and the degree above which a
-// row is a LONG row (split into narrow column slices across many warps).
-// Overridable for experiments with GSPMM_SEG_EDGES / GSPMM_LONG_EDGES.
+// Device plan defaults: cost (edges + 2 per row) per row segment, and the
+// coarsest long-row threshold.  Overridable for experiments with
+// GSPMM_SEG_EDGES / GSPMM_LONG_EDGES (the latter forces a single level).
 constexpr uint32_t kSegEdges = 1024;
 constexpr uint32_t kLongEdges = 4096;
 
@@ -74,11 +74,18 @@ struct gspmm_graph_s {
   uint32_t* d_indptr = nullptr;
   uint32_t* d_indices = nullptr;
   uint32_t* d_eids = nullptr;
-  uint32_t* d_long = nullptr;
-  uint32_t num_long = 0;
-  uint32_t long_threshold = 0;
-  uint2* d_segs = nullptr;
-  uint32_t num_segs = 0;
+  // Device plan, one level per long-row threshold (degree above which a row
+  // is folded by a whole CTA): picked per call from the row bytes.
+  struct Level {
+    uint32_t threshold = 0;
+    uint32_t* d_long = nullptr;  // long rows, heaviest first
+    uint32_t num_long = 0;
+    uint64_t long_edges = 0;     // edges in long rows (sizes the long-row grid)
+    uint2* d_segs = nullptr;     // segments of consecutive non-long rows
+    uint32_t num_segs = 0;
+  };
+  Level level[3];
+  int n_levels = 0;
   uint32_t* d_counter = nullptr;  // [0] segment units, [1] long-row units
   cudaStream_t side = nullptr;     // long-row kernel runs here concurrently
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -230,9 +237,12 @@ int bind(const gspmm_graph_s* g, const gspmm_config* cfg, const gspmm_mat* u,
   L.arg_other = opt->arg_other;
   L.arg_edge = opt->arg_edge;
   L.arg_ld = opt->arg_ld ? opt->arg_ld : w;
-  L.long_rows = g->d_long;
-  L.num_long = g->num_long;
-  L.long_threshold = g->num_long ? g->long_threshold : 0xffffffffu;
+  {
+    const auto& lv = g->level[g->n_levels - 1];  // rows.cu: coarsest level
+    L.long_rows = lv.d_long;
+    L.num_long = lv.num_long;
+    L.long_threshold = lv.num_long ? lv.threshold : 0xffffffffu;
+  }
   L.num_sms = g->num_sms;
   b->out_rows = entity_rows(g, cfg->out);
   b->width = w;
@@ -306,10 +316,17 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
   } else if ((kind = plan_kernel(b.L, &rw)) != 0) {
     StreamLaunch p;
     p.row = b.L;
-    p.segs = g->d_segs;
-    p.n_segs = g->num_segs;
-    p.long_rows = g->d_long;
-    p.n_long = g->num_long;
+    // plan level: rows gathering more than ~1 MB go to the long-row CTAs
+    const int slice_bytes = 4 * std::min(b.L.width, 256);
+    const uint32_t target = std::max<uint32_t>(1024, (1u << 20) / static_cast<uint32_t>(slice_bytes));
+    int li = 0;
+    for (int k = 0; k < g->n_levels; ++k)
+      if (g->level[k].threshold <= target) li = k;
+    const auto& lv = g->level[li];
+    p.segs = lv.d_segs;
+    p.n_segs = lv.num_segs;
+    p.long_rows = lv.d_long;
+    p.n_long = lv.num_long;
     p.counter = g->d_counter;
     p.rhs_width = rw;
     const int W = b.L.width;
@@ -359,6 +376,14 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
       pl.n_long_units = pl.n_long * pl.long_slices;
       pl.n_units = pl.n_long_units;
       pl.counter = g->d_counter + 1;
+      {
+        // long-row CTAs ~2x the long rows' share of the edges (measured on the
+        // cfg2-4 shapes: a long CTA streams ~24 GB/s and holds a whole SM)
+        static const uint32_t forced = env_u32("GSPMM_LONG_CTAS", 0);
+        const double share = g->m ? static_cast<double>(lv.long_edges) / g->m : 0.0;
+        uint32_t c = forced ? forced : static_cast<uint32_t>(share * g->num_sms * 2.0 + 1.0);
+        pl.long_ctas = std::min<uint32_t>(std::max<uint32_t>(c, 1), g->num_sms);
+      }
       p.mode = 0;
       p.n_long_units = 0;
       p.n_units = p.n_segs * p.seg_slices;
@@ -517,45 +542,52 @@ int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
   g->m = m;
   cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
 
-  // Device plan: long rows (heaviest first) and edge-balanced segments of
-  // consecutive non-long rows.
+  // Device plan levels: long rows (heaviest first) and edge-balanced
+  // segments of consecutive non-long rows, for each long-row threshold.
   const uint32_t seg_edges = env_u32("GSPMM_SEG_EDGES", kSegEdges);
-  g->long_threshold = env_u32("GSPMM_LONG_EDGES", kLongEdges);
-  std::vector<uint32_t> long_rows;
-  std::vector<uint2> segs;
-  {
+  const uint32_t forced_long = env_u32("GSPMM_LONG_EDGES", 0);
+  const uint32_t thresholds[3] = {1024, 2048, kLongEdges};
+  g->n_levels = forced_long ? 1 : 3;
+  std::vector<uint32_t> long_rows[3];
+  std::vector<uint2> segs[3];
+  for (int k = 0; k < g->n_levels; ++k) {
+    auto& lv = g->level[k];
+    lv.threshold = forced_long ? forced_long : thresholds[k];
     uint32_t begin = 0;
     uint64_t acc = 0;
     for (uint32_t r = 0; r < num_rows; ++r) {
       const uint32_t deg = indptr[r + 1] - indptr[r];
-      if (deg > g->long_threshold) {
-        long_rows.push_back(r);
-        if (r > begin) segs.push_back(make_uint2(begin, r));
+      if (deg > lv.threshold) {
+        long_rows[k].push_back(r);
+        lv.long_edges += deg;
+        if (r > begin) segs[k].push_back(make_uint2(begin, r));
         begin = r + 1;
         acc = 0;
         continue;
       }
-      acc += deg;
+      acc += deg + 2;  // cost: edges + per-row epilogue (empty rows are not free)
       if (acc >= seg_edges) {
-        segs.push_back(make_uint2(begin, r + 1));
+        segs[k].push_back(make_uint2(begin, r + 1));
         begin = r + 1;
         acc = 0;
       }
     }
-    if (num_rows > begin) segs.push_back(make_uint2(begin, num_rows));
+    if (num_rows > begin) segs[k].push_back(make_uint2(begin, num_rows));
+    std::stable_sort(long_rows[k].begin(), long_rows[k].end(), [&](uint32_t a, uint32_t b) {
+      return indptr[a + 1] - indptr[a] > indptr[b + 1] - indptr[b];
+    });
+    lv.num_long = static_cast<uint32_t>(long_rows[k].size());
+    lv.num_segs = static_cast<uint32_t>(segs[k].size());
   }
-  std::stable_sort(long_rows.begin(), long_rows.end(), [&](uint32_t a, uint32_t b) {
-    return indptr[a + 1] - indptr[a] > indptr[b + 1] - indptr[b];
-  });
-  g->num_long = static_cast<uint32_t>(long_rows.size());
-  g->num_segs = static_cast<uint32_t>(segs.size());
 
   auto cleanup = [&](cudaError_t e, const char* where) {
     cudaFree(g->d_indptr);
     cudaFree(g->d_indices);
     cudaFree(g->d_eids);
-    cudaFree(g->d_long);
-    cudaFree(g->d_segs);
+    for (auto& lv : g->level) {
+      cudaFree(lv.d_long);
+      cudaFree(lv.d_segs);
+    }
     cudaFree(g->d_counter);
     delete g;
     return cuda_fail(e, where);
@@ -567,9 +599,6 @@ int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
     return cleanup(e, "cudaMalloc indices");
   if ((e = cudaMalloc(&g->d_eids, sizeof(uint32_t) * std::max<uint64_t>(m, 1))) != cudaSuccess)
     return cleanup(e, "cudaMalloc edge_ids");
-  if ((e = cudaMalloc(&g->d_long, sizeof(uint32_t) * std::max<size_t>(long_rows.size(), 1))) !=
-      cudaSuccess)
-    return cleanup(e, "cudaMalloc plan");
   if ((e = cudaMemcpy(g->d_indptr, indptr, sizeof(uint32_t) * (num_rows + 1),
                       cudaMemcpyHostToDevice)) != cudaSuccess)
     return cleanup(e, "upload indptr");
@@ -581,17 +610,23 @@ int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
         cudaSuccess)
       return cleanup(e, "upload edge_ids");
   }
-  if (!long_rows.empty() &&
-      (e = cudaMemcpy(g->d_long, long_rows.data(), sizeof(uint32_t) * long_rows.size(),
-                      cudaMemcpyHostToDevice)) != cudaSuccess)
-    return cleanup(e, "upload plan");
-  if ((e = cudaMalloc(&g->d_segs, sizeof(uint2) * std::max<size_t>(segs.size(), 1))) !=
-      cudaSuccess)
-    return cleanup(e, "cudaMalloc segments");
-  if (!segs.empty() &&
-      (e = cudaMemcpy(g->d_segs, segs.data(), sizeof(uint2) * segs.size(),
-                      cudaMemcpyHostToDevice)) != cudaSuccess)
-    return cleanup(e, "upload segments");
+  for (int k = 0; k < g->n_levels; ++k) {
+    auto& lv = g->level[k];
+    if ((e = cudaMalloc(&lv.d_long, sizeof(uint32_t) * std::max<size_t>(long_rows[k].size(), 1))) !=
+        cudaSuccess)
+      return cleanup(e, "cudaMalloc plan");
+    if ((e = cudaMalloc(&lv.d_segs, sizeof(uint2) * std::max<size_t>(segs[k].size(), 1))) !=
+        cudaSuccess)
+      return cleanup(e, "cudaMalloc segments");
+    if (!long_rows[k].empty() &&
+        (e = cudaMemcpy(lv.d_long, long_rows[k].data(), sizeof(uint32_t) * long_rows[k].size(),
+                        cudaMemcpyHostToDevice)) != cudaSuccess)
+      return cleanup(e, "upload plan");
+    if (!segs[k].empty() &&
+        (e = cudaMemcpy(lv.d_segs, segs[k].data(), sizeof(uint2) * segs[k].size(),
+                        cudaMemcpyHostToDevice)) != cudaSuccess)
+      return cleanup(e, "upload segments");
+  }
   if ((e = cudaMalloc(&g->d_counter, 2 * sizeof(uint32_t))) != cudaSuccess)
     return cleanup(e, "cudaMalloc counter");
   *out = g;
@@ -604,8 +639,10 @@ int gspmm_graph_destroy(gspmm_graph g) {
   cudaFree(g->d_indptr);
   cudaFree(g->d_indices);
   cudaFree(g->d_eids);
-  cudaFree(g->d_long);
-  cudaFree(g->d_segs);
+  for (auto& lv : g->level) {
+    cudaFree(lv.d_long);
+    cudaFree(lv.d_segs);
+  }
   cudaFree(g->d_counter);
   if (g->side) {
     cudaStreamDestroy(g->side);
@@ -625,7 +662,7 @@ int gspmm_graph_info(gspmm_graph g, int* orientation, uint32_t* num_rows,
   if (num_rows) *num_rows = g->num_rows;
   if (num_cols) *num_cols = g->num_cols;
   if (num_edges) *num_edges = g->m;
-  if (num_long_rows) *num_long_rows = g->num_long;
+  if (num_long_rows) *num_long_rows = g->level[0].num_long;
   return GSPMM_OK;
 }
 

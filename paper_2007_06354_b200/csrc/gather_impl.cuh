@@ -391,10 +391,12 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long(const StreamLaunch p) 
       if (tid < cw) {
         const uint32_t cnt = min(static_cast<uint32_t>(R), n - k * R);
         const float* col = buf + tid;
+        const int soff = SMALL && rw > 0 ? hcol : 0;
+#pragma unroll 4
         for (uint32_t e = 0; e < cnt; ++e) {
           float m = col[static_cast<size_t>(e) * slot_f];
           if constexpr (SMALL) {
-            if (rw > 0) m = bin_apply<BOP>(m, sbuf[e * rws + hcol]);
+            if (rw > 0) m = bin_apply<BOP>(m, sbuf[e * rws + soff]);
             else m = __fmul_rn(bin_apply<BOP>(m, 0.0f), sbuf[e]);
           } else {
             m = bin_apply<BOP>(m, 0.0f);
@@ -499,8 +501,11 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
       if (e != cudaSuccess) return e;
       configured = dev;
     }
-    const unsigned grid = p.n_units < static_cast<uint32_t>(sms) ? p.n_units
-                                                                  : static_cast<unsigned>(sms);
+    // the host sizes the long-row grid by the long rows' share of the edges
+    // (p.long_ctas); the segment kernel's persistent blocks take the other
+    // SMs and absorb these ones when they finish
+    unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
+    if (grid > p.n_units) grid = p.n_units;
     k_long<VPL, BOP, ROP, ARG, SMALL><<<grid, kLongThreads, smem, s>>>(p);
   } else {
     constexpr int U = VPL == 1 ? 16 : 8;

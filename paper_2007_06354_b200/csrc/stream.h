@@ -20,6 +20,7 @@ struct StreamLaunch {
   uint32_t n_long_units = 0, n_units = 0;
   int rhs_width = 0;      // staged floats per edge of the small operand (0 = none)
   int mode = 0;           // gather.cu: 0 = row segments, 1 = long rows (one per CTA)
+  uint32_t long_ctas = 0; // gather.cu mode 1: grid size (0 = one per SM)
   // Units whose gathered slice is narrower than this many bytes stage rows
   // with per-lane 16-byte cp.async (LSU path) instead of one TMA bulk copy
   // per edge: small bulk copies are bound by the TMA request rate.
