@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libgspmm_b200.so")
+LIB_PATH = os.environ.get("GSPMM_LIB_PATH") or os.path.join(_HERE, "_lib", "libgspmm_b200.so")
 
 # status codes
 OK, ERR_CONFIG, ERR_SHAPE, ERR_STRUCTURE, ERR_CUDA, ERR_ARG = 0, 1, 2, 3, 4, 5

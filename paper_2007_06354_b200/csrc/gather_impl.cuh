@@ -34,6 +34,23 @@ namespace gspmm_b200 {
 namespace gather_detail {
 
 constexpr int kThreads = 256;
+// segment kernel geometry: edges per warp batch (<=128 / <=256 columns) and
+// minimum resident blocks per SM.  Measured on B200 (scripts/var_ab.sh): warp
+// parallelism beats per-warp depth -- U=8 at 3 blocks/SM for <=128 columns,
+// U=2 at 4 blocks/SM (32 warps) for 256 columns: 94% of HBM on uniform graphs.
+#ifndef GATHER_U1
+#define GATHER_U1 8
+#endif
+#ifndef GATHER_U2
+#define GATHER_U2 2
+#endif
+#ifndef GATHER_MINB1
+#define GATHER_MINB1 3
+#endif
+#ifndef GATHER_MINB2
+#define GATHER_MINB2 4
+
+#endif
 
 struct UnitCtx {
   uint32_t r0, r1, e0, e1;
@@ -443,7 +460,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long(const StreamLaunch p) 
 
 // -------------------------------------------------------------- segments
 template <int VPL, int U, int BOP, int ROP, bool ARG, bool SMALL>
-__global__ void __launch_bounds__(kThreads, 2) k_gather(const StreamLaunch p) {
+__global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : GATHER_MINB2) k_gather(const StreamLaunch p) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int warps = kThreads / 32;
@@ -508,7 +525,7 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     if (grid > p.n_units) grid = p.n_units;
     k_long<VPL, BOP, ROP, ARG, SMALL><<<grid, kLongThreads, smem, s>>>(p);
   } else {
-    constexpr int U = VPL == 1 ? 16 : 8;
+    constexpr int U = VPL == 1 ? GATHER_U1 : GATHER_U2;
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
