@@ -82,7 +82,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
@@ -374,7 +374,9 @@ def run_ours(args, rank, world, dist):
                    "parallelism": f"dst/src-row shards x{world}" if world > 1 else "single GPU",
                    "l2": "inputs (1 GB feature matrices) larger than the 126 MB L2; no flush",
                    "edge_operand": "weights permuted once to CSR order (device plan, untimed)"},
-        "roofline": {"bound": "hbm", "kernel": f"k_rows<4,MUL,SUM> ({dominant[0]})",
+        "roofline": {"bound": "hbm",
+                     "kernel": f"{dominant[0]} pass: k_gather<VPL2,MUL,SUM> (row segments) "
+                               "concurrent with k_long<VPL2,MUL,SUM> (long rows)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": dominant[2],
