@@ -56,6 +56,9 @@ const char* operand_name(int o) {
 // GSPMM_SEG_EDGES / GSPMM_LONG_EDGES (the latter forces a single level).
 constexpr uint32_t kSegEdges = 1024;
 constexpr uint32_t kLongEdges = 4096;
+// rows above this many edges are cut into 32-column slices so several CTAs
+// stream one row (the 66k-329k-edge hubs of the power-law configs)
+constexpr uint32_t kXlEdges = 16384;
 
 uint32_t env_u32(const char* name, uint32_t dflt) {
   const char* v = std::getenv(name);
@@ -80,6 +83,7 @@ struct gspmm_graph_s {
     uint32_t threshold = 0;
     uint32_t* d_long = nullptr;  // long rows, heaviest first
     uint32_t num_long = 0;
+    uint32_t num_xl = 0;         // leading long rows above kXlEdges (narrow slices)
     uint64_t long_edges = 0;     // edges in long rows (sizes the long-row grid)
     uint2* d_segs = nullptr;     // segments of consecutive non-long rows
     uint32_t num_segs = 0;
@@ -316,9 +320,10 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
   } else if ((kind = plan_kernel(b.L, &rw)) != 0) {
     StreamLaunch p;
     p.row = b.L;
-    // plan level: rows gathering more than ~1 MB go to the long-row CTAs
+    // plan level: rows gathering more than ~8 MB go to the long-row CTAs
+    // (measured: 4096 edges of 1 KB, 16384 of 400 B; heaviest segments run first)
     const int slice_bytes = 4 * std::min(b.L.width, 256);
-    const uint32_t target = std::max<uint32_t>(1024, (1u << 20) / static_cast<uint32_t>(slice_bytes));
+    const uint32_t target = std::max<uint32_t>(1024, (8u << 20) / static_cast<uint32_t>(slice_bytes));
     int li = 0;
     for (int k = 0; k < g->n_levels; ++k)
       if (g->level[k].threshold <= target) li = k;
@@ -373,7 +378,13 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
       pl.mode = 1;
       pl.long_sw = W <= 256 ? W : 256;
       pl.long_slices = static_cast<uint32_t>((W + pl.long_sw - 1) / pl.long_sw);
-      pl.n_long_units = pl.n_long * pl.long_slices;
+      static const bool long_tma = env_u32("GSPMM_LONG_TMA", 0) != 0;
+      pl.long_tma = long_tma;
+      pl.n_xl = long_tma || W <= 32 ? 0 : lv.num_xl;
+      pl.xl_sw = 32;
+      pl.xl_slices = static_cast<uint32_t>((W + 31) / 32);
+      pl.n_xl_units = pl.n_xl * pl.xl_slices;
+      pl.n_long_units = pl.n_xl_units + (pl.n_long - pl.n_xl) * pl.long_slices;
       pl.n_units = pl.n_long_units;
       pl.counter = g->d_counter + 1;
       {
@@ -382,6 +393,8 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
         static const uint32_t forced = env_u32("GSPMM_LONG_CTAS", 0);
         const double share = g->m ? static_cast<double>(lv.long_edges) / g->m : 0.0;
         uint32_t c = forced ? forced : static_cast<uint32_t>(share * g->num_sms * 2.0 + 1.0);
+        // the narrow slices of the heaviest rows must run side by side
+        c = std::max<uint32_t>(c, std::min<uint32_t>(pl.n_xl_units, g->num_sms / 2));
         pl.long_ctas = std::min<uint32_t>(std::max<uint32_t>(c, 1), g->num_sms);
       }
       p.mode = 0;
@@ -546,7 +559,7 @@ int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
   // segments of consecutive non-long rows, for each long-row threshold.
   const uint32_t seg_edges = env_u32("GSPMM_SEG_EDGES", kSegEdges);
   const uint32_t forced_long = env_u32("GSPMM_LONG_EDGES", 0);
-  const uint32_t thresholds[3] = {1024, 2048, kLongEdges};
+  const uint32_t thresholds[3] = {1024, kLongEdges, 16384};
   g->n_levels = forced_long ? 1 : 3;
   std::vector<uint32_t> long_rows[3];
   std::vector<uint2> segs[3];
@@ -573,10 +586,18 @@ int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
       }
     }
     if (num_rows > begin) segs[k].push_back(make_uint2(begin, num_rows));
+    // heaviest segments first: a segment holding one near-threshold row is the
+    // longest unit, and it must not start last
+    std::stable_sort(segs[k].begin(), segs[k].end(), [&](const uint2& a, const uint2& b) {
+      return indptr[a.y] - indptr[a.x] > indptr[b.y] - indptr[b.x];
+    });
     std::stable_sort(long_rows[k].begin(), long_rows[k].end(), [&](uint32_t a, uint32_t b) {
       return indptr[a + 1] - indptr[a] > indptr[b + 1] - indptr[b];
     });
     lv.num_long = static_cast<uint32_t>(long_rows[k].size());
+    const uint32_t xl_edges = env_u32("GSPMM_XL_EDGES", kXlEdges);
+    for (uint32_t r : long_rows[k])
+      if (indptr[r + 1] - indptr[r] > xl_edges) ++lv.num_xl;
     lv.num_segs = static_cast<uint32_t>(segs[k].size());
   }
 

@@ -279,28 +279,38 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
 }
 
 // -------------------------------------------------------------- LONG ROWS
-// One long row (a column slice of <= 256 floats of it) per CTA: the 16 warps
-// gather a round of R edges with LDG.128 into registers while the previous
-// round, staged in shared memory, is folded by the column owners (thread t
-// owns column t) in canonical edge order.  A lone warp cannot keep enough
-// bytes in flight for a 66k-329k-edge row (one owner must see every edge in
-// order); a CTA keeps ~128 KB in flight for it.
+// One column slice (32 / 64 / 128 / 256 floats) of one long row per CTA: the
+// 16 warps gather a round of R edges with LDG.128 into registers while the
+// previous round, staged in shared memory, is folded by the column owners
+// (thread t owns column t) in canonical edge order.  A lone warp cannot keep
+// enough bytes in flight for a 66k-329k-edge row (one owner must see every
+// edge in order); a CTA keeps ~128 KB in flight, and the heaviest rows are
+// cut into narrow slices so several CTAs on several SMs stream one row.
+// Narrow slices pack epi = 128 / slice edges into each warp load instruction
+// (lane = edge group g x column quad i).
 constexpr int kLongThreads = 512;
 
+// Shared memory is carved out of the same 228 KB as L1, and L1 tracks the
+// in-flight LDG misses: the round buffer is kept at 96 KB (measured: a 192 KB
+// carve-out halved the long-row stream rate).
 template <int VPL>
 struct LongGeom {
-  static constexpr int U = VPL == 1 ? 16 : 8;          // edges per warp per round
-  static constexpr int R = (kLongThreads / 32) * U;    // edges per round
+  static constexpr int U = VPL == 1 ? 12 : 6;          // load instructions per warp per round
+  static constexpr int kWarps = kLongThreads / 32;
   static constexpr int kMaxSmall = 16;                  // staged small floats per edge
-  static constexpr size_t smem_bytes(int slot_f) {
-    return sizeof(float) * (static_cast<size_t>(R) * slot_f + static_cast<size_t>(R) * kMaxSmall);
+  // round: R = kWarps * U * epi edges of slot_f floats; slot_f * epi = 128
+  // for narrow slices, 128 * VPL otherwise -> the data buffer is constant
+  static constexpr size_t data_floats() { return static_cast<size_t>(kWarps) * U * 128 * VPL; }
+  static constexpr size_t max_edges() { return static_cast<size_t>(kWarps) * U * 4; }
+  static constexpr size_t smem_bytes(int rws) {
+    return sizeof(float) * (data_floats() + max_edges() * static_cast<size_t>(rws));
   }
 };
 
 template <int VPL, int BOP, int ROP, bool ARG, bool SMALL>
 __global__ void __launch_bounds__(kLongThreads, 1) k_long(const StreamLaunch p) {
   using G = LongGeom<VPL>;
-  constexpr int U = G::U, R = G::R;
+  constexpr int U = G::U;
   extern __shared__ __align__(16) float sm[];
   __shared__ uint32_t s_unit;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -309,6 +319,8 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long(const StreamLaunch p) 
   const bool scale_on = SMALL && L.other_scale != nullptr;
   const int rws = SMALL ? (rw > 0 ? rw : 1) : 0;  // staged small floats per edge
   const bool need_eid = L.lhs.role == ROLE_EID || (rw && L.rhs.role == ROLE_EID);
+  float* buf = sm;
+  float* sbuf = sm + G::data_floats();
 
   for (;;) {
     if (tid == 0) s_unit = atomicAdd(p.counter, 1u);
@@ -317,75 +329,104 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long(const StreamLaunch p) 
     __syncthreads();
     if (unit >= p.n_units) break;
     const unsigned long long t0 = p.trace ? globaltimer_ns() : 0ull;
-    const uint32_t li = unit / p.long_slices;
-    const uint32_t slc = unit - li * p.long_slices;
+    // units: first the narrow slices of the heaviest rows, then wide slices
+    uint32_t li, slc;
+    int sw;
+    if (unit < p.n_xl_units) {
+      li = unit / p.xl_slices;
+      slc = unit - li * p.xl_slices;
+      sw = p.xl_sw;
+    } else {
+      const uint32_t v = unit - p.n_xl_units;
+      li = p.n_xl + v / p.long_slices;
+      slc = v - (li - p.n_xl) * p.long_slices;
+      sw = p.long_sw;
+    }
     const uint32_t r = __ldg(p.long_rows + li);
-    const int c0 = static_cast<int>(slc) * p.long_sw;
-    const int cw = min(p.long_sw, L.width - c0);
-    const int slot_f = (cw + 3) & ~3;
-    float* buf = sm;
-    float* sbuf = sm + static_cast<size_t>(R) * slot_f;
+    const int c0 = static_cast<int>(slc) * sw;
+    const int cw = min(sw, L.width - c0);
+    const int slot_f = cw <= 32 ? 32 : cw <= 64 ? 64 : cw <= 128 ? 128 : 256;
+    const int epi = slot_f > 128 ? 1 : 128 / slot_f;  // edges per warp load instruction
+    const int lpe = 32 / epi;                          // lanes per edge
+    const int g = lane / lpe, i = lane - g * lpe;
+    const int epw = U * epi;                           // edges per warp per round
+    const uint32_t R = static_cast<uint32_t>(G::kWarps * epw);
     const uint32_t e0 = __ldg(L.indptr + r), e1 = __ldg(L.indptr + r + 1);
     const uint32_t n = e1 - e0;
     const uint32_t rounds = (n + R - 1) / R;
-    const float* lbase = L.lhs.base + c0 + lane * 4;
+    const float* lbase = L.lhs.base + c0 + i * 4;
     bool col_ok[VPL];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) col_ok[v] = lane * 4 + v * 128 < cw;
+    for (int v = 0; v < VPL; ++v) col_ok[v] = i * 4 + v * 128 < cw && (v == 0 || slot_f > 128);
+    int hv[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) hv[v] = (SMALL && rw > 1) ? (c0 + i * 4 + v * 128) / L.rhs.group : 0;
 
-    // ids of this warp's U edges of a round: lane k < U <-> edge k
-    auto load_ids = [&](uint32_t rd, uint32_t& o, uint32_t& e) {
-      const uint32_t j = e0 + rd * R + warp * U + lane;
-      if (lane < U && j < e1) {
-        o = __ldg(L.indices + j);
-        if (need_eid) e = __ldg(L.eids + j);
+    // ids of this warp's epw (<= 64) edges of a round: two 32-id windows
+    auto load_ids = [&](uint32_t rd, uint32_t (&o)[2], uint32_t (&e)[2]) {
+      const uint32_t jb = e0 + rd * R + warp * epw;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t j = jb + 32u * h + lane;
+        if (32 * h < epw && static_cast<int>(32 * h + lane) < epw && j < e1) {
+          o[h] = __ldg(L.indices + j);
+          if (need_eid) e[h] = __ldg(L.eids + j);
+        }
       }
     };
     float4 x[U][VPL];
-    float sv[G::kMaxSmall];  // lane k < U: small operand of edge k
-    auto issue = [&](uint32_t rd, uint32_t o_win, uint32_t e_win) {
-      const uint32_t jb = e0 + rd * R + warp * U;
+    float sv[U][VPL];
+    auto issue = [&](uint32_t rd, const uint32_t (&o_w)[2], const uint32_t (&e_w)[2]) {
+      const uint32_t jb = e0 + rd * R + warp * epw;
 #pragma unroll
       for (int k = 0; k < U; ++k) {
-        const uint32_t o = __shfl_sync(kFull, o_win, k);
-        const uint32_t e = need_eid ? __shfl_sync(kFull, e_win, k) : 0u;
-        if (jb + k < e1) {
-          const float* src = lbase + operand_row(L.lhs.role, 0, o, e, jb + k) * L.lhs.ld;
+        const int q = k * epi + g;  // edge of this lane within the warp's chunk
+        const uint32_t o0 = __shfl_sync(kFull, o_w[0], q & 31);
+        const uint32_t o1 = __shfl_sync(kFull, o_w[1], q & 31);
+        const uint32_t o = q < 32 ? o0 : o1;
+        uint32_t e = 0;
+        if (need_eid) {
+          const uint32_t a0 = __shfl_sync(kFull, e_w[0], q & 31);
+          const uint32_t a1 = __shfl_sync(kFull, e_w[1], q & 31);
+          e = q < 32 ? a0 : a1;
+        }
+        const uint32_t j = jb + q;
+        if (j < e1) {
+          const float* src = lbase + operand_row(L.lhs.role, 0, o, e, j) * L.lhs.ld;
 #pragma unroll
           for (int v = 0; v < VPL; ++v)
             if (col_ok[v]) x[k][v] = __ldg(reinterpret_cast<const float4*>(src + v * 128));
-        }
-      }
-      if constexpr (SMALL) {
-        const uint32_t j = jb + lane;
-        if (lane < U && j < e1) {
-          if (rw > 0) {
-            const float* src = L.rhs.base + operand_row(L.rhs.role, 0, o_win, e_win, j) * L.rhs.ld;
+          if constexpr (SMALL) {
 #pragma unroll
-            for (int h = 0; h < G::kMaxSmall; ++h)
-              if (h < rw) sv[h] = __ldg(src + h);
-          } else if (scale_on) {
-            sv[0] = __ldg(L.other_scale + o_win);
+            for (int v = 0; v < VPL; ++v) {
+              if (rw > 0) {
+                sv[k][v] = col_ok[v]
+                    ? __ldg(L.rhs.base + operand_row(L.rhs.role, 0, o, e, j) * L.rhs.ld + hv[v])
+                    : 0.0f;
+              } else if (scale_on) {
+                sv[k][v] = __ldg(L.other_scale + o);
+              }
+            }
           }
         }
       }
     };
     auto stage = [&](uint32_t rd) {
-      const uint32_t jb = e0 + rd * R + warp * U;
+      const uint32_t jb = e0 + rd * R + warp * epw;
 #pragma unroll
       for (int k = 0; k < U; ++k) {
-        if (jb + k < e1) {
-          float* dst = buf + static_cast<size_t>(warp * U + k) * slot_f + lane * 4;
+        const int q = k * epi + g;
+        if (jb + q < e1) {
+          const int eidx = warp * epw + q;  // edge within the round
+          float* dst = buf + static_cast<size_t>(eidx) * slot_f + i * 4;
 #pragma unroll
           for (int v = 0; v < VPL; ++v)
             if (col_ok[v]) *reinterpret_cast<float4*>(dst + v * 128) = x[k][v];
-        }
-      }
-      if constexpr (SMALL) {
-        if (lane < U && jb + lane < e1) {
+          if constexpr (SMALL) {
 #pragma unroll
-          for (int h = 0; h < G::kMaxSmall; ++h)
-            if (h < rws) sbuf[(warp * U + lane) * rws + h] = sv[h];
+            for (int v = 0; v < VPL; ++v)
+              if (col_ok[v]) sbuf[eidx * rws + hv[v]] = sv[k][v];
+          }
         }
       }
     };
@@ -394,7 +435,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long(const StreamLaunch p) 
     float acc = red_identity<ROP>();
     uint32_t arg = 0xffffffffu;
     const int hcol = (SMALL && rw > 1) ? (c0 + tid) / L.rhs.group : 0;
-    uint32_t ida = 0, idea = 0, idb = 0, ideb = 0;
+    uint32_t ida[2] = {0, 0}, idea[2] = {0, 0}, idb[2] = {0, 0}, ideb[2] = {0, 0};
     load_ids(0, ida, idea);
     load_ids(1, idb, ideb);
     issue(0, ida, idea);
@@ -406,7 +447,7 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long(const StreamLaunch p) 
         load_ids(k + 2, idb, ideb);
       }
       if (tid < cw) {
-        const uint32_t cnt = min(static_cast<uint32_t>(R), n - k * R);
+        const uint32_t cnt = min(R, n - k * R);
         const float* col = buf + tid;
         const int soff = SMALL && rw > 0 ? hcol : 0;
 #pragma unroll 4
@@ -452,6 +493,205 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long(const StreamLaunch p) 
       t[0] = t0;
       t[1] = globaltimer_ns();
       t[2] = (static_cast<unsigned long long>(smid()) << 32) | 0xffffu;
+      t[3] = n;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------ LONG ROWS via TMA
+// Warp-specialised variant for slices of >= 512 B: warp 8 is the producer
+// (lane 0 issues one cp.async.bulk per edge into a shared-memory ring of
+// 8-edge stages, ~200 KB deep; lanes 0-7 stage the small operand with
+// cp.async on the same full barrier), warps 0-7 are the 256 column owners
+// that fold each stage in edge order and release it on the empty barrier.
+// The SM's TMA engine is otherwise idle (segments gather with LDG), and a
+// full-row TMA request per edge keeps ~200 edges in flight for one row.
+constexpr int kLtConsumers = 8;                      // warps folding
+constexpr int kLtThreads = (kLtConsumers + 1) * 32;  // + producer warp
+constexpr int kLtMaxStages = 32;
+constexpr int kLtRingBytes = 200 * 1024;
+constexpr int kIdWin = 8;  // id windows in flight (producer)
+
+__host__ __device__ constexpr size_t lt_smem_bytes() {
+  return kLtRingBytes + 2 * kLtMaxStages * sizeof(uint64_t) + 2 * kIdWin * 32 * sizeof(uint32_t);
+}
+
+template <int BOP, int ROP, bool ARG, bool SMALL>
+__global__ void __launch_bounds__(kLtThreads, 1) k_long_tma(const StreamLaunch p) {
+  extern __shared__ __align__(128) unsigned char lt_smem[];
+  __shared__ uint32_t s_unit;
+  float* ring = reinterpret_cast<float*>(lt_smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(lt_smem + kLtRingBytes);
+  uint64_t* empty = full + kLtMaxStages;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool producer = warp == kLtConsumers;
+  const RowLaunch& L = p.row;
+  const int rw = SMALL ? p.rhs_width : 0;
+  const bool scale_on = SMALL && L.other_scale != nullptr;
+  const int rws = SMALL ? (rw > 0 ? rw : 1) : 0;
+  const bool need_eid = L.lhs.role == ROLE_EID || (rw && L.rhs.role == ROLE_EID);
+  if (tid == 0) {
+    for (int b = 0; b < kLtMaxStages; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], kLtConsumers);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t full_phase = 0, empty_phase = 0;  // per-stage parity bits (per role)
+
+  for (;;) {
+    if (tid == 0) s_unit = atomicAdd(p.counter, 1u);
+    __syncthreads();
+    const uint32_t unit = s_unit;
+    __syncthreads();
+    if (unit >= p.n_units) break;
+    const unsigned long long t0 = p.trace ? globaltimer_ns() : 0ull;
+    const uint32_t li = unit / p.long_slices;
+    const uint32_t slc = unit - li * p.long_slices;
+    const uint32_t r = __ldg(p.long_rows + li);
+    const int c0 = static_cast<int>(slc) * p.long_sw;
+    const int cw = min(p.long_sw, L.width - c0);
+    const int slot_f = (cw + 3) & ~3;
+    const uint32_t slot_bytes = static_cast<uint32_t>(slot_f) * 4u;
+    int nst = kLtRingBytes / (8 * 4 * (slot_f + rws));
+    nst = nst > kLtMaxStages ? kLtMaxStages : nst;
+    float* tab = ring + static_cast<size_t>(nst) * 8 * slot_f;  // small operand per slot
+    const uint32_t e0 = __ldg(L.indptr + r), e1 = __ldg(L.indptr + r + 1);
+    const uint32_t n = e1 - e0;
+    const uint32_t n_stages = (n + 7) / 8;
+
+    if (producer) {
+      const float* lbase = L.lhs.base + c0;
+      // ids staged kIdWin windows (x32 edges) ahead through a shared ring with
+      // cp.async groups: the producer never waits on a fresh global load
+      uint32_t* id_o = reinterpret_cast<uint32_t*>(lt_smem + kLtRingBytes +
+                                                   2 * kLtMaxStages * sizeof(uint64_t));
+      uint32_t* id_e = id_o + kIdWin * 32;
+      auto load_win = [&](uint32_t w) {
+        const uint32_t j = e0 + 32u * w + lane;
+        const int sl = static_cast<int>(w % kIdWin) * 32 + lane;
+        if (j < e1) {
+          cp_async_4(id_o + sl, L.indices + j);
+          if (need_eid) cp_async_4(id_e + sl, L.eids + j);
+        }
+        cp_async_commit();
+      };
+      for (uint32_t w = 0; w < static_cast<uint32_t>(kIdWin); ++w) load_win(w);
+      for (uint32_t s = 0; s < n_stages; ++s) {
+        const int b = static_cast<int>(s % static_cast<uint32_t>(nst));
+        if (s >= static_cast<uint32_t>(nst)) {  // wait for the consumers to free it
+          mbar_wait(&empty[b], (empty_phase >> b) & 1u);
+          empty_phase ^= 1u << b;
+        }
+        if ((s & 3u) == 0) {  // entering id window s/4
+          if (s != 0) load_win((s >> 2) + kIdWin - 1);
+          cp_async_wait_group<kIdWin - 1>();
+          __syncwarp();
+        }
+        const uint32_t j0 = e0 + s * 8u;
+        const uint32_t cnt = min(8u, e1 - j0);
+        const int src = static_cast<int>(((s >> 2) % kIdWin) * 32 + (s & 3u) * 8u) + (lane & 7);
+        const uint32_t o = id_o[src];
+        const uint32_t e = need_eid ? id_e[src] : 0u;
+        // issuing lanes rotate over the warp (stage s uses lanes 8*(s%4) ..
+        // +7): bulk copies outstanding per issuing thread are limited
+        const uint32_t lbase8 = (s & 3u) * 8u;
+        const bool issuer = static_cast<uint32_t>(lane) >= lbase8 &&
+                            static_cast<uint32_t>(lane) < lbase8 + 8u;
+        const uint32_t l = static_cast<uint32_t>(lane) - lbase8;  // edge of this lane
+        const int slot = b * 8 + static_cast<int>(l);
+        if constexpr (SMALL) {
+          if (issuer && l < cnt) {
+            if (rw > 0) {
+              const float* sp = L.rhs.base + operand_row(L.rhs.role, 0, o, e, j0 + l) * L.rhs.ld;
+              for (int h = 0; h < rw; ++h) cp_async_4(tab + slot * rws + h, sp + h);
+            } else if (scale_on) {
+              cp_async_4(tab + slot, L.other_scale + o);
+            }
+          }
+          if (issuer) cp_async_arrive(&full[b]);
+          __syncwarp();
+        }
+        if (lane == 0) mbar_arrive_expect_tx(&full[b], cnt * slot_bytes);
+        __syncwarp();
+        if (issuer && l < cnt)
+          tma_load_1d(ring + slot * slot_f,
+                      lbase + operand_row(L.lhs.role, 0, o, e, j0 + l) * L.lhs.ld, slot_bytes,
+                      &full[b]);
+      }
+      // drain: the last min(nst, n_stages) stages' empties are consumed here
+      // so both roles enter the next unit with matching phases
+      const uint32_t tail = min(static_cast<uint32_t>(nst), n_stages);
+      for (uint32_t s = n_stages - tail; s < n_stages; ++s) {
+        const int b = static_cast<int>(s % static_cast<uint32_t>(nst));
+        mbar_wait(&empty[b], (empty_phase >> b) & 1u);
+        empty_phase ^= 1u << b;
+      }
+    } else {
+      // consumers: thread tid owns column c0 + tid
+      float acc = red_identity<ROP>();
+      uint32_t arg = 0xffffffffu;
+      const bool own = tid < cw;
+      const int hcol = (SMALL && rw > 1) ? (c0 + tid) / L.rhs.group : 0;
+      for (uint32_t s = 0; s < n_stages; ++s) {
+        const int b = static_cast<int>(s % static_cast<uint32_t>(nst));
+        mbar_wait(&full[b], (full_phase >> b) & 1u);
+        full_phase ^= 1u << b;
+        const uint32_t cnt = min(8u, n - s * 8u);
+        if (own) {
+          float mv[8], sv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            mv[q] = ring[static_cast<size_t>(b * 8 + q) * slot_f + tid];
+            if constexpr (SMALL) sv[q] = tab[(b * 8 + q) * rws + hcol];
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (static_cast<uint32_t>(q) < cnt) {
+              float m;
+              if constexpr (SMALL) {
+                m = rw > 0 ? bin_apply<BOP>(mv[q], sv[q])
+                           : __fmul_rn(bin_apply<BOP>(mv[q], 0.0f), sv[q]);
+              } else {
+                m = bin_apply<BOP>(mv[q], 0.0f);
+              }
+              if constexpr (ARG) {
+                if (red_wins<ROP>(acc, m)) {
+                  acc = m;
+                  arg = e0 + s * 8u + q;
+                }
+              } else {
+                acc = red_combine<ROP>(acc, m);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[b]);
+      }
+      if (own) {
+        float a = acc;
+        if constexpr (ROP == R_MAX || ROP == R_MIN) {
+          if (n == 0) a = 0.0f;
+        }
+        if (L.mean) a = n ? __fdiv_rn(a, __uint2float_rn(n)) : 0.0f;
+        L.out[static_cast<int64_t>(r) * L.out_ld + c0 + tid] = a;
+        if constexpr (ARG) {
+          const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + tid;
+          const bool none = arg == 0xffffffffu;
+          if (L.arg_other)
+            L.arg_other[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.indices + arg));
+          if (L.arg_edge) L.arg_edge[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.eids + arg));
+        }
+      }
+    }
+    if (p.trace && tid == 0) {
+      unsigned long long* t = p.trace + 4ull * unit;
+      t[0] = t0;
+      t[1] = globaltimer_ns();
+      t[2] = (static_cast<unsigned long long>(smid()) << 32) | 0xfffeu;
       t[3] = n;
     }
     __syncthreads();
@@ -505,16 +745,31 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const int sms = p.row.num_sms > 0 ? p.row.num_sms : 148;
-  if (p.mode == 1) {
-    const int slot_f = (p.long_sw + 3) & ~3;
-    const size_t smem = LongGeom<VPL>::smem_bytes(slot_f);
+  if (p.mode == 1 && p.long_tma) {
+    // wide long-row slices: TMA-fed, warp-specialised CTAs
+    static int configured_t = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_t != dev) {
+      e = cudaFuncSetAttribute(k_long_tma<BOP, ROP, ARG, SMALL>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(lt_smem_bytes()));
+      if (e != cudaSuccess) return e;
+      configured_t = dev;
+    }
+    unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
+    if (grid > p.n_units) grid = p.n_units;
+    k_long_tma<BOP, ROP, ARG, SMALL><<<grid, kLtThreads, lt_smem_bytes(), s>>>(p);
+  } else if (p.mode == 1) {
+    const int rws = SMALL ? (p.rhs_width > 0 ? p.rhs_width : 1) : 0;
+    const size_t smem = LongGeom<VPL>::smem_bytes(rws);
     static int configured = -1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured != dev) {
       e = cudaFuncSetAttribute(k_long<VPL, BOP, ROP, ARG, SMALL>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(LongGeom<VPL>::smem_bytes(VPL == 1 ? 128 : 256)));
+                               static_cast<int>(LongGeom<VPL>::smem_bytes(LongGeom<VPL>::kMaxSmall)));
       if (e != cudaSuccess) return e;
       configured = dev;
     }

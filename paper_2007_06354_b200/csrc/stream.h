@@ -21,6 +21,12 @@ struct StreamLaunch {
   int rhs_width = 0;      // staged floats per edge of the small operand (0 = none)
   int mode = 0;           // gather.cu: 0 = row segments, 1 = long rows (one per CTA)
   uint32_t long_ctas = 0; // gather.cu mode 1: grid size (0 = one per SM)
+  // gather.cu mode 1: the first n_xl long rows (heaviest) are cut into
+  // xl_slices narrow slices of xl_sw columns (units [0, n_xl_units)), the
+  // rest into long_slices slices of long_sw columns
+  uint32_t n_xl = 0, xl_slices = 1, n_xl_units = 0;
+  int xl_sw = 32;
+  bool long_tma = false;  // GSPMM_LONG_TMA=1: warp-specialised TMA long rows
   // Units whose gathered slice is narrower than this many bytes stage rows
   // with per-lane 16-byte cp.async (LSU path) instead of one TMA bulk copy
   // per edge: small bulk copies are bound by the TMA request rate.

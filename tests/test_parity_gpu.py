@@ -425,3 +425,25 @@ np.save(sys.argv[2], out.cpu().numpy())
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(path))
     assert O.bit_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("xl", [1, 50])
+def test_narrow_slices_of_heaviest_rows(xl, monkeypatch):
+    # rows above GSPMM_XL_EDGES are cut into 32-column slices streamed by
+    # several CTAs; results stay bitwise for every width
+    monkeypatch.setenv("GSPMM_XL_EDGES", str(xl))
+    rng = np.random.default_rng(7)
+    n = 3000
+    src = np.concatenate([rng.integers(0, n, 40000), rng.integers(0, n, 30000)]).astype(np.uint32)
+    dst = np.concatenate([np.zeros(40000, np.int64) + 5, rng.integers(0, n, 30000)]).astype(np.uint32)
+    g = O.Graph(n, src, dst)
+    w = O.gcn_weights(n, src, dst)
+    for dim in (20, 100, 128, 256, 300):
+        x = O.normal_features(n, dim, dim)
+        for cfg, kw in (((O.U, O.E, O.MUL, O.SUM, O.V), dict(u=x, e=w)),
+                        ((O.U, O.NONE, O.COPY, O.MAX, O.V), dict(u=x))):
+            assert O.bit_equal(gpu_reduce(g, cfg, **kw), O.binary_reduce(g, cfg, **kw)), (xl, dim)
+        val, au, _ = gpu_reduce(g, (O.U, O.NONE, O.COPY, O.MAX, O.V), u=x, want_arg_other=True)
+        v2, au2, _ = O.copy_max_argmax(g, x)
+        assert O.bit_equal(val, v2) and (au == au2).all()
+        g.__dict__.pop("_dev", None)
