@@ -221,6 +221,15 @@ int gspmm_transpose(uint32_t num_rows, uint32_t num_cols,
 /* U[-1,1) (random_features, generate.cpp:256-266) and builder N(0,1) */
 void gspmm_synth_uniform(int64_t count, uint64_t seed, float* out, int threads);
 void gspmm_synth_normal(int64_t count, uint64_t seed, float* out, int threads);
+/* Power-law in-degree graph (cfg5, GraphSAGE-mean on a Reddit-shaped graph;
+ * builder-defined): node v draws its in-degree from the discrete
+ * inverse CDF of P(d) ~ d^-2 on [d_min, d_max] with u01(seed, v); its edges
+ * follow in edge-id order, each source uniform on [0, n) by the 128-bit
+ * multiply-shift of splitmix64(seed ^ 0x5851f42d4c957f2d, edge id).
+ * Call with src/dst NULL to get the edge count. */
+int64_t gspmm_synth_powerlaw(uint32_t n, uint32_t d_min, uint32_t d_max,
+                             uint64_t seed, uint32_t* src, uint32_t* dst,
+                             int threads);
 /* GCN weight w[e] = 1/sqrt(deg_out(src[e]) * deg_in(dst[e])), edge-id order */
 void gspmm_synth_gcn_weights(uint32_t n, int64_t m, const uint32_t* src,
                              const uint32_t* dst, float* w, int threads);

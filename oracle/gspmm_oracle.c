@@ -224,6 +224,38 @@ int64_t or_gen_rmat(uint32_t n, uint64_t num_edges, double a, double b,
 
 void or_free(void* p) { free(p); }
 
+/* Builder-defined power-law in-degree generator for cfg5 (the reference has
+ * none): in-degree of node v from the inverse CDF of P(d) ~ d^-2
+ * on [d_min, d_max] at u01(seed, v); edges in edge-id order grouped by
+ * destination, source of edge e = (splitmix64(seed ^ 0x5851f42d4c957f2d, e)
+ * * n) >> 64.  Restated independently of the product's synth.cpp. */
+int64_t or_gen_powerlaw(uint32_t n, uint32_t d_min, uint32_t d_max, uint64_t seed,
+                        uint32_t** src, uint32_t** dst) {
+  const double a = 1.0 / d_min, b = 1.0 / d_min - 1.0 / d_max;
+  uint64_t m = 0;
+  uint32_t* deg = (uint32_t*)malloc((size_t)(n ? n : 1) * sizeof(uint32_t));
+  for (uint32_t v = 0; v < n; ++v) {
+    double d = floor(1.0 / (a - or_u01_at(seed, v) * b));
+    if (d < d_min) d = d_min;
+    if (d > d_max) d = d_max;
+    deg[v] = (uint32_t)d;
+    m += deg[v];
+  }
+  uint32_t* s = (uint32_t*)malloc((size_t)(m ? m : 1) * sizeof(uint32_t));
+  uint32_t* t = (uint32_t*)malloc((size_t)(m ? m : 1) * sizeof(uint32_t));
+  const uint64_t seed2 = seed ^ 0x5851f42d4c957f2dULL;
+  uint64_t e = 0;
+  for (uint32_t v = 0; v < n; ++v)
+    for (uint32_t k = 0; k < deg[v]; ++k, ++e) {
+      s[e] = (uint32_t)(((unsigned __int128)or_splitmix64_at(seed2, e) * n) >> 64);
+      t[e] = v;
+    }
+  free(deg);
+  *src = s;
+  *dst = t;
+  return (int64_t)m;
+}
+
 /* random_features, generate.cpp:256-266 */
 void or_random_features(int64_t rows, int64_t dim, uint64_t seed, float* out) {
   const int64_t total = rows * dim;

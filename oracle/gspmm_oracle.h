@@ -49,6 +49,8 @@ int64_t or_gen_rmat(uint32_t n, uint64_t num_edges, double a, double b,
 int64_t or_gen_sbm(uint32_t n, int blocks, double p_in, double p_out,
                    uint64_t seed, uint32_t** src, uint32_t** dst);
 void or_free(void* p);
+int64_t or_gen_powerlaw(uint32_t n, uint32_t d_min, uint32_t d_max, uint64_t seed,
+                        uint32_t** src, uint32_t** dst);
 void or_random_features(int64_t rows, int64_t dim, uint64_t seed, float* out);
 void or_normal_features(int64_t count, uint64_t seed, float* out);
 void or_normal_features_at(int64_t offset, int64_t count, uint64_t seed, float* out);

@@ -76,6 +76,7 @@ def _load_c():
         "or_gen_rmat": (i64, [u32, u64, dbl, dbl, dbl, dbl, u64, C.POINTER(_u32p), C.POINTER(_u32p)]),
         "or_gen_sbm": (i64, [u32, i32, dbl, dbl, u64, C.POINTER(_u32p), C.POINTER(_u32p)]),
         "or_free": (None, [vp]),
+        "or_gen_powerlaw": (i64, [u32, u32, u32, u64, C.POINTER(_u32p), C.POINTER(_u32p)]),
         "or_random_features": (None, [i64, i64, u64, vp]),
         "or_normal_features": (None, [i64, u64, vp]),
         "or_normal_features_at": (None, [i64, i64, u64, vp]),
@@ -201,6 +202,13 @@ def gen_rmat(n, num_edges, a=0.57, b=0.19, c=0.19, d=0.05, seed=0):
 def gen_sbm(n, blocks, p_in, p_out, seed=0):
     ps, pd = _u32p(), _u32p()
     m = LIB.or_gen_sbm(n, blocks, p_in, p_out, seed, C.byref(ps), C.byref(pd))
+    return _take_edges(m, ps, pd, LIB.or_free)
+
+
+def gen_powerlaw(n, d_min, d_max, seed=0):
+    """Builder-defined power-law in-degree graph (cfg5)."""
+    ps, pd = _u32p(), _u32p()
+    m = LIB.or_gen_powerlaw(n, d_min, d_max, seed, C.byref(ps), C.byref(pd))
     return _take_edges(m, ps, pd, LIB.or_free)
 
 

@@ -106,6 +106,7 @@ SIGNATURES = {
     "gspmm_synth_uniform": (None, [_i64, _u64, _vp, _i32]),
     "gspmm_synth_normal": (None, [_i64, _u64, _vp, _i32]),
     "gspmm_synth_gcn_weights": (None, [_u32, _i64, _vp, _vp, _vp, _i32]),
+    "gspmm_synth_powerlaw": (_i64, [_u32, _u32, _u32, _u64, _vp, _vp, _i32]),
 }
 
 

@@ -20,7 +20,7 @@ __all__ = [
     "Graph", "binary_reduce", "binary_reduce_host", "copy_reduce", "argmax_backward",
     "named_config", "validate_config", "required_orientation", "out_shape",
     "synth_rmat", "synth_er", "build_csr", "transpose", "synth_uniform", "synth_normal",
-    "synth_gcn_weights", "launch_count",
+    "synth_gcn_weights", "synth_powerlaw", "launch_count",
 ]
 
 
@@ -317,6 +317,17 @@ def synth_normal(rows, dim, seed, threads=0, out=None):
     out = np.empty((rows, dim), np.float32) if out is None else out
     A.LIB.gspmm_synth_normal(rows * dim, seed, out.ctypes.data, threads)
     return out
+
+
+def synth_powerlaw(n, d_min, d_max, seed=0, threads=0):
+    """Power-law in-degree graph (cfg5, see gspmm_synth_powerlaw)."""
+    m = A.LIB.gspmm_synth_powerlaw(n, d_min, d_max, seed, None, None, threads)
+    if m < 0:
+        raise A.ConfigError("powerlaw: bad parameters")
+    src = np.empty(max(m, 1), np.uint32)
+    dst = np.empty(max(m, 1), np.uint32)
+    A.LIB.gspmm_synth_powerlaw(n, d_min, d_max, seed, _ptr(src), _ptr(dst), threads)
+    return src[:m], dst[:m]
 
 
 def synth_gcn_weights(n, src, dst, threads=0):

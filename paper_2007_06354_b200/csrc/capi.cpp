@@ -91,6 +91,7 @@ struct gspmm_graph_s {
   Level level[3];
   int n_levels = 0;
   uint32_t* d_counter = nullptr;  // [0] segment units, [1] long-row units
+  uint32_t* d_rowof = nullptr;     // owner row of each CSR position (edge dots), lazy
   cudaStream_t side = nullptr;     // long-row kernel runs here concurrently
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int num_sms = 148;
@@ -315,7 +316,17 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int rw = 0;
   int kind = 0;
-  if (b.L.binop == GSPMM_DOT) {
+  if (b.L.binop == GSPMM_DOT && b.L.out_edge &&
+      (b.L.lhs.mode != MODE_FULL || (b.L.lhs.ld % 2 == 0 && aligned(b.L.lhs.base, 8))) &&
+      (b.L.rhs.mode != MODE_FULL || (b.L.rhs.ld % 2 == 0 && aligned(b.L.rhs.base, 8)))) {
+    // edge-destined dots stream edge batches; needs the row of each edge
+    if (!g->d_rowof) {
+      CUDA_TRY(cudaMalloc(&g->d_rowof, sizeof(uint32_t) * std::max<uint64_t>(g->m, 1)),
+               "row-of-edge array");
+      CUDA_TRY(launch_row_of_edge(g->d_indptr, g->num_rows, g->d_rowof, s), "row-of-edge");
+    }
+    err = launch_dot_edges(b.L, g->d_rowof, g->m, s);
+  } else if (b.L.binop == GSPMM_DOT) {
     err = launch_dot(b.L, s);
   } else if ((kind = plan_kernel(b.L, &rw)) != 0) {
     StreamLaunch p;
@@ -665,6 +676,7 @@ int gspmm_graph_destroy(gspmm_graph g) {
     cudaFree(lv.d_segs);
   }
   cudaFree(g->d_counter);
+  cudaFree(g->d_rowof);
   if (g->side) {
     cudaStreamDestroy(g->side);
     cudaEventDestroy(g->ev_fork);

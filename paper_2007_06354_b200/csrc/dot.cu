@@ -142,7 +142,121 @@ cudaError_t launch_dr(const RowLaunch& p, cudaStream_t s) {
   }
 }
 
+// ------------------------------------------------------- edge-destined dot
+// out == E (u_dot_v_copy_e: SDDMM scores, grad of edge weights, per-head
+// grad of attention): every edge is independent, so warps stream fixed
+// batches of 32 edges over the whole edge range (no row plan, no long-row
+// tail).  The owner row of edge j comes from the handle's row-of-edge array.
+// Per 64-column chunk the warp gathers both operand rows of each edge with
+// 64-bit loads (8 edges in flight), parks the products in a conflict-free
+// shared tile, and lane k folds edge k's products in column order.
+constexpr int kEdWarps = 4;
+constexpr int kEdCW = 64;             // columns per chunk (2 per lane)
+constexpr int kEdStride = kEdCW + 1;  // padded tile row
+
+__global__ void __launch_bounds__(kEdWarps * 32) k_dot_edges(const RowLaunch p,
+                                                             const uint32_t* __restrict__ rowof,
+                                                             uint64_t m) {
+  __shared__ float tiles[kEdWarps][32 * kEdStride];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* tile = tiles[warp];
+  const int G = p.gather_dim;
+  const int D = G / p.heads;
+  const uint64_t n_batches = (m + 31) / 32;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kEdWarps;
+  const bool l2 = p.lhs.mode == MODE_FULL, r2 = p.rhs.mode == MODE_FULL;
+  for (uint64_t bt = static_cast<uint64_t>(blockIdx.x) * kEdWarps + warp; bt < n_batches;
+       bt += stride) {
+    const uint64_t jb = bt * 32;
+    const int n = static_cast<int>(m - jb < 32 ? m - jb : 32);
+    uint32_t my_o = 0, my_e = 0, my_r = 0;
+    if (lane < n) {
+      my_o = __ldg(p.indices + jb + lane);
+      my_e = __ldg(p.eids + jb + lane);
+      my_r = __ldg(rowof + jb + lane);
+    }
+    float acc = 0.0f;
+    int head = 0;
+    for (int cb = 0; cb < G; cb += kEdCW) {
+      const int c0 = cb + lane * 2;
+      for (int i0 = 0; i0 < n; i0 += 8) {
+        float2 lv[8], rv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int i = i0 + k;
+          const uint32_t o = __shfl_sync(kFull, my_o, i & 31);
+          const uint32_t e = __shfl_sync(kFull, my_e, i & 31);
+          const uint32_t r = __shfl_sync(kFull, my_r, i & 31);
+          if (i < n && c0 < G) {
+            const uint32_t j = static_cast<uint32_t>(jb) + i;
+            const float* lp = p.lhs.base + operand_row(p.lhs.role, r, o, e, j) * p.lhs.ld;
+            const float* rp = p.rhs.base + operand_row(p.rhs.role, r, o, e, j) * p.rhs.ld;
+            if (l2) {
+              lv[k] = __ldg(reinterpret_cast<const float2*>(lp + c0));
+            } else {
+              lv[k].x = lv[k].y = __ldg(lp);
+            }
+            if (r2) {
+              rv[k] = __ldg(reinterpret_cast<const float2*>(rp + c0));
+            } else {
+              rv[k].x = rv[k].y = __ldg(rp);
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int i = i0 + k;
+          if (i < n) {
+            tile[i * kEdStride + lane] = c0 < G ? __fmul_rn(lv[k].x, rv[k].x) : 0.0f;
+            tile[i * kEdStride + 32 + lane] = c0 + 1 < G ? __fmul_rn(lv[k].y, rv[k].y) : 0.0f;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane < n) {
+        const int cend = min(kEdCW, G - cb);
+        for (int c = 0; c < cend; ++c) {
+          // column cb + c lives at tile column (c % 2) * 32 + c / 2
+          acc = __fadd_rn(acc, tile[lane * kEdStride + (c & 1) * 32 + (c >> 1)]);
+          if ((cb + c + 1) % D == 0) {
+            p.out[static_cast<int64_t>(my_e) * p.out_ld + head] = acc;
+            acc = 0.0f;
+            ++head;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void k_row_of_edge(const uint32_t* __restrict__ indptr, uint32_t rows,
+                              uint32_t* __restrict__ rowof) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride)
+    for (uint32_t j = __ldg(indptr + r); j < __ldg(indptr + r + 1); ++j) rowof[j] = r;
+}
+
 }  // namespace
+
+cudaError_t launch_row_of_edge(const uint32_t* indptr, uint32_t rows, uint32_t* rowof,
+                               cudaStream_t s) {
+  k_row_of_edge<<<148 * 8, 256, 0, s>>>(indptr, rows, rowof);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dot_edges(const RowLaunch& p, const uint32_t* rowof, uint64_t m,
+                             cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  const uint64_t batches = (m + 31) / 32;
+  uint64_t blocks = (batches + kEdWarps - 1) / kEdWarps;
+  const uint64_t cap = static_cast<uint64_t>(p.num_sms > 0 ? p.num_sms : 148) * 16;
+  if (blocks > cap) blocks = cap;
+  k_dot_edges<<<static_cast<unsigned>(blocks), kEdWarps * 32, 0, s>>>(p, rowof, m);
+  note_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_dot(const RowLaunch& p, cudaStream_t s) {
   switch (p.vec) {

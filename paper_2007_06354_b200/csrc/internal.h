@@ -66,6 +66,11 @@ struct RowLaunch {
 // Kernel launchers (rows.cu, dot.cu, aux.cu).  Return cudaGetLastError().
 cudaError_t launch_rows(const RowLaunch& p, cudaStream_t s);
 cudaError_t launch_dot(const RowLaunch& p, cudaStream_t s);
+// out == E dot over edge batches; rowof[j] = owner row of CSR position j
+cudaError_t launch_dot_edges(const RowLaunch& p, const uint32_t* rowof, uint64_t m,
+                             cudaStream_t s);
+cudaError_t launch_row_of_edge(const uint32_t* indptr, uint32_t rows, uint32_t* rowof,
+                               cudaStream_t s);
 cudaError_t launch_permute_edges(const uint32_t* eids, uint64_t m,
                                  const float* src, int64_t dim, int64_t src_ld,
                                  float* dst, int64_t dst_ld, cudaStream_t s);

@@ -336,6 +336,36 @@ void gspmm_synth_normal(int64_t count, uint64_t seed, float* out, int threads) {
   });
 }
 
+int64_t gspmm_synth_powerlaw(uint32_t n, uint32_t d_min, uint32_t d_max, uint64_t seed,
+                             uint32_t* src, uint32_t* dst, int threads) {
+  if (n == 0 || d_min == 0 || d_max < d_min) return -GSPMM_ERR_CONFIG;
+  // in-degree of node v: inverse CDF of P(d) ~ d^-2 on [d_min, d_max]
+  const double a = 1.0 / d_min, b = 1.0 / d_min - 1.0 / d_max;
+  std::vector<uint64_t> off(static_cast<size_t>(n) + 1, 0);
+  parallel_for(n, threads, [&](int64_t lo, int64_t hi, int) {
+    for (int64_t v = lo; v < hi; ++v) {
+      const double u = u01_at(seed, static_cast<uint64_t>(v));
+      double d = std::floor(1.0 / (a - u * b));
+      if (d < d_min) d = d_min;
+      if (d > d_max) d = d_max;
+      off[v + 1] = static_cast<uint64_t>(d);
+    }
+  });
+  for (uint32_t v = 0; v < n; ++v) off[v + 1] += off[v];
+  const uint64_t m = off[n];
+  if (!src || !dst) return static_cast<int64_t>(m);
+  const uint64_t seed2 = seed ^ 0x5851f42d4c957f2dULL;
+  parallel_chunks(n, 256, threads, [&](int64_t lo, int64_t hi) {
+    for (int64_t v = lo; v < hi; ++v)
+      for (uint64_t e = off[v]; e < off[v + 1]; ++e) {
+        const unsigned __int128 x = static_cast<unsigned __int128>(splitmix64_at(seed2, e)) * n;
+        src[e] = static_cast<uint32_t>(x >> 64);
+        dst[e] = static_cast<uint32_t>(v);
+      }
+  });
+  return static_cast<int64_t>(m);
+}
+
 void gspmm_synth_gcn_weights(uint32_t n, int64_t m, const uint32_t* src, const uint32_t* dst,
                              float* w, int threads) {
   std::vector<std::atomic<uint32_t>> dout(n), din(n);

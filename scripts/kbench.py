@@ -19,6 +19,8 @@ PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if 
 
 
 def graph(kind, n, m, seed=0, loops=False, sym=False):
+    if kind == "powerlaw":
+        return P.synth_powerlaw(n, 90, 21000, seed)
     if kind in ("er", "star"):
         src, dst = P.synth_er(n, m, -1.0, seed)
     else:
@@ -60,6 +62,10 @@ CASES = {
     "star256": ("star", 1_000_000, 16_000_000, 256, False, False, "gcn"),
     "rmat100sym": ("rmat", 2_449_029, 61_859_140, 100, False, True, "mean"),
     "rmat512h": ("rmat", 1_000_000, 32_000_000, 512, False, False, "heads"),
+    "cfg3max": ("rmat", 2_449_029, 61_859_140, 100, False, True, "maxarg"),
+    "cfg5mean": ("powerlaw", 232_965, 0, 602, False, False, "mean604"),
+    "cfg2dot": ("rmat", 1_000_000, 16_000_000, 256, True, False, "dot"),
+    "cfg4dot": ("rmat", 1_000_000, 32_000_000, 512, False, False, "dotheads"),
 }
 
 
@@ -87,6 +93,24 @@ def run(name):
     elif op == "mean":
         fn = lambda: P.binary_reduce(g, (P.U, P.NONE, P.COPY, P.MEAN, P.V), u=x, out=out)
         eb = 0
+    elif op == "mean604":  # F=602 rows padded to a 16-byte leading dimension
+        xp = torch.zeros(n, 604, device="cuda")
+        xp[:, :F] = x
+        op_ = torch.empty(n, 604, device="cuda")
+        fn = lambda: P.binary_reduce(g, (P.U, P.NONE, P.COPY, P.MEAN, P.V), u=xp[:, :F],
+                                     out=op_[:, :F])
+        eb = 0
+    elif op == "maxarg":
+        fn = lambda: P.binary_reduce(g, "u_copy_max_v", u=x, out=out, want_arg_other=True)
+        eb = 0
+    elif op in ("dot", "dotheads"):
+        # edge grads: grad_e[e, h] = dot(x[u_e, h], y[v_e, h]) (u_dot_v_copy_e)
+        y = torch.randn(n, F, device="cuda")
+        heads = 8 if op == "dotheads" else 1
+        oe = torch.empty(E, heads, device="cuda")
+        fn = lambda: P.binary_reduce(g, (P.U, P.V, P.DOT, P.COPY_LAST, P.E), u=x, v=y, out=oe,
+                                     heads=heads)
+        eb = E * heads * 4 - n * F * 4  # writes E x heads, reads y rows per edge (cached)
     else:
         fn = lambda: P.binary_reduce(g, "u_copy_add_v", u=x, out=out)
         eb = 0

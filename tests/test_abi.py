@@ -106,6 +106,15 @@ def test_synth_matches_oracle(seed):
     assert (P.synth_gcn_weights(2000, s, t) == O.gcn_weights(2000, s, t)).all()
 
 
+def test_powerlaw_generator_matches_oracle():
+    for seed in range(3):
+        s, d = P.synth_powerlaw(2000, 5, 400, seed, threads=3)
+        s2, d2 = O.gen_powerlaw(2000, 5, 400, seed)
+        assert (s == s2).all() and (d == d2).all()
+        deg = np.bincount(d, minlength=2000)
+        assert deg.min() >= 5 and deg.max() <= 400
+
+
 def test_synth_empty_and_errors():
     s, t = P.synth_rmat(10, 0)
     assert len(s) == 0
