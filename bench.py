@@ -77,6 +77,7 @@ class ClockSampler:
         self.device = device
         self.proc = None
         self.lines = []
+        self.start = 0
 
     def __enter__(self):
         try:
@@ -86,6 +87,12 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
+            # nvidia-smi needs a moment to start: wait for its first sample so
+            # the (tens of ms) timed region is covered, then count from here
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.005)
+            self.start = len(self.lines)
         except Exception:
             self.proc = None
         return self
@@ -105,7 +112,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
+        for line in self.lines[self.start:]:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 9:
                 continue
@@ -393,7 +400,7 @@ def run_ours(args, rank, world, dist):
                    "edge_operand": "weights permuted once to CSR order (device plan, untimed)"},
         "roofline": {"bound": "hbm",
                      "kernel": f"{dominant[0]} pass: k_gather<VPL2,MUL,SUM> (row segments) "
-                               "concurrent with k_long<VPL2,MUL,SUM> (long rows)",
+                               "concurrent with k_long_ws<MUL,SUM> (long rows)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": dominant[2],

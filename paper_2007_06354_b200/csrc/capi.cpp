@@ -56,7 +56,7 @@ const char* operand_name(int o) {
 // GSPMM_SEG_EDGES / GSPMM_LONG_EDGES (the latter forces a single level).
 constexpr uint32_t kSegEdges = 1024;
 constexpr uint32_t kLongEdges = 4096;
-// rows above this many edges are cut into 32-column slices so several CTAs
+// rows above this many edges are cut into 64-column slices so several CTAs
 // stream one row (the 66k-329k-edge hubs of the power-law configs)
 constexpr uint32_t kXlEdges = 16384;
 
@@ -88,7 +88,7 @@ struct gspmm_graph_s {
     uint2* d_segs = nullptr;     // segments of consecutive non-long rows
     uint32_t num_segs = 0;
   };
-  Level level[3];
+  Level level[5];
   int n_levels = 0;
   uint32_t* d_counter = nullptr;  // [0] segment units, [1] long-row units
   uint32_t* d_rowof = nullptr;     // owner row of each CSR position (edge dots), lazy
@@ -243,7 +243,7 @@ int bind(const gspmm_graph_s* g, const gspmm_config* cfg, const gspmm_mat* u,
   L.arg_edge = opt->arg_edge;
   L.arg_ld = opt->arg_ld ? opt->arg_ld : w;
   {
-    const auto& lv = g->level[g->n_levels - 1];  // rows.cu: coarsest level
+    const auto& lv = g->level[g->n_levels > 2 ? 2 : g->n_levels - 1];  // rows.cu: 16384
     L.long_rows = lv.d_long;
     L.num_long = lv.num_long;
     L.long_threshold = lv.num_long ? lv.threshold : 0xffffffffu;
@@ -290,6 +290,7 @@ int plan_kernel(const RowLaunch& L, int* rhs_width) {
   if (forced == 0 || std::getenv("GSPMM_DISABLE_STREAM") != nullptr) return 0;
   if (L.binop == GSPMM_DOT || L.out_edge || !L.out) return 0;
   if (L.reduce == R_PROD || L.reduce == R_LAST) return 0;  // rare: rows.cu
+  if (L.other_scale && L.rhs.base) return 0;                // scale on top of an rhs: rows.cu
   if (L.lhs.mode != MODE_FULL || L.lhs.role == ROLE_ROW) return 0;
   if (L.lhs.ld % 4 || !aligned(L.lhs.base, 16)) return 0;
   if (L.out_ld % 4 || !aligned(L.out, 16)) return 0;
@@ -334,7 +335,16 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
     // plan level: rows gathering more than ~8 MB go to the long-row CTAs
     // (measured: 4096 edges of 1 KB, 16384 of 400 B; heaviest segments run first)
     const int slice_bytes = 4 * std::min(b.L.width, 256);
-    const uint32_t target = std::max<uint32_t>(1024, (8u << 20) / static_cast<uint32_t>(slice_bytes));
+    uint32_t target = std::max<uint32_t>(1024, (8u << 20) / static_cast<uint32_t>(slice_bytes));
+    {
+      // a row no heavier than half the average per-warp share of the
+      // segment work finishes inside the segment kernel's span: keep it there
+      // (measured: long-row CTAs stream a row slower per SM than warps do)
+      const uint32_t slices = static_cast<uint32_t>((b.L.width + 255) / 256);
+      const double warps = static_cast<double>(g->num_sms) * (b.L.width > 128 ? 32 : 24);
+      const double half_share = 0.5 * static_cast<double>(g->m) * slices / warps;
+      if (half_share > target) target = static_cast<uint32_t>(std::min(half_share, 4.0e9));
+    }
     int li = 0;
     for (int k = 0; k < g->n_levels; ++k)
       if (g->level[k].threshold <= target) li = k;
@@ -387,23 +397,36 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
       // events so the call stays ordered on the caller's stream.
       StreamLaunch pl = p;
       pl.mode = 1;
-      pl.long_sw = W <= 256 ? W : 256;
-      pl.long_slices = static_cast<uint32_t>((W + pl.long_sw - 1) / pl.long_sw);
+      // long-row kernel: k_long_ws (default), k_long (GSPMM_LONG_KERNEL=ldg),
+      // k_long_tma (GSPMM_LONG_TMA=1)
+      static const char* lk = std::getenv("GSPMM_LONG_KERNEL");
       static const bool long_tma = env_u32("GSPMM_LONG_TMA", 0) != 0;
+      static const bool long_ws = !long_tma && !(lk && std::strcmp(lk, "ldg") == 0);
+      pl.long_ws = long_ws;
+      if (long_ws) {
+        // <= 512-column slices of balanced width (16-byte multiples)
+        const int ns = (W + 511) / 512;
+        pl.long_sw = ((W + ns - 1) / ns + 3) & ~3;
+      } else {
+        pl.long_sw = W <= 256 ? W : 256;
+      }
+      pl.long_slices = static_cast<uint32_t>((W + pl.long_sw - 1) / pl.long_sw);
       pl.long_tma = long_tma;
       pl.n_xl = long_tma || W <= 32 ? 0 : lv.num_xl;
-      pl.xl_sw = 32;
-      pl.xl_slices = static_cast<uint32_t>((W + 31) / 32);
+      static const int xl_sw = static_cast<int>(env_u32("GSPMM_XL_SW", 64));
+      pl.xl_sw = xl_sw;
+      pl.xl_slices = static_cast<uint32_t>((W + xl_sw - 1) / xl_sw);
       pl.n_xl_units = pl.n_xl * pl.xl_slices;
       pl.n_long_units = pl.n_xl_units + (pl.n_long - pl.n_xl) * pl.long_slices;
       pl.n_units = pl.n_long_units;
       pl.counter = g->d_counter + 1;
       {
         // long-row CTAs ~2x the long rows' share of the edges (measured on the
-        // cfg2-4 shapes: a long CTA streams ~24 GB/s and holds a whole SM)
+        // cfg2-4 shapes: a long-row CTA streams ~30 GB/s and holds a whole SM)
         static const uint32_t forced = env_u32("GSPMM_LONG_CTAS", 0);
         const double share = g->m ? static_cast<double>(lv.long_edges) / g->m : 0.0;
-        uint32_t c = forced ? forced : static_cast<uint32_t>(share * g->num_sms * 2.0 + 1.0);
+        static const double factor = env_u32("GSPMM_LONG_FACTOR10", 20) / 10.0;
+        uint32_t c = forced ? forced : static_cast<uint32_t>(share * g->num_sms * factor + 1.0);
         // the narrow slices of the heaviest rows must run side by side
         c = std::max<uint32_t>(c, std::min<uint32_t>(pl.n_xl_units, g->num_sms / 2));
         pl.long_ctas = std::min<uint32_t>(std::max<uint32_t>(c, 1), g->num_sms);
@@ -570,10 +593,10 @@ int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
   // segments of consecutive non-long rows, for each long-row threshold.
   const uint32_t seg_edges = env_u32("GSPMM_SEG_EDGES", kSegEdges);
   const uint32_t forced_long = env_u32("GSPMM_LONG_EDGES", 0);
-  const uint32_t thresholds[3] = {1024, kLongEdges, 16384};
-  g->n_levels = forced_long ? 1 : 3;
-  std::vector<uint32_t> long_rows[3];
-  std::vector<uint2> segs[3];
+  const uint32_t thresholds[5] = {1024, kLongEdges, 16384, 32768, 65536};
+  g->n_levels = forced_long ? 1 : 5;
+  std::vector<uint32_t> long_rows[5];
+  std::vector<uint2> segs[5];
   for (int k = 0; k < g->n_levels; ++k) {
     auto& lv = g->level[k];
     lv.threshold = forced_long ? forced_long : thresholds[k];

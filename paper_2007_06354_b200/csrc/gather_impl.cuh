@@ -159,17 +159,32 @@ __device__ __forceinline__ float small_value(const RowLaunch& L, int rw, uint32_
 // ------------------------------------------------------------------ WIDE
 // One edge per warp load instruction; lanes own columns lane*4 + v*128.
 // Batches of U edges: all U rows' loads are issued, then folded in edge
-// order as runs of the current row (the finalize code exists once).
-template <int VPL, int U, int BOP, int ROP, bool ARG, bool SMALL>
-__device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, int rw,
-                                          bool scale_on, bool need_eid, int lane) {
+// order -- straight through when the batch lies inside the current row (the
+// common case), edge by edge with row flushes otherwise.
+// The small per-edge operand is resolved at compile time (SK): none; a
+// scalar per edge gathered once per 32-edge id window by the lane owning the
+// edge and broadcast by shuffle (by CSR position, edge id or neighbour; also
+// the per-neighbour scale of the mean backward); or per-head values.
+// Measured: the previous, runtime-dispatched form executed ~125 warp
+// instructions per 1 KB edge (branches, constant-bank reloads, spills) and
+// kept the SMs ~70% issue-busy at 2.5 TB/s of DRAM traffic.
+enum SmallKind : int { SK_NONE = 0, SK_WIN = 1, SK_SCALE = 2, SK_HEAD = 3 };
+
+template <int VPL, int U, int BOP, int ROP, bool ARG, int SK, bool LO>
+__device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, bool need_eid,
+                                          const float* sbase, int64_t sld, int32_t srole,
+                                          int lane) {
   const float* lbase = L.lhs.base + u.c0 + lane * 4;
   const int64_t lld = L.lhs.ld;
   const int32_t lrole = L.lhs.role;
+  const uint32_t* __restrict__ indices = L.indices;
+  const uint32_t* __restrict__ eids = L.eids;
   bool col_ok[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) col_ok[v] = lane * 4 + v * 128 < u.cw;
-  const bool rs_pos = SMALL && rw == 1 && L.rhs.role == ROLE_POS;
+  int hv[VPL];  // SK_HEAD: head of each of this lane's column quads
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) hv[v] = SK == SK_HEAD ? (u.c0 + lane * 4 + v * 128) / L.rhs.group : 0;
 
   RowCursor rc;
   rc.init(L.indptr, u.r0, u.r1, u.e0, lane);
@@ -178,22 +193,31 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
 
   // id windows: lane k <-> edge e0 + 32w + k; the next window is in flight
   uint32_t win_o = 0, win_e = 0, nxt_o = 0, nxt_e = 0;
-  float win_r = 0.0f, nxt_r = 0.0f;  // scalar rhs in CSR order rides along
-  auto load_win = [&](uint32_t w, uint32_t& o, uint32_t& e, float& rs) {
+  float win_r = 0.0f, nxt_r = 0.0f;
+  auto load_win = [&](uint32_t w, uint32_t& o, uint32_t& e, float& rv) {
     const uint32_t j = u.e0 + 32u * w + lane;
     if (j < u.e1) {
-      o = __ldg(L.indices + j);
-      if (need_eid) e = __ldg(L.eids + j);
-      if (rs_pos) rs = __ldg(L.rhs.base + static_cast<int64_t>(j) * L.rhs.ld);
+      o = __ldg(indices + j);
+      if (need_eid) e = __ldg(eids + j);
+      if constexpr (SK == SK_WIN || SK == SK_SCALE) {
+        const uint32_t row = srole == ROLE_POS ? j : srole == ROLE_EID ? e : o;
+        rv = __ldg(sbase + static_cast<int64_t>(row) * sld);
+      }
     }
   };
-  const uint32_t n_edges = u.e1 - u.e0;
   load_win(0, win_o, win_e, win_r);
   load_win(1, nxt_o, nxt_e, nxt_r);
   constexpr int kPerWin = 32 / U;
-  const uint32_t n_batches = (n_edges + U - 1) / U;
+  const uint32_t n_batches = (u.e1 - u.e0 + U - 1) / U;
 
-  uint32_t j = u.e0;
+  auto flush = [&]() {
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+      acc.store(L, rc.r, rc.row_end - rc.row_start, u.c0, u.cw, v, lane * 4 + v * 128);
+    acc.reset();
+  };
+
+  uint32_t j = u.e0;  // next edge to fold
   for (uint32_t b = 0; b < n_batches; ++b) {
     if (b != 0 && (b % kPerWin) == 0) {  // entering the next id window
       win_o = nxt_o;
@@ -204,72 +228,67 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
     const uint32_t jb = u.e0 + b * U;
     const uint32_t n = min(static_cast<uint32_t>(U), u.e1 - jb);
     float4 x[U][VPL];
-    float r[U][VPL];  // small operand per edge and vector (or the scale)
+    float r[U][SK == SK_HEAD ? VPL : 1];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const int sl = static_cast<int>((b % kPerWin) * U) + k;
       const uint32_t o = __shfl_sync(kFull, win_o, sl);
-      const uint32_t e = need_eid ? __shfl_sync(kFull, win_e, sl) : 0u;
-      float rs = 0.0f;
-      if (rs_pos) rs = __shfl_sync(kFull, win_r, sl);
+      uint32_t e = 0;
+      if (!LO || SK == SK_HEAD) {
+        if (need_eid) e = __shfl_sync(kFull, win_e, sl);
+      }
+      if constexpr (SK == SK_WIN || SK == SK_SCALE) r[k][0] = __shfl_sync(kFull, win_r, sl);
       if (static_cast<uint32_t>(k) < n) {
-        const int64_t lr = operand_row(lrole, 0, o, e, jb + k);
-        const float* src = lbase + lr * lld;
+        const uint32_t lr = LO ? o : static_cast<uint32_t>(operand_row(lrole, 0, o, e, jb + k));
+        const float* src = lbase + static_cast<int64_t>(lr) * lld;
 #pragma unroll
         for (int v = 0; v < VPL; ++v)
           if (col_ok[v]) x[k][v] = __ldg(reinterpret_cast<const float4*>(src + v * 128));
-        if constexpr (SMALL) {
+        if constexpr (SK == SK_HEAD) {
+          const float* sp = L.rhs.base + operand_row(L.rhs.role, 0, o, e, jb + k) * L.rhs.ld;
 #pragma unroll
-          for (int v = 0; v < VPL; ++v) {
-            if (rs_pos) r[k][v] = rs;
-            else if (rw > 0)
-              r[k][v] = col_ok[v] ? small_value(L, rw, o, e, jb + k, u.c0 + lane * 4 + v * 128)
-                                  : 0.0f;
-            else if (scale_on) r[k][v] = __ldg(L.other_scale + o);
-          }
+          for (int v = 0; v < VPL; ++v) r[k][v] = col_ok[v] ? __ldg(sp + hv[v]) : 0.0f;
         }
       }
     }
-    uint32_t k0 = 0;
-    while (k0 < n) {
-      while (j == rc.row_end) {
+    auto fold_edge = [&](int k, uint32_t jpos) {
 #pragma unroll
-        for (int v = 0; v < VPL; ++v)
-          acc.store(L, rc.r, rc.row_end - rc.row_start, u.c0, u.cw, v, lane * 4 + v * 128);
-        acc.reset();
-        rc.advance(L.indptr, lane);
+      for (int v = 0; v < VPL; ++v) {
+        if (!col_ok[v]) continue;
+        const float xs[4] = {x[k][v].x, x[k][v].y, x[k][v].z, x[k][v].w};
+        float m[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if constexpr (SK == SK_NONE) m[t] = bin_apply<BOP>(xs[t], 0.0f);
+          else if constexpr (SK == SK_SCALE) m[t] = __fmul_rn(bin_apply<BOP>(xs[t], 0.0f), r[k][0]);
+          else if constexpr (SK == SK_WIN) m[t] = bin_apply<BOP>(xs[t], r[k][0]);
+          else m[t] = bin_apply<BOP>(xs[t], r[k][v]);
+        }
+        acc.fold(v, m, jpos);
       }
-      const uint32_t k1 = k0 + min(n - k0, rc.row_end - j);
+    };
+    if (rc.row_end - j >= n) {  // the whole batch folds into the current row
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (static_cast<uint32_t>(k) < n) fold_edge(k, j + k);
+      j += n;
+    } else {
 #pragma unroll
       for (int k = 0; k < U; ++k) {
-        if (static_cast<uint32_t>(k) < k0 || static_cast<uint32_t>(k) >= k1) continue;
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-          if (!col_ok[v]) continue;
-          const float xs[4] = {x[k][v].x, x[k][v].y, x[k][v].z, x[k][v].w};
-          float m[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            if constexpr (SMALL) {
-              if (rw > 0) m[t] = bin_apply<BOP>(xs[t], r[k][v]);
-              else m[t] = __fmul_rn(bin_apply<BOP>(xs[t], 0.0f), r[k][v]);  // copy * scale
-            } else {
-              m[t] = bin_apply<BOP>(xs[t], 0.0f);
-            }
+        if (static_cast<uint32_t>(k) < n) {
+          while (j == rc.row_end) {
+            flush();
+            rc.advance(L.indptr, lane);
           }
-          acc.fold(v, m, u.e0 + b * U + k);
+          fold_edge(k, j);
+          ++j;
         }
       }
-      j += k1 - k0;
-      k0 = k1;
     }
   }
   // the current row and trailing empty rows
   while (rc.r < u.r1) {
-#pragma unroll
-    for (int v = 0; v < VPL; ++v)
-      acc.store(L, rc.r, rc.row_end - rc.row_start, u.c0, u.cw, v, lane * 4 + v * 128);
-    acc.reset();
+    flush();
     if (rc.r + 1 < u.r1) {
       rc.advance(L.indptr, lane);
     } else {
@@ -499,6 +518,261 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long(const StreamLaunch p) 
   }
 }
 
+// ------------------------------------- LONG ROWS, warp-specialised LDGSTS
+// The production long-row CTA.  One column slice (<= 512 floats) of one long
+// row per unit, streamed through a shared-memory ring of NB stages of R edges
+// by cp.async (LDGSTS: global -> shared, no registers hold data in flight).
+// Producers and consumers are decoupled by per-stage mbarriers: 12 producer
+// warps issue the copies of stage s as soon as the consumers released its
+// slot (empty[s % NB]); 4 consumer warps -- the column owners, one column
+// (narrow slices) or four (wide) per thread -- fold stage s in canonical edge
+// order as soon as its copies landed (full[s % NB]).  A copy costs one id
+// (shared-memory broadcast) and one 64-bit address per lane per edge.  The
+// ids of stage s + NB ride in stage s's copy group into a 2*NB id ring, so
+// issuing never waits on a global load.
+// Measured on B200 (scripts/mb_long.cu, scripts/var_long.sh): per-SM stream
+// rate grows with producer warps up to ~12 and with 48 KB stages; a CTA
+// barrier per stage (fold delaying the next issue) cost ~25%, and feeding
+// addresses from ids loaded into registers one stage earlier capped a CTA at
+// one id-load latency per stage (~20 GB/s).
+#ifndef WS_NB
+#define WS_NB 3
+#endif
+#ifndef WS_DF
+#define WS_DF 12288
+#endif
+#ifndef WS_P
+#define WS_P 12
+#endif
+constexpr int kWsProducers = WS_P, kWsConsumers = 4;
+constexpr int kWsThreads = 32 * (kWsProducers + kWsConsumers);
+struct WsGeom {
+  static constexpr int NB = WS_NB;
+  static constexpr int DF = WS_DF;          // data floats per stage
+  static constexpr int SF = DF / 6;         // small-operand floats per stage
+  static constexpr int MR = 256;            // max edges per stage
+  static constexpr size_t smem_bytes(bool small) {
+    return sizeof(float) * (static_cast<size_t>(NB) * (DF + (small ? SF : 0)) + 4ull * NB * MR) +
+           2ull * NB * sizeof(uint64_t);
+  }
+};
+
+template <int BOP, int ROP, bool ARG, bool SMALL>
+__global__ void __launch_bounds__(kWsThreads, 1) k_long_ws(const StreamLaunch p) {
+  using G = WsGeom;
+  constexpr int NB = G::NB;
+  extern __shared__ __align__(16) float sm[];
+  __shared__ uint32_t s_unit;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool producer = warp < kWsProducers;
+  const RowLaunch& L = p.row;
+  const int rw = SMALL ? p.rhs_width : 0;
+  const bool scale_on = SMALL && L.other_scale != nullptr;
+  const bool need_eid = L.lhs.role == ROLE_EID || (rw && L.rhs.role == ROLE_EID);
+  float* sdata = sm;                                                    // NB x DF
+  uint32_t* sid = reinterpret_cast<uint32_t*>(sm + static_cast<size_t>(NB) * G::DF);  // 2NB x MR
+  uint32_t* seid = sid + 2 * NB * G::MR;                                // 2NB x MR
+  float* ssmall = reinterpret_cast<float*>(seid + 2 * NB * G::MR);      // NB x SF
+  uint64_t* full = reinterpret_cast<uint64_t*>(ssmall + (SMALL ? NB * G::SF : 0));
+  uint64_t* empty = full + NB;
+  if (tid == 0) {
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full[b], kWsProducers);
+      mbar_init(&empty[b], kWsConsumers);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t gs0 = 0;  // stages this CTA ran before the current unit (ring position)
+
+  for (;;) {
+    if (tid == 0) s_unit = atomicAdd(p.counter, 1u);
+    __syncthreads();
+    const uint32_t unit = s_unit;
+    __syncthreads();
+    if (unit >= p.n_units) break;
+    const unsigned long long t0 = p.trace ? globaltimer_ns() : 0ull;
+    uint32_t li, slc;
+    int sw;
+    if (unit < p.n_xl_units) {
+      li = unit / p.xl_slices;
+      slc = unit - li * p.xl_slices;
+      sw = p.xl_sw;
+    } else {
+      const uint32_t v = unit - p.n_xl_units;
+      li = p.n_xl + v / p.long_slices;
+      slc = v - (li - p.n_xl) * p.long_slices;
+      sw = p.long_sw;
+    }
+    const uint32_t r = __ldg(p.long_rows + li);
+    const int c0 = static_cast<int>(slc) * sw;
+    const int cw = min(sw, L.width - c0);
+    const int slot_f = (cw + 3) & ~3;
+    const int qpe = slot_f >> 2;
+    const int cq = (cw + 3) >> 2;
+    const int h0 = (SMALL && rw > 1) ? c0 / L.rhs.group : 0;
+    const int nh = SMALL ? ((rw > 1) ? (c0 + cw - 1) / L.rhs.group - h0 + 1 : 1) : 1;
+    uint32_t R = static_cast<uint32_t>(G::DF / slot_f);
+    if (R > static_cast<uint32_t>(G::MR)) R = G::MR;
+    if (SMALL && R * nh > static_cast<uint32_t>(G::SF)) R = G::SF / nh;
+    const uint32_t e0 = __ldg(L.indptr + r), e1 = __ldg(L.indptr + r + 1);
+    const uint32_t n = e1 - e0;
+    const uint32_t rounds = (n + R - 1) / R;
+
+    if (producer) {
+      const int ptid = tid;  // 0 .. 32 * kWsProducers - 1
+      const int lpe = qpe >= 32 ? 32 : qpe > 8 ? (qpe > 16 ? 32 : 16) : qpe > 4 ? 8 : qpe > 2 ? 4 : qpe;
+      const int epi = 32 / lpe;
+      const int sub = lane / lpe, il = lane - sub * lpe;
+      const int tpe = (qpe + lpe - 1) / lpe;
+      const uint32_t ngroups = (R + epi - 1) / epi;
+      const float* lbase = L.lhs.base + c0 + il * 4;
+      const int64_t lld = L.lhs.ld;
+      const int32_t lrole = L.lhs.role;
+      auto fetch_ids = [&](uint32_t m) {  // ids of unit stage m -> id slot (gs0 + m) % 2NB
+        if (m >= rounds) return;
+        const uint32_t slot = (gs0 + m) % (2 * NB);
+        for (uint32_t t = static_cast<uint32_t>(ptid); t < R; t += 32 * kWsProducers) {
+          const uint32_t j = e0 + m * R + t;
+          if (j < e1) {
+            cp_async_4(sid + slot * G::MR + t, L.indices + j);
+            if (need_eid) cp_async_4(seid + slot * G::MR + t, L.eids + j);
+          }
+        }
+      };
+      // prologue: ids of the first NB stages, visible to every producer
+      for (uint32_t m = 0; m < static_cast<uint32_t>(NB); ++m) fetch_ids(m);
+      cp_async_commit();
+      cp_async_wait_group<0>();
+      named_barrier_sync(1, 32 * kWsProducers);
+      for (uint32_t s = 0; s < rounds; ++s) {
+        const uint32_t gsi = gs0 + s;
+        const int b = static_cast<int>(gsi % NB);
+        if (gsi >= static_cast<uint32_t>(NB)) mbar_wait(&empty[b], ((gsi / NB) - 1) & 1u);
+        const uint32_t islot = gsi % (2 * NB);
+        const uint32_t* io = sid + islot * G::MR;
+        const uint32_t* ie = seid + islot * G::MR;
+        float* bd = sdata + static_cast<size_t>(b) * G::DF + il * 4;
+        float* bs = ssmall + static_cast<size_t>(b) * G::SF;
+        const uint32_t jr0 = s * R;
+        for (uint32_t g = static_cast<uint32_t>(warp); g < ngroups; g += kWsProducers) {
+          const uint32_t q = g * epi + sub;
+          if (q >= R || jr0 + q >= n) continue;
+          const uint32_t j = e0 + jr0 + q;
+          const uint32_t o = io[q];
+          const uint32_t e = need_eid ? ie[q] : 0u;
+          const float* src = lbase + operand_row(lrole, 0, o, e, j) * lld;
+          float* dst = bd + q * slot_f;
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (t < tpe && il + t * lpe < cq) cp_async_16(dst + t * lpe * 4, src + t * lpe * 4);
+          if constexpr (SMALL) {
+            if (rw > 0) {
+              const float* sp = L.rhs.base + operand_row(L.rhs.role, 0, o, e, j) * L.rhs.ld + h0;
+              for (int h = il; h < nh; h += lpe) cp_async_4(bs + q * nh + h, sp + h);
+            } else if (il == 0 && scale_on) {
+              cp_async_4(bs + q, L.other_scale + o);
+            }
+          }
+        }
+        fetch_ids(s + NB);
+        cp_async_arrive(&full[b]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[b]);
+      }
+      cp_async_wait_group<0>();
+    } else {
+      const int ctid = tid - 32 * kWsProducers;  // 0 .. 127
+      auto run = [&](auto fw_tag) {
+        constexpr int FW = decltype(fw_tag)::value;
+        const int cc = ctid * FW;
+        const bool own = cc < cw;
+        const int hrel = (SMALL && rw > 1) ? (c0 + cc) / L.rhs.group - h0 : 0;
+        float acc[FW];
+        uint32_t arg[FW];
+#pragma unroll
+        for (int t = 0; t < FW; ++t) {
+          acc[t] = red_identity<ROP>();
+          arg[t] = 0xffffffffu;
+        }
+        for (uint32_t s = 0; s < rounds; ++s) {
+          const uint32_t gsi = gs0 + s;
+          const int b = static_cast<int>(gsi % NB);
+          mbar_wait(&full[b], (gsi / NB) & 1u);
+          if (own) {
+            const uint32_t cnt = min(R, n - s * R);
+            const float* col = sdata + static_cast<size_t>(b) * G::DF + cc;
+            const float* sv = ssmall + static_cast<size_t>(b) * G::SF + hrel;
+#pragma unroll 8
+            for (uint32_t e = 0; e < cnt; ++e) {
+              float x[FW];
+              if constexpr (FW == 4) {
+                const float4 v = *reinterpret_cast<const float4*>(col + static_cast<size_t>(e) * slot_f);
+                x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+              } else {
+                x[0] = col[static_cast<size_t>(e) * slot_f];
+              }
+              float sval = 0.0f;
+              if constexpr (SMALL) sval = sv[e * nh];
+#pragma unroll
+              for (int t = 0; t < FW; ++t) {
+                float m;
+                if constexpr (SMALL) {
+                  if (rw > 0) m = bin_apply<BOP>(x[t], sval);
+                  else m = __fmul_rn(bin_apply<BOP>(x[t], 0.0f), sval);
+                } else {
+                  m = bin_apply<BOP>(x[t], 0.0f);
+                }
+                if constexpr (ARG) {
+                  if (red_wins<ROP>(acc[t], m)) {
+                    acc[t] = m;
+                    arg[t] = e0 + s * R + e;
+                  }
+                } else {
+                  acc[t] = red_combine<ROP>(acc[t], m);
+                }
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[b]);
+        }
+        if (own) {
+#pragma unroll
+          for (int t = 0; t < FW; ++t) {
+            if (cc + t >= cw) break;
+            float a = acc[t];
+            if constexpr (ROP == R_MAX || ROP == R_MIN) {
+              if (n == 0) a = 0.0f;
+            }
+            if (L.mean) a = n ? __fdiv_rn(a, __uint2float_rn(n)) : 0.0f;
+            L.out[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t] = a;
+            if constexpr (ARG) {
+              const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + cc + t;
+              const bool none = arg[t] == 0xffffffffu;
+              if (L.arg_other)
+                L.arg_other[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.indices + arg[t]));
+              if (L.arg_edge)
+                L.arg_edge[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.eids + arg[t]));
+            }
+          }
+        }
+      };
+      if (cw > 128) run(std::integral_constant<int, 4>{});
+      else run(std::integral_constant<int, 1>{});
+      if (p.trace && ctid == 0) {
+        unsigned long long* t = p.trace + 4ull * unit;
+        t[0] = t0;
+        t[1] = globaltimer_ns();
+        t[2] = (static_cast<unsigned long long>(smid()) << 32) | 0xfffcu;
+        t[3] = n;
+      }
+    }
+    gs0 += rounds;
+    __syncthreads();  // next unit: the id ring's first slots are rewritten
+  }
+}
+
 // ------------------------------------------------------ LONG ROWS via TMA
 // Warp-specialised variant for slices of >= 512 B: warp 8 is the producer
 // (lane 0 issues one cp.async.bulk per edge into a shared-memory ring of
@@ -699,15 +973,18 @@ __global__ void __launch_bounds__(kLtThreads, 1) k_long_tma(const StreamLaunch p
 }
 
 // -------------------------------------------------------------- segments
-template <int VPL, int U, int BOP, int ROP, bool ARG, bool SMALL>
+template <int VPL, int U, int BOP, int ROP, bool ARG, int SK, bool LO>
 __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : GATHER_MINB2) k_gather(const StreamLaunch p) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int warps = kThreads / 32;
   const RowLaunch& L = p.row;
-  const int rw = SMALL ? p.rhs_width : 0;
-  const bool scale_on = SMALL && L.other_scale != nullptr;
-  const bool need_eid = L.lhs.role == ROLE_EID || (rw && L.rhs.role == ROLE_EID);
+  const bool need_eid = L.lhs.role == ROLE_EID ||
+                        ((SK == SK_WIN || SK == SK_HEAD) && L.rhs.role == ROLE_EID);
+  // small scalar operand gathered in the id windows: value = sbase[row * sld]
+  const float* sbase = SK == SK_SCALE ? L.other_scale : L.rhs.base;
+  const int64_t sld = SK == SK_SCALE ? 1 : L.rhs.ld;
+  const int32_t srole = SK == SK_SCALE ? static_cast<int32_t>(ROLE_OTHER) : L.rhs.role;
 
   const uint32_t n_static = gridDim.x * warps;
   uint32_t next_unit = blockIdx.x + gridDim.x * static_cast<uint32_t>(warp);
@@ -728,7 +1005,7 @@ __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : GATHER_MIN
     u.cw = min(p.seg_sw, L.width - u.c0);
     u.e0 = __ldg(L.indptr + u.r0);
     u.e1 = __ldg(L.indptr + u.r1);
-    wide_unit<VPL, U, BOP, ROP, ARG, SMALL>(L, u, rw, scale_on, need_eid, lane);
+    wide_unit<VPL, U, BOP, ROP, ARG, SK, LO>(L, u, need_eid, sbase, sld, srole, lane);
     if (p.trace && lane == 0) {
       unsigned long long* t = p.trace + 4ull * unit;
       t[0] = t0;
@@ -740,8 +1017,9 @@ __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : GATHER_MIN
 }
 
 // p.mode: 0 = row segments (k_gather), 1 = long rows (k_long)
-template <int VPL, int BOP, int ROP, bool ARG, bool SMALL>
+template <int VPL, int BOP, int ROP, bool ARG, int SK, bool LO>
 cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
+  constexpr bool SMALL = SK != SK_NONE;
   cudaError_t e = cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const int sms = p.row.num_sms > 0 ? p.row.num_sms : 148;
@@ -760,6 +1038,21 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
     if (grid > p.n_units) grid = p.n_units;
     k_long_tma<BOP, ROP, ARG, SMALL><<<grid, kLtThreads, lt_smem_bytes(), s>>>(p);
+  } else if (p.mode == 1 && p.long_ws) {
+    const bool small = SMALL;
+    static int configured_w = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_w != dev) {
+      e = cudaFuncSetAttribute(k_long_ws<BOP, ROP, ARG, SMALL>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(WsGeom::smem_bytes(small)));
+      if (e != cudaSuccess) return e;
+      configured_w = dev;
+    }
+    unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
+    if (grid > p.n_units) grid = p.n_units;
+    k_long_ws<BOP, ROP, ARG, SMALL><<<grid, kWsThreads, WsGeom::smem_bytes(small), s>>>(p);
   } else if (p.mode == 1) {
     const int rws = SMALL ? (p.rhs_width > 0 ? p.rhs_width : 1) : 0;
     const size_t smem = LongGeom<VPL>::smem_bytes(rws);
@@ -784,11 +1077,11 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
-                                                    k_gather<VPL, U, BOP, ROP, ARG, SMALL>,
+                                                    k_gather<VPL, U, BOP, ROP, ARG, SK, LO>,
                                                     kThreads, 0);
       if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
-    k_gather<VPL, U, BOP, ROP, ARG, SMALL><<<sms * blocks_per_sm, kThreads, 0, s>>>(p);
+    k_gather<VPL, U, BOP, ROP, ARG, SK, LO><<<sms * blocks_per_sm, kThreads, 0, s>>>(p);
   }
   note_launch();
   return cudaGetLastError();
@@ -796,25 +1089,40 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
 
 template <int VPL, int BOP>
 cudaError_t launch_red(const StreamLaunch& p, cudaStream_t s) {
-  const bool arg = p.row.arg_other || p.row.arg_edge;
-  auto small = [&](auto rop, auto argt) {
+  const RowLaunch& L = p.row;
+  const bool arg = L.arg_other || L.arg_edge;
+  // small operand kind (the host routes other_scale together with an rhs to
+  // rows.cu)
+  const int sk = L.rhs.base ? (p.rhs_width > 1 ? SK_HEAD : SK_WIN)
+                            : (L.other_scale ? SK_SCALE : SK_NONE);
+  const bool lo = L.lhs.role == ROLE_OTHER;
+  auto go = [&](auto rop, auto argt, auto skt) -> cudaError_t {
     constexpr int R = decltype(rop)::value;
     constexpr bool A = decltype(argt)::value;
+    constexpr int K = decltype(skt)::value;
+    // copy_u / u_op_e with the gathered neighbour rows: the specialised
+    // instances; copy_e and other layouts: the generic-role instance
+    if (lo) return launch_k<VPL, BOP, R, A, K, true>(p, s);
+    return launch_k<VPL, BOP, R, A, K, false>(p, s);
+  };
+  auto by_sk = [&](auto rop, auto argt) -> cudaError_t {
+    using std::integral_constant;
     if constexpr (BOP == B_COPY) {
-      return p.row.other_scale ? launch_k<VPL, BOP, R, A, true>(p, s)
-                               : launch_k<VPL, BOP, R, A, false>(p, s);
+      if (sk == SK_SCALE) return go(rop, argt, integral_constant<int, SK_SCALE>{});
+      return go(rop, argt, integral_constant<int, SK_NONE>{});
     } else {
-      return launch_k<VPL, BOP, R, A, true>(p, s);
+      if (sk == SK_HEAD) return go(rop, argt, integral_constant<int, SK_HEAD>{});
+      return go(rop, argt, integral_constant<int, SK_WIN>{});
     }
   };
   using F = std::false_type;
   using T = std::true_type;
-  switch (p.row.reduce) {
-    case R_SUM: return small(std::integral_constant<int, R_SUM>{}, F{});
-    case R_MAX: return arg ? small(std::integral_constant<int, R_MAX>{}, T{})
-                           : small(std::integral_constant<int, R_MAX>{}, F{});
-    default: return arg ? small(std::integral_constant<int, R_MIN>{}, T{})
-                        : small(std::integral_constant<int, R_MIN>{}, F{});
+  switch (L.reduce) {
+    case R_SUM: return by_sk(std::integral_constant<int, R_SUM>{}, F{});
+    case R_MAX: return arg ? by_sk(std::integral_constant<int, R_MAX>{}, T{})
+                           : by_sk(std::integral_constant<int, R_MAX>{}, F{});
+    default: return arg ? by_sk(std::integral_constant<int, R_MIN>{}, T{})
+                        : by_sk(std::integral_constant<int, R_MIN>{}, F{});
   }
 }
 

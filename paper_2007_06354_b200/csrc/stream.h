@@ -27,6 +27,7 @@ struct StreamLaunch {
   uint32_t n_xl = 0, xl_slices = 1, n_xl_units = 0;
   int xl_sw = 32;
   bool long_tma = false;  // GSPMM_LONG_TMA=1: warp-specialised TMA long rows
+  bool long_ws = true;  // long rows: k_long_ws (default) or k_long (GSPMM_LONG_KERNEL=ldg)
   // Units whose gathered slice is narrower than this many bytes stage rows
   // with per-lane 16-byte cp.async (LSU path) instead of one TMA bulk copy
   // per edge: small bulk copies are bound by the TMA request rate.
