@@ -174,17 +174,24 @@ template <int VPL, int U, int BOP, int ROP, bool ARG, int SK, bool LO>
 __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, bool need_eid,
                                           const float* sbase, int64_t sld, int32_t srole,
                                           int lane) {
-  const float* lbase = L.lhs.base + u.c0 + lane * 4;
-  const int64_t lld = L.lhs.ld;
+  // per-lane row-relative byte offsets of the VPL column quads; quads past
+  // the slice read column 0 (always inside the row) and are never stored
+  const char* lrow[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    const int c = lane * 4 + v * 128;
+    lrow[v] = reinterpret_cast<const char*>(L.lhs.base + u.c0 + (c < u.cw ? c : 0));
+  }
+  const uint32_t ldb = static_cast<uint32_t>(L.lhs.ld) * 4u;  // row stride in bytes
   const int32_t lrole = L.lhs.role;
   const uint32_t* __restrict__ indices = L.indices;
   const uint32_t* __restrict__ eids = L.eids;
-  bool col_ok[VPL];
-#pragma unroll
-  for (int v = 0; v < VPL; ++v) col_ok[v] = lane * 4 + v * 128 < u.cw;
   int hv[VPL];  // SK_HEAD: head of each of this lane's column quads
 #pragma unroll
-  for (int v = 0; v < VPL; ++v) hv[v] = SK == SK_HEAD ? (u.c0 + lane * 4 + v * 128) / L.rhs.group : 0;
+  for (int v = 0; v < VPL; ++v) {
+    const int c = lane * 4 + v * 128;
+    hv[v] = SK == SK_HEAD ? (u.c0 + (c < u.cw ? c : 0)) / L.rhs.group : 0;
+  }
 
   RowCursor rc;
   rc.init(L.indptr, u.r0, u.r1, u.e0, lane);
@@ -229,32 +236,32 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
     const uint32_t n = min(static_cast<uint32_t>(U), u.e1 - jb);
     float4 x[U][VPL];
     float r[U][SK == SK_HEAD ? VPL : 1];
+    // loads: unconditional (a tail batch re-reads its last edge), so the
+    // batch is straight-line code
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      const int sl = static_cast<int>((b % kPerWin) * U) + k;
+      const int kk = static_cast<uint32_t>(k) < n ? k : static_cast<int>(n) - 1;
+      const int sl = static_cast<int>((b % kPerWin) * U) + kk;
       const uint32_t o = __shfl_sync(kFull, win_o, sl);
       uint32_t e = 0;
       if (!LO || SK == SK_HEAD) {
         if (need_eid) e = __shfl_sync(kFull, win_e, sl);
       }
       if constexpr (SK == SK_WIN || SK == SK_SCALE) r[k][0] = __shfl_sync(kFull, win_r, sl);
-      if (static_cast<uint32_t>(k) < n) {
-        const uint32_t lr = LO ? o : static_cast<uint32_t>(operand_row(lrole, 0, o, e, jb + k));
-        const float* src = lbase + static_cast<int64_t>(lr) * lld;
+      const uint32_t lr = LO ? o : static_cast<uint32_t>(operand_row(lrole, 0, o, e, jb + kk));
 #pragma unroll
-        for (int v = 0; v < VPL; ++v)
-          if (col_ok[v]) x[k][v] = __ldg(reinterpret_cast<const float4*>(src + v * 128));
-        if constexpr (SK == SK_HEAD) {
-          const float* sp = L.rhs.base + operand_row(L.rhs.role, 0, o, e, jb + k) * L.rhs.ld;
+      for (int v = 0; v < VPL; ++v)
+        x[k][v] = __ldg(reinterpret_cast<const float4*>(lrow[v] + static_cast<uint64_t>(lr) * ldb));
+      if constexpr (SK == SK_HEAD) {
+        const float* sp = L.rhs.base + operand_row(L.rhs.role, 0, o, e, jb + kk) * L.rhs.ld;
 #pragma unroll
-          for (int v = 0; v < VPL; ++v) r[k][v] = col_ok[v] ? __ldg(sp + hv[v]) : 0.0f;
-        }
+        for (int v = 0; v < VPL; ++v) r[k][v] = __ldg(sp + hv[v]);
       }
     }
+    // quads past the slice fold garbage that is never stored
     auto fold_edge = [&](int k, uint32_t jpos) {
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
-        if (!col_ok[v]) continue;
         const float xs[4] = {x[k][v].x, x[k][v].y, x[k][v].z, x[k][v].w};
         float m[4];
 #pragma unroll
@@ -267,11 +274,11 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
         acc.fold(v, m, jpos);
       }
     };
-    if (rc.row_end - j >= n) {  // the whole batch folds into the current row
+    if (n == static_cast<uint32_t>(U) && rc.row_end - j >= static_cast<uint32_t>(U)) {
+      // the whole batch folds into the current row
 #pragma unroll
-      for (int k = 0; k < U; ++k)
-        if (static_cast<uint32_t>(k) < n) fold_edge(k, j + k);
-      j += n;
+      for (int k = 0; k < U; ++k) fold_edge(k, j + k);
+      j += U;
     } else {
 #pragma unroll
       for (int k = 0; k < U; ++k) {
