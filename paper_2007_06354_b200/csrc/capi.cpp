@@ -421,11 +421,11 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
       pl.n_units = pl.n_long_units;
       pl.counter = g->d_counter + 1;
       {
-        // long-row CTAs ~2x the long rows' share of the edges (measured on the
+        // long-row CTAs ~3x the long rows' share of the edges (measured on the
         // cfg2-4 shapes: a long-row CTA streams ~30 GB/s and holds a whole SM)
         static const uint32_t forced = env_u32("GSPMM_LONG_CTAS", 0);
         const double share = g->m ? static_cast<double>(lv.long_edges) / g->m : 0.0;
-        static const double factor = env_u32("GSPMM_LONG_FACTOR10", 20) / 10.0;
+        static const double factor = env_u32("GSPMM_LONG_FACTOR10", 30) / 10.0;
         uint32_t c = forced ? forced : static_cast<uint32_t>(share * g->num_sms * factor + 1.0);
         // the narrow slices of the heaviest rows must run side by side
         c = std::max<uint32_t>(c, std::min<uint32_t>(pl.n_xl_units, g->num_sms / 2));
