@@ -652,6 +652,20 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_long_ws(const StreamLaunch p)
       cp_async_commit();
       cp_async_wait_group<0>();
       named_barrier_sync(1, 32 * kWsProducers);
+      // per-lane constants of the copy loop: which of the <= 4 quads of an
+      // edge this lane copies, source / shared byte offsets
+      uint32_t tmask = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t < tpe && il + t * lpe < cq) tmask |= 1u << t;
+      const char* lsrc = reinterpret_cast<const char*>(lbase);
+      const uint32_t ldb = static_cast<uint32_t>(lld) * 4u;
+      const uint32_t slot_b = static_cast<uint32_t>(slot_f) * 4u;
+      const uint32_t tstep = static_cast<uint32_t>(lpe) * 16u;
+      const bool small1 = SMALL && (rw == 1 || (rw == 0 && scale_on));
+      const float* s1base = rw == 1 ? L.rhs.base : L.other_scale;
+      const int64_t s1ld = rw == 1 ? L.rhs.ld : 1;
+      const int32_t s1role = rw == 1 ? L.rhs.role : static_cast<int32_t>(ROLE_OTHER);
       for (uint32_t s = 0; s < rounds; ++s) {
         const uint32_t gsi = gs0 + s;
         const int b = static_cast<int>(gsi % NB);
@@ -659,26 +673,32 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_long_ws(const StreamLaunch p)
         const uint32_t islot = gsi % (2 * NB);
         const uint32_t* io = sid + islot * G::MR;
         const uint32_t* ie = seid + islot * G::MR;
-        float* bd = sdata + static_cast<size_t>(b) * G::DF + il * 4;
+        const uint32_t sd = smem_u32(sdata + static_cast<size_t>(b) * G::DF) + static_cast<uint32_t>(il) * 16u;
         float* bs = ssmall + static_cast<size_t>(b) * G::SF;
         const uint32_t jr0 = s * R;
-        for (uint32_t g = static_cast<uint32_t>(warp); g < ngroups; g += kWsProducers) {
+        const uint32_t cnt = min(R, n - jr0);
+        const uint32_t gcount = (cnt + epi - 1) / epi;
+        for (uint32_t g = static_cast<uint32_t>(warp); g < gcount; g += kWsProducers) {
           const uint32_t q = g * epi + sub;
-          if (q >= R || jr0 + q >= n) continue;
+          if (q >= cnt) continue;
           const uint32_t j = e0 + jr0 + q;
           const uint32_t o = io[q];
           const uint32_t e = need_eid ? ie[q] : 0u;
-          const float* src = lbase + operand_row(lrole, 0, o, e, j) * lld;
-          float* dst = bd + q * slot_f;
+          const uint32_t row = lrole == ROLE_OTHER ? o : static_cast<uint32_t>(operand_row(lrole, 0, o, e, j));
+          const char* src = lsrc + static_cast<uint64_t>(row) * ldb;
+          const uint32_t d = sd + q * slot_b;
 #pragma unroll
           for (int t = 0; t < 4; ++t)
-            if (t < tpe && il + t * lpe < cq) cp_async_16(dst + t * lpe * 4, src + t * lpe * 4);
+            if ((tmask >> t) & 1u) cp_async_16_s(d + t * tstep, src + t * tstep);
           if constexpr (SMALL) {
-            if (rw > 0) {
+            if (small1) {
+              if (il == 0) {
+                const uint32_t sr = s1role == ROLE_POS ? j : s1role == ROLE_EID ? e : o;
+                cp_async_4(bs + q, s1base + static_cast<int64_t>(sr) * s1ld);
+              }
+            } else {
               const float* sp = L.rhs.base + operand_row(L.rhs.role, 0, o, e, j) * L.rhs.ld + h0;
               for (int h = il; h < nh; h += lpe) cp_async_4(bs + q * nh + h, sp + h);
-            } else if (il == 0 && scale_on) {
-              cp_async_4(bs + q, L.other_scale + o);
             }
           }
         }
