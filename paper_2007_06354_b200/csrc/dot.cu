@@ -230,6 +230,98 @@ __global__ void __launch_bounds__(kEdWarps * 32) k_dot_edges(const RowLaunch p,
   }
 }
 
+// Vector variant for 16-byte-aligned full-width operands with G % 4 == 0:
+// 128-column chunks, lanes own 4 consecutive columns (LDG.128 of both
+// operand rows, 4 products, one STS.128 into the edge's tile row), then lane k
+// folds edge k's products in column order with LDS.128.  The tile row stride
+// of 132 floats keeps both the row writes and the per-lane column reads free
+// of bank conflicts.  ~3x fewer instructions per byte than k_dot_edges.
+constexpr int kEd4Warps = 4;
+constexpr int kEd4CW = 128;
+constexpr int kEd4Stride = kEd4CW + 4;
+constexpr int kEd4U = 8;
+
+__global__ void __launch_bounds__(kEd4Warps * 32) k_dot_edges4(const RowLaunch p,
+                                                               const uint32_t* __restrict__ rowof,
+                                                               uint64_t m) {
+  extern __shared__ __align__(16) float tiles4[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* tile = tiles4 + warp * 32 * kEd4Stride;
+  const int G = p.gather_dim;
+  const int D = G / p.heads;
+  const uint64_t n_batches = (m + 31) / 32;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kEd4Warps;
+  const int32_t lrole = p.lhs.role, rrole = p.rhs.role;
+  const uint32_t lldb = static_cast<uint32_t>(p.lhs.ld) * 4u, rldb = static_cast<uint32_t>(p.rhs.ld) * 4u;
+  const char* lbase = reinterpret_cast<const char*>(p.lhs.base);
+  const char* rbase = reinterpret_cast<const char*>(p.rhs.base);
+  for (uint64_t bt = static_cast<uint64_t>(blockIdx.x) * kEd4Warps + warp; bt < n_batches;
+       bt += stride) {
+    const uint64_t jb = bt * 32;
+    const int n = static_cast<int>(m - jb < 32 ? m - jb : 32);
+    uint32_t my_o = 0, my_e = 0, my_r = 0;
+    if (lane < n) {
+      my_o = __ldg(p.indices + jb + lane);
+      my_e = __ldg(p.eids + jb + lane);
+      my_r = __ldg(rowof + jb + lane);
+    }
+    float acc = 0.0f;
+    int head = 0, left = D;  // columns left in the current head
+    for (int cb = 0; cb < G; cb += kEd4CW) {
+      const int c0 = cb + lane * 4;
+      const bool cok = c0 < G;
+      const uint32_t coff = static_cast<uint32_t>(cok ? c0 : 0) * 4u;
+      for (int i0 = 0; i0 < n; i0 += kEd4U) {
+        float4 lv[kEd4U], rv[kEd4U];
+#pragma unroll
+        for (int k = 0; k < kEd4U; ++k) {
+          const int i = min(i0 + k, n - 1);  // a tail re-reads the last edge
+          const uint32_t o = __shfl_sync(kFull, my_o, i);
+          const uint32_t e = __shfl_sync(kFull, my_e, i);
+          const uint32_t r = __shfl_sync(kFull, my_r, i);
+          const uint32_t j = static_cast<uint32_t>(jb) + static_cast<uint32_t>(i);
+          const uint32_t lr = static_cast<uint32_t>(operand_row(lrole, r, o, e, j));
+          const uint32_t rr = static_cast<uint32_t>(operand_row(rrole, r, o, e, j));
+          lv[k] = __ldg(reinterpret_cast<const float4*>(lbase + static_cast<uint64_t>(lr) * lldb + coff));
+          rv[k] = __ldg(reinterpret_cast<const float4*>(rbase + static_cast<uint64_t>(rr) * rldb + coff));
+        }
+#pragma unroll
+        for (int k = 0; k < kEd4U; ++k) {
+          const int i = i0 + k;
+          if (i < n) {
+            float4 pr;
+            pr.x = __fmul_rn(lv[k].x, rv[k].x);
+            pr.y = __fmul_rn(lv[k].y, rv[k].y);
+            pr.z = __fmul_rn(lv[k].z, rv[k].z);
+            pr.w = __fmul_rn(lv[k].w, rv[k].w);
+            *reinterpret_cast<float4*>(tile + i * kEd4Stride + lane * 4) = pr;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane < n) {
+        const int cend = min(kEd4CW, G - cb);  // a multiple of 4
+        const float* row = tile + lane * kEd4Stride;
+        for (int c = 0; c < cend; c += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(row + c);
+          const float xs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            acc = __fadd_rn(acc, xs[t]);
+            if (--left == 0) {
+              p.out[static_cast<int64_t>(my_e) * p.out_ld + head] = acc;
+              acc = 0.0f;
+              ++head;
+              left = D;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 __global__ void k_row_of_edge(const uint32_t* __restrict__ indptr, uint32_t rows,
                               uint32_t* __restrict__ rowof) {
   const uint32_t stride = gridDim.x * blockDim.x;
@@ -249,6 +341,24 @@ cudaError_t launch_row_of_edge(const uint32_t* indptr, uint32_t rows, uint32_t* 
 cudaError_t launch_dot_edges(const RowLaunch& p, const uint32_t* rowof, uint64_t m,
                              cudaStream_t s) {
   if (m == 0) return cudaSuccess;
+  auto al16 = [](const float* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+  if (p.lhs.mode == MODE_FULL && p.rhs.mode == MODE_FULL && p.gather_dim % 4 == 0 &&
+      p.lhs.ld % 4 == 0 && p.rhs.ld % 4 == 0 && al16(p.lhs.base) && al16(p.rhs.base)) {
+    const size_t smem = sizeof(float) * kEd4Warps * 32 * kEd4Stride;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_dot_edges4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+      attr = true;
+    }
+    const uint64_t batches = (m + 31) / 32;
+    uint64_t blocks = (batches + kEd4Warps - 1) / kEd4Warps;
+    const uint64_t cap = static_cast<uint64_t>(p.num_sms > 0 ? p.num_sms : 148) * 3;
+    if (blocks > cap) blocks = cap;
+    k_dot_edges4<<<static_cast<unsigned>(blocks), kEd4Warps * 32, smem, s>>>(p, rowof, m);
+    note_launch();
+    return cudaGetLastError();
+  }
   const uint64_t batches = (m + 31) / 32;
   uint64_t blocks = (batches + kEdWarps - 1) / kEdWarps;
   const uint64_t cap = static_cast<uint64_t>(p.num_sms > 0 ? p.num_sms : 148) * 16;
