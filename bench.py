@@ -417,6 +417,115 @@ def run_ours(args, rank, world, dist):
     return result
 
 
+# ------------------------------------------------- config 5 (multi-GPU)
+C5_NODES, C5_DMIN, C5_DMAX, C5_FEAT = 232_965, 90, 21_000, 602
+C5_WORKLOAD = ("cfg5: GraphSAGE-mean fwd+bwd, power-law in-degree graph 232,965 nodes "
+               "(in-degree 90..21000, mean ~495, ~115M edges, uniform sources), "
+               "x fp32 [232965 x 602] N(0,1); dst rows and source-feature rows sharded, "
+               "source features / output gradients all-gathered by 256-column chunk")
+
+
+def run_cfg5(args, rank, world, dist):
+    """--workload cfg5: BASELINE config 5 through paper_2007_06354_b200.dist.
+
+    Each rank owns an edge-balanced node range: its dst rows and its rows of
+    x.  Forward: all-gather x by column chunk (NCCL, comm stream) overlapped
+    with the per-chunk mean over the rank's CSR slice; backward: the same
+    with grad_out over the transposed slice, scaled by 1/deg (other_scale).
+    One step = forward + backward; value = 2E / step time (max over ranks),
+    all-gathers inside the timed region (with; `compute_ms`
+    reports the same step on pre-gathered inputs: without)."""
+    import torch
+    import paper_2007_06354_b200 as P
+    from paper_2007_06354_b200.dist import ShardPlan, ShardedMean
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    t0 = time.time()
+    src, dst = P.synth_powerlaw(C5_NODES, C5_DMIN, C5_DMAX, SEEDS["graph"])
+    E = len(src)
+    dcsr = P.build_csr(C5_NODES, src, dst, P.DST_MAJOR)
+    scsr = P.transpose(C5_NODES, C5_NODES, *dcsr)
+    plan = ShardPlan(*dcsr, C5_NODES, rank, world, *scsr)
+    x = np.empty((C5_NODES, C5_FEAT), np.float32)
+    P.synth_normal(C5_NODES, C5_FEAT, SEEDS["x"], out=x)
+    gy = np.empty((C5_NODES, C5_FEAT), np.float32)
+    P.synth_normal(C5_NODES, C5_FEAT, SEEDS["grad"], out=gy)
+    log(f"[bench] cfg5 rank {rank}: {E} edges, rows [{plan.lo},{plan.hi}) "
+        f"({int(plan.fwd[0][-1])} in-edges, {int(plan.bwd[0][-1])} out-edges), "
+        f"inputs {time.time() - t0:.1f}s")
+
+    allgather = None
+    if dist is None:
+        allgather = lambda full, local: full.copy_(local)  # noqa: E731  (world 1)
+    sm = ShardedMean(plan, C5_FEAT, chunk=256, device=f"cuda:{dev}", allgather=allgather)
+    ld = (C5_FEAT + 3) & ~3
+    out = torch.empty((plan.rows, ld), dtype=torch.float32, device=dev)[:, :C5_FEAT]
+    gx = torch.empty((plan.rows, ld), dtype=torch.float32, device=dev)[:, :C5_FEAT]
+    x_l = torch.from_numpy(x[plan.lo:plan.hi]).cuda(dev)
+    gy_l = torch.from_numpy(gy[plan.lo:plan.hi]).cuda(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        sm.load(x_l)
+        sm.forward(out)
+        sm.load(gy_l)
+        sm.backward(gx)
+
+    def timed(fn, k):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        t = torch.tensor([a.elapsed_time(b) / k], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    launches0 = P.launch_count()
+    with ClockSampler(dev) as clk:
+        ms = timed(step, args.steps)
+    launches = (P.launch_count() - launches0) // max(1, args.steps + args.warmup) * args.steps
+
+    # the same aggregation on already-gathered inputs (no collective)
+    def compute_only():
+        for kind, o in (("fwd", out), ("bwd", gx)):
+            for k, (c0, w, _) in enumerate(sm.chunks):
+                sm.aggregate(kind, k, sm.full[k][:, :w], o[:, c0:c0 + w], sm.scale)
+    compute_ms = timed(compute_only, args.steps)
+
+    def fwd_only():
+        for k, (c0, w, _) in enumerate(sm.chunks):
+            sm.aggregate("fwd", k, sm.full[k][:, :w], out[:, c0:c0 + w], sm.scale)
+    fwd_ms = timed(fwd_only, args.steps)
+    gathered_bytes = 2 * plan.gathered_rows * sum(wp for (_, _, wp) in sm.chunks) * 4
+    if rank != 0:
+        return None
+    return {
+        "metric": "aggregated edges/s (cfg5 GraphSAGE-mean fwd+bwd, dst-row shards + "
+                  "source-feature all-gather)",
+        "value": 2 * E / (ms * 1e-3), "unit": "edges/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (power-law in-degree graph and N(0,1) features, seeded)",
+        "config": {"workload": C5_WORKLOAD, "edges": E, "nodes": C5_NODES, "feat": C5_FEAT,
+                   "parallelism": f"node shards x{world}, NCCL all-gather by column chunk"
+                   if world > 1 else "single GPU (all-gather degenerates to a copy)",
+                   "l2": "inputs (560 MB feature matrices) larger than the 126 MB L2; no flush"},
+        "compute_ms_per_step": compute_ms, "compute_fwd_ms": fwd_ms,
+        "compute_bwd_ms": compute_ms - fwd_ms,
+        "allgather_bytes_per_step_per_rank": int(gathered_bytes),
+        "gpu_launches": int(launches), "clocks": clk.summary(), "impl": "b200",
+    }
+
+
 def run_reference(args, rank, world):
     """--impl reference: the unmodified reference library on the host cores."""
     if rank != 0:
@@ -471,6 +580,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5"],
+                    help="cfg2 (BASELINE configs[1], the headline) or cfg5 (multi-GPU "
+                         "GraphSAGE-mean with source-feature all-gather)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         log("[bench] warmup raised to 3 (timing rule)")
@@ -488,7 +600,7 @@ def main():
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
             tdist.init_process_group("nccl")
             dist = tdist
-        res = run_ours(args, rank, world, dist)
+        res = (run_cfg5 if args.workload == "cfg5" else run_ours)(args, rank, world, dist)
         if dist:
             dist.destroy_process_group()
     if rank == 0 and res is not None:

@@ -564,10 +564,11 @@ struct WsGeom {
   }
 };
 
-template <int BOP, int ROP, bool ARG, bool SMALL>
+template <int BOP, int ROP, bool ARG, int SK>
 __global__ void __launch_bounds__(kWsThreads, 1) k_long_ws(const StreamLaunch p) {
   using G = WsGeom;
   constexpr int NB = G::NB;
+  constexpr bool SMALL = SK != SK_NONE;
   extern __shared__ __align__(16) float sm[];
   __shared__ uint32_t s_unit;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -662,7 +663,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_long_ws(const StreamLaunch p)
       const uint32_t ldb = static_cast<uint32_t>(lld) * 4u;
       const uint32_t slot_b = static_cast<uint32_t>(slot_f) * 4u;
       const uint32_t tstep = static_cast<uint32_t>(lpe) * 16u;
-      const bool small1 = SMALL && (rw == 1 || (rw == 0 && scale_on));
+      constexpr bool small1 = SK == SK_WIN || SK == SK_SCALE;
       const float* s1base = rw == 1 ? L.rhs.base : L.other_scale;
       const int64_t s1ld = rw == 1 ? L.rhs.ld : 1;
       const int32_t s1role = rw == 1 ? L.rhs.role : static_cast<int32_t>(ROLE_OTHER);
@@ -744,12 +745,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_long_ws(const StreamLaunch p)
 #pragma unroll
               for (int t = 0; t < FW; ++t) {
                 float m;
-                if constexpr (SMALL) {
-                  if (rw > 0) m = bin_apply<BOP>(x[t], sval);
-                  else m = __fmul_rn(bin_apply<BOP>(x[t], 0.0f), sval);
-                } else {
-                  m = bin_apply<BOP>(x[t], 0.0f);
-                }
+                if constexpr (SK == SK_SCALE) m = __fmul_rn(bin_apply<BOP>(x[t], 0.0f), sval);
+                else if constexpr (SK == SK_NONE) m = bin_apply<BOP>(x[t], 0.0f);
+                else m = bin_apply<BOP>(x[t], sval);
                 if constexpr (ARG) {
                   if (red_wins<ROP>(acc[t], m)) {
                     acc[t] = m;
@@ -1071,7 +1069,7 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured_w != dev) {
-      e = cudaFuncSetAttribute(k_long_ws<BOP, ROP, ARG, SMALL>,
+      e = cudaFuncSetAttribute(k_long_ws<BOP, ROP, ARG, SK>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(WsGeom::smem_bytes(small)));
       if (e != cudaSuccess) return e;
@@ -1079,7 +1077,7 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     }
     unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
     if (grid > p.n_units) grid = p.n_units;
-    k_long_ws<BOP, ROP, ARG, SMALL><<<grid, kWsThreads, WsGeom::smem_bytes(small), s>>>(p);
+    k_long_ws<BOP, ROP, ARG, SK><<<grid, kWsThreads, WsGeom::smem_bytes(small), s>>>(p);
   } else if (p.mode == 1) {
     const int rws = SMALL ? (p.rhs_width > 0 ? p.rhs_width : 1) : 0;
     const size_t smem = LongGeom<VPL>::smem_bytes(rws);
