@@ -183,6 +183,22 @@ int gspmm_argmax_backward(const int32_t* arg, int64_t rows, int64_t dim,
                           int64_t grad_ld, float* grad_src, int64_t src_rows,
                           int64_t src_ld, void* stream);
 
+/* Fused GAT edge softmax over the in-edges of each destination (
+ * the composite e_copy_max_v -> e_sub_v_copy_e -> exp -> e_copy_add_v ->
+ * e_div_v_copy_e of PAPER Table 2): per head h,
+ *   a[e,h] = expf(l[e,h] - m[v,h]) / z[v,h],  m = max, z = sum over in-edges of v.
+ * Dst-major handle.  logits / out: E x heads (heads <= 32), rows in the
+ * logits' edge_order (GSPMM_EDGE_BY_ID: row = edge id; BY_POS: CSR position);
+ * out uses the same order.  The max is the reference reducer; z is an fp32
+ * sum in a fixed order (deterministic); parity with the composite is within
+ * tolerance (expf). */
+int gspmm_edge_softmax(gspmm_graph g, const gspmm_mat* logits,
+                       const gspmm_out* out, void* stream);
+/* Its backward: grad_l[e,h] = a[e,h] * (grad_a[e,h] - sum_row(a * grad_a)[v,h]). */
+int gspmm_edge_softmax_backward(gspmm_graph g, const gspmm_mat* a,
+                                const gspmm_mat* grad_a,
+                                const gspmm_out* grad_logits, void* stream);
+
 /* ---- host-buffer entry (the reference's synchronous call shape) ----
  * Same arguments with HOST pointers; copies in, computes, copies out and
  * synchronizes.  Pinned host memory makes the copies asynchronous DMA. */

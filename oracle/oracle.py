@@ -472,6 +472,14 @@ def softmax_attention(n, dst, logits):
     return (ex / den[dst]).astype(np.float32)
 
 
+def softmax_attention_backward(n, dst, a, grad_a):
+    """Edge-softmax backward (f64): grad_l = a * (grad_a - sum_row(a * grad_a))."""
+    a64, g64 = a.astype(np.float64), grad_a.astype(np.float64)
+    s = np.zeros((n, a.shape[1]))
+    np.add.at(s, dst, a64 * g64)
+    return a64 * (g64 - s[dst])
+
+
 # ----------------------------------------------------------- comparisons
 def max_rel_error(got, want):
     got = np.ascontiguousarray(got, np.float32)

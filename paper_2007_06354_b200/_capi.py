@@ -93,6 +93,8 @@ SIGNATURES = {
                                       _P(Options), _vp]),
     "gspmm_copy_reduce": (_i32, [_vp, _P(Mat), _i32, _P(Out), _vp]),
     "gspmm_argmax_backward": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
+    "gspmm_edge_softmax": (_i32, [_vp, _P(Mat), _P(Out), _vp]),
+    "gspmm_edge_softmax_backward": (_i32, [_vp, _P(Mat), _P(Mat), _P(Out), _vp]),
     "gspmm_binary_reduce_host": (_i32, [_vp, _P(Config), _P(Mat), _P(Mat), _P(Mat), _P(Out),
                                         _P(Options), _vp]),
     "gspmm_out_shape": (_i32, [_vp, _P(Config), _P(Mat), _P(Mat), _P(Mat), _P(Options),

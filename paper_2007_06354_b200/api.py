@@ -20,7 +20,7 @@ __all__ = [
     "Graph", "binary_reduce", "binary_reduce_host", "copy_reduce", "argmax_backward",
     "named_config", "validate_config", "required_orientation", "out_shape",
     "synth_rmat", "synth_er", "build_csr", "transpose", "synth_uniform", "synth_normal",
-    "synth_gcn_weights", "synth_powerlaw", "launch_count",
+    "synth_gcn_weights", "synth_powerlaw", "launch_count", "edge_softmax", "edge_softmax_backward",
 ]
 
 
@@ -239,6 +239,35 @@ def argmax_backward(arg, grad_out, src_rows, *, out=None, stream=None):
                                       grad_out.data_ptr(), grad_out.stride(0), out.data_ptr(),
                                       src_rows, out.stride(0), _stream(stream, grad_out)),
           "argmax_backward")
+    return out
+
+
+def edge_softmax(graph, logits, *, out=None, e_order=EDGE_BY_ID, stream=None):
+    """Fused GAT edge softmax over in-edges (dst-major handle): logits [E, H]
+    (H <= 32) in `e_order`; returns a [E, H] in the same order."""
+    import torch
+    lg = logits if logits.dim() == 2 else logits.reshape(-1, 1)
+    if out is None:
+        out = torch.empty(lg.shape, dtype=torch.float32, device=lg.device)
+    o2 = out if out.dim() == 2 else out.reshape(-1, 1)
+    mo = A.Out(o2.data_ptr(), o2.shape[0], o2.shape[1], o2.stride(0))
+    check(A.LIB.gspmm_edge_softmax(graph.handle, C.byref(_dev_mat(lg, e_order)), C.byref(mo),
+                                   _stream(stream, lg)), "edge_softmax")
+    return out
+
+
+def edge_softmax_backward(graph, a, grad_a, *, out=None, e_order=EDGE_BY_ID, stream=None):
+    """grad_logits = a * (grad_a - sum over the row of a * grad_a)."""
+    import torch
+    a2 = a if a.dim() == 2 else a.reshape(-1, 1)
+    g2 = grad_a if grad_a.dim() == 2 else grad_a.reshape(-1, 1)
+    if out is None:
+        out = torch.empty(a2.shape, dtype=torch.float32, device=a2.device)
+    o2 = out if out.dim() == 2 else out.reshape(-1, 1)
+    mo = A.Out(o2.data_ptr(), o2.shape[0], o2.shape[1], o2.stride(0))
+    check(A.LIB.gspmm_edge_softmax_backward(graph.handle, C.byref(_dev_mat(a2, e_order)),
+                                            C.byref(_dev_mat(g2, e_order)), C.byref(mo),
+                                            _stream(stream, a2)), "edge_softmax_backward")
     return out
 
 

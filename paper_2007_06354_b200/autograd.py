@@ -12,6 +12,7 @@ library's sm_100a kernels (no torch compute on the hot path):
                       [E, H] per head)             grad_w = u_dot_v_copy_e(x, dy)       (out = E, per head)
   u_add_v_sum(x, y)   u_add_v_add_v                grad_x = v_copy_add_u(dy); grad_y = v_copy_add_v(dy)
   u_mul_v_sum(x, y)   u_mul_v_add_v                grad_x = v_copy_add_u(dy * y);  grad_y = u_mul_v_add_v(x, dy)
+  edge_softmax(l)     fused max/exp/sum/div        grad_l = a * (da - sum_row(a * da))  (fused)
 
 u_mul_v's grad_x[u] = sum_v dy[v] * y[v] needs the product of two V rows per
 edge, which the operator set cannot express in one call (lhs != rhs,
@@ -31,7 +32,7 @@ import torch
 from . import api as P
 
 __all__ = ["GraphOps", "copy_u_sum", "copy_u_mean", "copy_u_max", "copy_e_sum", "u_mul_e_sum",
-           "u_add_v_sum", "u_mul_v_sum"]
+           "u_add_v_sum", "u_mul_v_sum", "edge_softmax"]
 
 
 class GraphOps:
@@ -156,6 +157,25 @@ class _UMulVSum(torch.autograd.Function):
         gx = P.binary_reduce(g.bwd, (P.V, P.NONE, P.COPY, P.SUM, P.U), v=_c(dy * y))
         gy = P.binary_reduce(g.fwd, "u_mul_v_add_v", u=_c(x), v=dy)
         return None, gx, gy
+
+
+class _EdgeSoftmax(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, g, logits):
+        a = P.edge_softmax(g.fwd, _c(logits))
+        ctx.g = g
+        ctx.save_for_backward(a)
+        return a
+
+    @staticmethod
+    def backward(ctx, da):
+        (a,) = ctx.saved_tensors
+        return None, P.edge_softmax_backward(ctx.g.fwd, a, _c(da))
+
+
+def edge_softmax(g, logits):
+    """GAT attention: softmax of logits [E, H] over the in-edges of each node."""
+    return _EdgeSoftmax.apply(g, logits)
 
 
 def copy_u_sum(g, x):

@@ -790,6 +790,51 @@ int gspmm_copy_reduce(gspmm_graph g, const gspmm_mat* src, int reduce,
   return fail(GSPMM_ERR_SHAPE, "copy_reduce: source rows match neither the node nor the edge count");
 }
 
+// Fused GAT edge softmax (softmax.cu) over the in-edges of each destination.
+static int softmax_common(gspmm_graph g, bool backward, const gspmm_mat* l, const gspmm_mat* ga,
+                   const gspmm_out* out, void* stream) {
+  if (!g || !l || !out || (backward && !ga)) return fail(GSPMM_ERR_ARG, "null argument");
+  if (g->orientation != GSPMM_DST_MAJOR)
+    return fail(GSPMM_ERR_SHAPE, "edge_softmax: needs the dst-major handle (softmax over in-edges)");
+  const int64_t m = static_cast<int64_t>(g->m);
+  const int64_t heads = l->dim;
+  if (heads < 1 || heads > 32) return fail(GSPMM_ERR_SHAPE, "edge_softmax: 1..32 heads");
+  auto check = [&](int64_t rows, int64_t dim, int64_t ld, const char* what) -> int {
+    if (rows != m || dim != heads || (ld != 0 && ld < dim))
+      return fail(GSPMM_ERR_SHAPE, std::string("edge_softmax: ") + what + " must be " +
+                                       std::to_string(m) + " x " + std::to_string(heads));
+    return GSPMM_OK;
+  };
+  int st = check(l->rows, l->dim, l->ld, backward ? "a" : "logits");
+  if (!st && backward) st = check(ga->rows, ga->dim, ga->ld, "grad_a");
+  if (!st) st = check(out->rows, out->dim, out->ld, "out");
+  if (st) return st;
+  if (backward && ga->edge_order != l->edge_order)
+    return fail(GSPMM_ERR_ARG, "edge_softmax: a and grad_a must share one edge order");
+  if (m && (!l->data || !out->data || (backward && !ga->data)))
+    return fail(GSPMM_ERR_ARG, "null data");
+  CUDA_TRY(cudaSetDevice(g->device), "cudaSetDevice");
+  const auto& lv = g->level[0];
+  const cudaError_t e = launch_edge_softmax(
+      backward, g->d_indptr, g->d_eids, g->num_rows, static_cast<int>(heads),
+      l->edge_order == GSPMM_EDGE_BY_POS, l->data, l->ld ? l->ld : heads,
+      backward ? ga->data : nullptr, backward ? (ga->ld ? ga->ld : heads) : 0, out->data,
+      out->ld ? out->ld : heads, lv.d_long, lv.num_long, lv.threshold, g->num_sms,
+      static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "edge_softmax");
+  return GSPMM_OK;
+}
+
+int gspmm_edge_softmax(gspmm_graph g, const gspmm_mat* logits, const gspmm_out* out,
+                       void* stream) {
+  return softmax_common(g, false, logits, nullptr, out, stream);
+}
+
+int gspmm_edge_softmax_backward(gspmm_graph g, const gspmm_mat* a, const gspmm_mat* grad_a,
+                                const gspmm_out* grad_logits, void* stream) {
+  return softmax_common(g, true, a, grad_a, grad_logits, stream);
+}
+
 int gspmm_argmax_backward(const int32_t* arg, int64_t rows, int64_t dim,
                           int64_t arg_ld, const float* grad_out, int64_t grad_ld,
                           float* grad_src, int64_t src_rows, int64_t src_ld,

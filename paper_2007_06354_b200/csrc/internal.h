@@ -81,6 +81,15 @@ cudaError_t launch_argmax_backward(const int32_t* arg, int64_t rows,
                                    int64_t src_ld, double* acc,
                                    cudaStream_t s);
 
+// Fused edge softmax over in-edges (softmax.cu): forward (l -> out = a) or
+// backward (l = a, g = grad_a -> out = grad_l).  Rows above long_threshold
+// edges are listed in long_rows and run one CTA per row.
+cudaError_t launch_edge_softmax(bool backward, const uint32_t* indptr, const uint32_t* eids,
+                                uint32_t rows, int heads, bool by_pos, const float* l,
+                                int64_t l_ld, const float* g, int64_t g_ld, float* out,
+                                int64_t out_ld, const uint32_t* long_rows, uint32_t n_long,
+                                uint32_t long_threshold, int num_sms, cudaStream_t s);
+
 // Launch counter (evidence of native execution), bumped by each launcher.
 void note_launch(uint64_t n = 1);
 

@@ -66,6 +66,8 @@ CASES = {
     "cfg5mean": ("powerlaw", 232_965, 0, 602, False, False, "mean604"),
     "cfg2dot": ("rmat", 1_000_000, 16_000_000, 256, True, False, "dot"),
     "cfg4dot": ("rmat", 1_000_000, 32_000_000, 512, False, False, "dotheads"),
+    "cfg4softmax": ("rmat", 1_000_000, 32_000_000, 8, False, False, "softmax"),
+    "cfg4softmaxbwd": ("rmat", 1_000_000, 32_000_000, 8, False, False, "softmaxbwd"),
 }
 
 
@@ -111,11 +113,25 @@ def run(name):
         fn = lambda: P.binary_reduce(g, (P.U, P.V, P.DOT, P.COPY_LAST, P.E), u=x, v=y, out=oe,
                                      heads=heads)
         eb = E * heads * 4 - n * F * 4  # writes E x heads, reads y rows per edge (cached)
+    elif op in ("softmax", "softmaxbwd"):
+        # GAT attention over 8 heads: logits in CSR order, E x 8
+        lg = torch.randn(E, F, device="cuda")
+        a = P.edge_softmax(g, lg, e_order=P.EDGE_BY_POS)
+        ga = torch.randn(E, F, device="cuda")
+        if op == "softmax":
+            fn = lambda: P.edge_softmax(g, lg, out=a, e_order=P.EDGE_BY_POS)
+            eb = 0
+        else:
+            gl = torch.empty_like(a)
+            fn = lambda: P.edge_softmax_backward(g, a, ga, out=gl, e_order=P.EDGE_BY_POS)
+            eb = E * F * 4  # reads a and grad_a
     else:
         fn = lambda: P.binary_reduce(g, "u_copy_add_v", u=x, out=out)
         eb = 0
     ms = time_pass(fn)
     byts = E * F * 4 + (n + 1) * 4 + E * 4 + eb + n * F * 4
+    if op in ("softmax", "softmaxbwd"):  # read logits (a, grad_a) once, write once; indptr
+        byts = E * F * 4 * 2 + eb + (n + 1) * 4
     gbs = byts / ms / 1e6
     res = dict(case=name, E=E, F=F, ms=round(ms, 4), gbs=round(gbs, 1), frac=round(gbs / PEAK, 3),
                max_deg=int(deg.max()), long_rows=g.num_long_rows,
