@@ -148,6 +148,13 @@ int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
                        uint32_t num_cols, const uint32_t* indptr,
                        const uint32_t* indices, const uint32_t* edge_ids,
                        int validate, gspmm_graph* out);
+/* Same, from DEVICE arrays of a canonical CSR (e.g. gspmm_build_csr_device
+ * output): indptr is read back for the row plan, indices / edge_ids are
+ * copied device to device.  No host validation. */
+int gspmm_graph_create_device(int device, int orientation, uint32_t num_rows,
+                              uint32_t num_cols, const uint32_t* d_indptr,
+                              const uint32_t* d_indices,
+                              const uint32_t* d_edge_ids, gspmm_graph* out);
 int gspmm_graph_destroy(gspmm_graph g);
 int gspmm_graph_info(gspmm_graph g, int* orientation, uint32_t* num_rows,
                      uint32_t* num_cols, uint64_t* num_edges,
@@ -234,6 +241,20 @@ int gspmm_transpose(uint32_t num_rows, uint32_t num_cols,
                     const uint32_t* indptr, const uint32_t* indices,
                     const uint32_t* edge_ids, uint32_t* t_indptr,
                     uint32_t* t_indices, uint32_t* t_edge_ids, int threads);
+/* Device-side canonical CSR construction (csr.cpp:31-109 on the GPU):
+ * d_src / d_dst in edge-id order -> indptr[n+1], indices[m], edge_ids[m]
+ * (rows = dst for GSPMM_DST_MAJOR, src for GSPMM_SRC_MAJOR; neighbours
+ * ascending, then edge id).  Bit-identical to gspmm_build_csr. */
+int gspmm_build_csr_device(uint32_t n, int64_t m, const uint32_t* d_src,
+                           const uint32_t* d_dst, int orientation,
+                           uint32_t* d_indptr, uint32_t* d_indices,
+                           uint32_t* d_edge_ids, void* stream);
+/* Device-side transpose of a canonical CSR (csr.cpp:95-109). */
+int gspmm_transpose_device(uint32_t num_rows, uint32_t num_cols, int64_t m,
+                           const uint32_t* d_indptr, const uint32_t* d_indices,
+                           const uint32_t* d_edge_ids, uint32_t* d_t_indptr,
+                           uint32_t* d_t_indices, uint32_t* d_t_edge_ids,
+                           void* stream);
 /* U[-1,1) (random_features, generate.cpp:256-266) and builder N(0,1) */
 void gspmm_synth_uniform(int64_t count, uint64_t seed, float* out, int threads);
 void gspmm_synth_normal(int64_t count, uint64_t seed, float* out, int threads);

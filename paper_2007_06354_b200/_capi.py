@@ -84,6 +84,7 @@ SIGNATURES = {
     "gspmm_named_config": (_i32, [C.c_char_p, _P(Config)]),
     "gspmm_required_orientation": (_i32, [_i32, _i32]),
     "gspmm_graph_create": (_i32, [_i32, _i32, _u32, _u32, _vp, _vp, _vp, _i32, _P(_vp)]),
+    "gspmm_graph_create_device": (_i32, [_i32, _i32, _u32, _u32, _vp, _vp, _vp, _P(_vp)]),
     "gspmm_graph_destroy": (_i32, [_vp]),
     "gspmm_graph_info": (_i32, [_vp, _P(_i32), _P(_u32), _P(_u32), _P(_u64), _P(_u32)]),
     "gspmm_graph_device_csr": (_i32, [_vp, _P(_vp), _P(_vp), _P(_vp)]),
@@ -105,6 +106,8 @@ SIGNATURES = {
     "gspmm_free": (None, [_vp]),
     "gspmm_build_csr": (_i32, [_u32, _i64, _vp, _vp, _i32, _vp, _vp, _vp, _i32]),
     "gspmm_transpose": (_i32, [_u32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _i32]),
+    "gspmm_build_csr_device": (_i32, [_u32, _i64, _vp, _vp, _i32, _vp, _vp, _vp, _vp]),
+    "gspmm_transpose_device": (_i32, [_u32, _u32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "gspmm_synth_uniform": (None, [_i64, _u64, _vp, _i32]),
     "gspmm_synth_normal": (None, [_i64, _u64, _vp, _i32]),
     "gspmm_synth_gcn_weights": (None, [_u32, _i64, _vp, _vp, _vp, _i32]),

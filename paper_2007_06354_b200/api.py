@@ -21,6 +21,7 @@ __all__ = [
     "named_config", "validate_config", "required_orientation", "out_shape",
     "synth_rmat", "synth_er", "build_csr", "transpose", "synth_uniform", "synth_normal",
     "synth_gcn_weights", "synth_powerlaw", "launch_count", "edge_softmax", "edge_softmax_backward",
+    "build_csr_device", "transpose_device",
 ]
 
 
@@ -88,6 +89,29 @@ class Graph:
         nl = C.c_uint32()
         check(A.LIB.gspmm_graph_info(h, None, None, None, None, C.byref(nl)))
         self.num_long_rows = nl.value
+
+    @classmethod
+    def from_device(cls, indptr, indices, edge_ids, num_rows=None, num_cols=None,
+                    orientation=DST_MAJOR):
+        """Handle over a canonical CSR held in CUDA tensors (int32 storage of
+        the u32 arrays, e.g. from ``build_csr_device``): no host round trip
+        except indptr for the row plan."""
+        self = cls.__new__(cls)
+        self.num_rows = indptr.numel() - 1 if num_rows is None else int(num_rows)
+        self.num_cols = self.num_rows if num_cols is None else int(num_cols)
+        self.orientation = orientation
+        self.device = indptr.device.index or 0
+        self.num_edges = int(indices.numel())
+        h = C.c_void_p()
+        check(A.LIB.gspmm_graph_create_device(self.device, orientation, self.num_rows, self.num_cols,
+                                              indptr.data_ptr(), indices.data_ptr(),
+                                              edge_ids.data_ptr(), C.byref(h)),
+              "graph_create_device")
+        self._h = h
+        nl = C.c_uint32()
+        check(A.LIB.gspmm_graph_info(h, None, None, None, None, C.byref(nl)))
+        self.num_long_rows = nl.value
+        return self
 
     @property
     def handle(self):
@@ -334,6 +358,37 @@ def transpose(num_rows, num_cols, indptr, indices, eids, threads=0):
                                 _ptr(t_indptr), _ptr(t_indices), _ptr(t_eids), threads),
           "transpose")
     return t_indptr, t_indices[:m], t_eids[:m]
+
+
+def build_csr_device(n, src, dst, orientation=DST_MAJOR, stream=None):
+    """Canonical CSR on the device from CUDA edge lists (int32/uint32 storage,
+    edge-id order); returns (indptr, indices, edge_ids) as int32 CUDA
+    tensors holding the u32 values.  Bit-identical to ``build_csr``."""
+    import torch
+    m = src.numel()
+    dev = src.device
+    indptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    indices = torch.empty(max(m, 1), dtype=torch.int32, device=dev)[:m]
+    eids = torch.empty(max(m, 1), dtype=torch.int32, device=dev)[:m]
+    check(A.LIB.gspmm_build_csr_device(n, m, src.data_ptr(), dst.data_ptr(), orientation,
+                                       indptr.data_ptr(), indices.data_ptr(), eids.data_ptr(),
+                                       _stream(stream, src)), "build_csr_device")
+    return indptr, indices, eids
+
+
+def transpose_device(num_rows, num_cols, indptr, indices, eids, stream=None):
+    """Device transpose of a canonical CSR (int32 CUDA tensors)."""
+    import torch
+    m = indices.numel()
+    dev = indptr.device
+    t_indptr = torch.empty(num_cols + 1, dtype=torch.int32, device=dev)
+    t_indices = torch.empty(max(m, 1), dtype=torch.int32, device=dev)[:m]
+    t_eids = torch.empty(max(m, 1), dtype=torch.int32, device=dev)[:m]
+    check(A.LIB.gspmm_transpose_device(num_rows, num_cols, m, indptr.data_ptr(),
+                                       indices.data_ptr(), eids.data_ptr(), t_indptr.data_ptr(),
+                                       t_indices.data_ptr(), t_eids.data_ptr(),
+                                       _stream(stream, indptr)), "transpose_device")
+    return t_indptr, t_indices, t_eids
 
 
 def synth_uniform(rows, dim, seed, threads=0, out=None):

@@ -1,0 +1,127 @@
+// build.cu -- device-side canonical CSR construction:
+// the GPU analogue of build_csr / from_keys / transpose (csr.cpp:31-109).
+//
+// Canonical order (csr.hpp:31-35): rows ascending, within a row neighbour
+// ascending, then edge id ascending.  Edges arrive in edge-id order, so one
+// STABLE radix sort of the 64-bit key (row << 32 | neighbour) with the edge
+// id as the value gives exactly that order (equal keys keep edge-id order).
+// indptr is the exclusive scan of the row histogram.  The transpose sorts
+// (neighbour << 32 | row) of the canonical CSR with the original edge ids:
+// within an equal key the input is already in edge-id order, and the stable
+// sort keeps it.  CUB's radix sort / scan are used as library primitives
+// (setup path, not the aggregation hot path).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "internal.h"
+
+namespace gspmm_b200 {
+namespace {
+
+__global__ void k_make_keys(const uint32_t* __restrict__ row, const uint32_t* __restrict__ col,
+                            uint64_t m, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                            const uint32_t* __restrict__ val_src) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
+    keys[i] = (static_cast<uint64_t>(__ldg(row + i)) << 32) | __ldg(col + i);
+    vals[i] = val_src ? __ldg(val_src + i) : static_cast<uint32_t>(i);
+  }
+}
+
+__global__ void k_split_keys(const uint64_t* __restrict__ keys, uint64_t m,
+                             uint32_t* __restrict__ indices, uint32_t* __restrict__ counts) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const uint64_t k = keys[i];
+    indices[i] = static_cast<uint32_t>(k);
+    atomicAdd(counts + static_cast<uint32_t>(k >> 32), 1u);
+  }
+}
+
+__global__ void k_rows_of(const uint32_t* __restrict__ indptr, uint32_t rows,
+                          uint32_t* __restrict__ rowof) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride)
+    for (uint32_t j = __ldg(indptr + r); j < __ldg(indptr + r + 1); ++j) rowof[j] = r;
+}
+
+int bits_for(uint32_t n) {
+  int b = 1;
+  while (b < 32 && (1ull << b) < n) ++b;
+  return b;
+}
+
+// rows[i], cols[i] for i < m (edge-id order, or the canonical CSR order for
+// a transpose with vals = its edge ids) -> canonical CSR with num_rows rows.
+cudaError_t sort_build(uint32_t num_rows, uint32_t num_cols, uint64_t m, const uint32_t* rows,
+                       const uint32_t* cols, const uint32_t* vals_in, uint32_t* indptr,
+                       uint32_t* indices, uint32_t* eids, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  uint64_t *k0 = nullptr, *k1 = nullptr;
+  uint32_t *v0 = nullptr, *counts = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0, scan_bytes = 0;
+  const size_t mm = m ? m : 1;
+  const int end_bit = 32 + bits_for(num_rows ? num_rows : 1);
+  (void)num_cols;
+  auto done = [&](cudaError_t err) {
+    cudaFreeAsync(k0, s);
+    cudaFreeAsync(k1, s);
+    cudaFreeAsync(v0, s);
+    cudaFreeAsync(counts, s);
+    cudaFreeAsync(tmp, s);
+    return err;
+  };
+  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&k0), 8 * mm, s))) return done(e);
+  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&k1), 8 * mm, s))) return done(e);
+  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&v0), 4 * mm, s))) return done(e);
+  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&counts), 4 * (size_t(num_rows) + 1), s)))
+    return done(e);
+  if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, v0, eids, m, 0, end_bit, s)))
+    return done(e);
+  if ((e = cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, counts, indptr, num_rows + 1, s)))
+    return done(e);
+  if ((e = cudaMallocAsync(&tmp, std::max(tmp_bytes, scan_bytes) + 16, s))) return done(e);
+  const unsigned grid = 148 * 8;
+  if (m) {
+    k_make_keys<<<grid, 256, 0, s>>>(rows, cols, m, k0, v0, vals_in);
+    note_launch();
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, v0, eids, m, 0, end_bit, s)))
+      return done(e);
+  }
+  if ((e = cudaMemsetAsync(counts, 0, 4 * (size_t(num_rows) + 1), s))) return done(e);
+  if (m) {
+    k_split_keys<<<grid, 256, 0, s>>>(k1, m, indices, counts);
+    note_launch();
+  }
+  size_t sb = std::max(tmp_bytes, scan_bytes) + 16;
+  if ((e = cub::DeviceScan::ExclusiveSum(tmp, sb, counts, indptr, num_rows + 1, s))) return done(e);
+  return done(cudaGetLastError());
+}
+
+}  // namespace
+
+cudaError_t launch_build_csr(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                             bool dst_major, uint32_t* indptr, uint32_t* indices, uint32_t* eids,
+                             cudaStream_t s) {
+  return sort_build(n, n, m, dst_major ? dst : src, dst_major ? src : dst, nullptr, indptr,
+                    indices, eids, s);
+}
+
+cudaError_t launch_transpose_csr(uint32_t num_rows, uint32_t num_cols, uint64_t m,
+                                 const uint32_t* indptr, const uint32_t* indices,
+                                 const uint32_t* eids, uint32_t* t_indptr, uint32_t* t_indices,
+                                 uint32_t* t_eids, cudaStream_t s) {
+  uint32_t* rowof = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&rowof), 4 * (m ? m : 1), s);
+  if (e) return e;
+  if (num_rows) {
+    k_rows_of<<<148 * 8, 256, 0, s>>>(indptr, num_rows, rowof);
+    note_launch();
+  }
+  e = sort_build(num_cols, num_rows, m, indices, rowof, eids, t_indptr, t_indices, t_eids, s);
+  cudaFreeAsync(rowof, s);
+  return e;
+}
+
+}  // namespace gspmm_b200

@@ -658,10 +658,11 @@ int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
                       cudaMemcpyHostToDevice)) != cudaSuccess)
     return cleanup(e, "upload indptr");
   if (m) {
-    if ((e = cudaMemcpy(g->d_indices, indices, sizeof(uint32_t) * m, cudaMemcpyHostToDevice)) !=
+    // host or device arrays (gspmm_graph_create_device): direction from UVA
+    if ((e = cudaMemcpy(g->d_indices, indices, sizeof(uint32_t) * m, cudaMemcpyDefault)) !=
         cudaSuccess)
       return cleanup(e, "upload indices");
-    if ((e = cudaMemcpy(g->d_eids, edge_ids, sizeof(uint32_t) * m, cudaMemcpyHostToDevice)) !=
+    if ((e = cudaMemcpy(g->d_eids, edge_ids, sizeof(uint32_t) * m, cudaMemcpyDefault)) !=
         cudaSuccess)
       return cleanup(e, "upload edge_ids");
   }
@@ -685,6 +686,49 @@ int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
   if ((e = cudaMalloc(&g->d_counter, 2 * sizeof(uint32_t))) != cudaSuccess)
     return cleanup(e, "cudaMalloc counter");
   *out = g;
+  return GSPMM_OK;
+}
+
+int gspmm_graph_create_device(int device, int orientation, uint32_t num_rows,
+                              uint32_t num_cols, const uint32_t* d_indptr,
+                              const uint32_t* d_indices, const uint32_t* d_edge_ids,
+                              gspmm_graph* out) {
+  if (!out || !d_indptr) return fail(GSPMM_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(device), "cudaSetDevice");
+  // the row plan is built on the host from indptr (rows + 1 words)
+  std::vector<uint32_t> h(static_cast<size_t>(num_rows) + 1);
+  CUDA_TRY(cudaMemcpy(h.data(), d_indptr, sizeof(uint32_t) * h.size(), cudaMemcpyDeviceToHost),
+           "download indptr");
+  return gspmm_graph_create(device, orientation, num_rows, num_cols, h.data(), d_indices,
+                            d_edge_ids, 0, out);
+}
+
+int gspmm_build_csr_device(uint32_t n, int64_t m, const uint32_t* d_src, const uint32_t* d_dst,
+                           int orientation, uint32_t* d_indptr, uint32_t* d_indices,
+                           uint32_t* d_edge_ids, void* stream) {
+  if (m < 0 || !d_indptr || (m && (!d_src || !d_dst || !d_indices || !d_edge_ids)))
+    return fail(GSPMM_ERR_ARG, "null argument");
+  if (orientation != GSPMM_SRC_MAJOR && orientation != GSPMM_DST_MAJOR)
+    return fail(GSPMM_ERR_ARG, "orientation must be 0 (src-major) or 1 (dst-major)");
+  if (static_cast<uint64_t>(m) > 0xffffffffull) return fail(GSPMM_ERR_ARG, "more than 2^32 - 1 edges");
+  const cudaError_t e = launch_build_csr(n, static_cast<uint64_t>(m), d_src, d_dst,
+                                         orientation == GSPMM_DST_MAJOR, d_indptr, d_indices,
+                                         d_edge_ids, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "build_csr_device");
+  return GSPMM_OK;
+}
+
+int gspmm_transpose_device(uint32_t num_rows, uint32_t num_cols, int64_t m,
+                           const uint32_t* d_indptr, const uint32_t* d_indices,
+                           const uint32_t* d_edge_ids, uint32_t* d_t_indptr,
+                           uint32_t* d_t_indices, uint32_t* d_t_edge_ids, void* stream) {
+  if (m < 0 || !d_indptr || !d_t_indptr ||
+      (m && (!d_indices || !d_edge_ids || !d_t_indices || !d_t_edge_ids)))
+    return fail(GSPMM_ERR_ARG, "null argument");
+  const cudaError_t e = launch_transpose_csr(num_rows, num_cols, static_cast<uint64_t>(m), d_indptr,
+                                             d_indices, d_edge_ids, d_t_indptr, d_t_indices,
+                                             d_t_edge_ids, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "transpose_device");
   return GSPMM_OK;
 }
 

@@ -90,6 +90,15 @@ cudaError_t launch_edge_softmax(bool backward, const uint32_t* indptr, const uin
                                 int64_t out_ld, const uint32_t* long_rows, uint32_t n_long,
                                 uint32_t long_threshold, int num_sms, cudaStream_t s);
 
+// Device-side canonical CSR build / transpose (build.cu).
+cudaError_t launch_build_csr(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                             bool dst_major, uint32_t* indptr, uint32_t* indices, uint32_t* eids,
+                             cudaStream_t s);
+cudaError_t launch_transpose_csr(uint32_t num_rows, uint32_t num_cols, uint64_t m,
+                                 const uint32_t* indptr, const uint32_t* indices,
+                                 const uint32_t* eids, uint32_t* t_indptr, uint32_t* t_indices,
+                                 uint32_t* t_eids, cudaStream_t s);
+
 // Launch counter (evidence of native execution), bumped by each launcher.
 void note_launch(uint64_t n = 1);
 
