@@ -100,6 +100,32 @@ struct gspmm_graph_s {
   size_t ws_bytes = 0;
 };
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// libcuda link dependency).
+bool gspmm_b200::encode_rows_tmap(CUtensorMap* map, const OperandDesc& d, int width, int box) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode enc = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<Encode>(f);
+  }();
+  if (!enc || box < 8 || box > 256 || box % 8 || d.ld % 4 || d.rows < 1) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(width), static_cast<cuuint64_t>(d.rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(d.ld) * 4u};
+  const cuuint32_t boxd[2] = {static_cast<cuuint32_t>(box), 1u};
+  const cuuint32_t es[2] = {1u, 1u};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(d.base), dims, strides,
+             boxd, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 namespace {
 
 // ---------------------------------------------------------------- config
@@ -218,6 +244,7 @@ int bind(const gspmm_graph_s* g, const gspmm_config* cfg, const gspmm_mat* u,
     OperandDesc d;
     d.base = m->data;
     d.ld = m->ld ? m->ld : m->dim;
+    d.rows = m->rows;
     d.role = role_of(g, o, m->edge_order);
     if (m->dim == 1 && gather > 1) {
       d.mode = MODE_SCALAR;  // stride 0, kernels.cpp:451-453
@@ -362,26 +389,47 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
     p.tma_min_bytes = tma_min;
     static const char* trace_path = std::getenv("GSPMM_UNIT_TRACE");
     // development aid: per-unit timing of one launch, appended to a file
+    // (GSPMM_UNIT_TRACE_CONCURRENT=1: the launches of the call are not
+    // serialised; the buffers are read back after the join)
+    static const bool trace_conc = env_u32("GSPMM_UNIT_TRACE_CONCURRENT", 0) != 0;
+    struct Pending {
+      unsigned long long* d;
+      size_t bytes;
+      unsigned long long hdr[4];
+    };
+    std::vector<Pending> pending;
+    auto flush_trace = [&](cudaStream_t st) {
+      cudaStreamSynchronize(st);
+      for (auto& pd : pending) {
+        std::vector<unsigned long long> h(pd.bytes / sizeof(unsigned long long));
+        cudaMemcpy(h.data(), pd.d, pd.bytes, cudaMemcpyDeviceToHost);
+        if (FILE* f = std::fopen(trace_path, "ab")) {
+          std::fwrite(pd.hdr, sizeof(pd.hdr), 1, f);
+          std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+          std::fclose(f);
+        }
+      }
+      pending.clear();
+    };
     auto traced = [&](StreamLaunch q, cudaStream_t st, auto&& fn) -> cudaError_t {
       if (!trace_path || !*trace_path) return fn(q, st);
-      unsigned long long* d = nullptr;
       const size_t bytes = sizeof(unsigned long long) * 4 * std::max<uint32_t>(q.n_units, 1);
-      cudaError_t e2 = cudaMalloc(&d, bytes);
-      if (e2 != cudaSuccess) return e2;
+      // buffers cached per (mode, size): no allocation between the launches
+      static std::vector<std::pair<size_t, unsigned long long*>> cache[3];
+      unsigned long long* d = nullptr;
+      for (auto& c : cache[q.mode & 1]) if (c.first == bytes) d = c.second;
+      cudaError_t e2 = cudaSuccess;
+      if (!d) {
+        e2 = cudaMalloc(&d, bytes);
+        if (e2 != cudaSuccess) return e2;
+        cache[q.mode & 1].push_back({bytes, d});
+      }
       cudaMemsetAsync(d, 0, bytes, st);
       q.trace = d;
       e2 = fn(q, st);
-      std::vector<unsigned long long> h(bytes / sizeof(unsigned long long));
-      cudaMemcpyAsync(h.data(), d, bytes, cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
-      cudaFree(d);
-      if (FILE* f = std::fopen(trace_path, "ab")) {
-        const unsigned long long hdr[4] = {0xC0FFEEull, q.n_units, q.n_long_units,
-                                           static_cast<unsigned long long>(q.mode)};
-        std::fwrite(hdr, sizeof(hdr), 1, f);
-        std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
-        std::fclose(f);
-      }
+      pending.push_back({d, bytes, {0xC0FFEEull, q.n_units, q.n_long_units,
+                                    static_cast<unsigned long long>(q.mode)}});
+      if (!trace_conc) flush_trace(st);
       return e2;
     };
     if (kind == 2) {
@@ -402,8 +450,20 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
       static const char* lk = std::getenv("GSPMM_LONG_KERNEL");
       static const bool long_tma = env_u32("GSPMM_LONG_TMA", 0) != 0;
       static const bool long_ws = !long_tma && !(lk && std::strcmp(lk, "ldg") == 0);
-      pl.long_ws = long_ws;
-      if (long_ws) {
+      // default: the LDGSTS CTAs; GSPMM_LONG_KERNEL=g4 selects the TMA
+      // gather4 CTAs, =ldg the register-staged ones (measured alternatives)
+      static const bool long_g4 = !long_tma && lk && std::strcmp(lk, "g4") == 0;
+      pl.long_ws = long_ws && !long_g4;
+      pl.long_g4 = long_g4;
+      static const int xl_sw = static_cast<int>(env_u32("GSPMM_XL_SW", long_g4 ? 128 : 64));
+      if (long_g4) {
+        // <= 256-column slices (the TMA box limit) of balanced width, boxes
+        // rounded up to 8 floats (four rows of a box are 128-byte aligned)
+        const int ns = (W + 255) / 256;
+        pl.long_sw = ((W + ns - 1) / ns + 7) & ~7;
+        pl.g4_box = pl.long_sw;
+        pl.g4_box_xl = (xl_sw + 7) & ~7;
+      } else if (long_ws) {
         // <= 512-column slices of balanced width (16-byte multiples)
         const int ns = (W + 511) / 512;
         pl.long_sw = ((W + ns - 1) / ns + 3) & ~3;
@@ -412,10 +472,9 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
       }
       pl.long_slices = static_cast<uint32_t>((W + pl.long_sw - 1) / pl.long_sw);
       pl.long_tma = long_tma;
-      pl.n_xl = long_tma || W <= 32 ? 0 : lv.num_xl;
-      static const int xl_sw = static_cast<int>(env_u32("GSPMM_XL_SW", 64));
-      pl.xl_sw = xl_sw;
-      pl.xl_slices = static_cast<uint32_t>((W + xl_sw - 1) / xl_sw);
+      pl.xl_sw = long_g4 ? pl.g4_box_xl : xl_sw;
+      pl.n_xl = long_tma || W <= 32 || pl.xl_sw >= pl.long_sw ? 0 : lv.num_xl;
+      pl.xl_slices = static_cast<uint32_t>((W + pl.xl_sw - 1) / pl.xl_sw);
       pl.n_xl_units = pl.n_xl * pl.xl_slices;
       pl.n_long_units = pl.n_xl_units + (pl.n_long - pl.n_xl) * pl.long_slices;
       pl.n_units = pl.n_long_units;
@@ -452,6 +511,7 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
         cudaError_t ej = cudaStreamWaitEvent(s, g->ev_join, 0);
         if (err == cudaSuccess) err = ej;
       }
+      if (!pending.empty()) flush_trace(s);
     }
   } else {
     err = launch_rows(b.L, s);

@@ -798,6 +798,282 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_long_ws(const StreamLaunch p)
   }
 }
 
+// ------------------------------------------ LONG ROWS, TMA tile::gather4
+// One column slice (<= 256 floats, the TMA box width) of one long row per
+// unit.  Warp 0 is the producer: each lane turns four staged neighbour ids
+// into one `cp.async.bulk.tensor.2d...tile::gather4` that lands four rows of
+// the slice in a shared-memory ring stage (completion by transaction bytes
+// on the stage's `full` mbarrier); warps 1-4 are the column owners that fold
+// each stage in canonical edge order and release it on `empty`.  No register
+// or L1 line holds a row in flight: the whole ~190 KB ring is the in-flight
+// window, and the load-store units stay free for the co-resident segment
+// warps.  Ids (and the small per-edge operand) arrive by cp.async NB stages
+// ahead, so issuing never waits on a global load.
+// Measured on B200 (scripts/mb_gather4.cu): one CTA streams ~73 rows/us of
+// 1 KB (74 GB/s, the per-SM share of the L2 limit) against ~41 for the
+// LDGSTS CTA above; the rate is bound by ~25 gather4 per us per SM, so the
+// slice should be as wide as the row allows.
+#ifndef G4_NB
+#define G4_NB 4
+#endif
+#ifndef G4_DF
+#define G4_DF 12288
+#endif
+constexpr int kG4Consumers = 4;
+constexpr int kG4Threads = 32 * (1 + kG4Consumers);
+struct G4Geom {
+  static constexpr int NB = G4_NB;
+  static constexpr int DF = G4_DF;  // data floats per stage
+  static constexpr int MR = 256;    // max edges per stage
+  static constexpr int SF = 512;    // small-operand floats per stage
+  static constexpr size_t smem_bytes() {
+    return sizeof(float) * (static_cast<size_t>(NB) * (DF + SF) + 4ull * NB * MR) +
+           2ull * NB * sizeof(uint64_t);
+  }
+};
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, int col, int r0,
+                                            int r1, int r2, int r3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int BOP, int ROP, bool ARG, int SK>
+__global__ void __launch_bounds__(kG4Threads, 1)
+    k_long_g4(const __grid_constant__ StreamLaunch p, const __grid_constant__ CUtensorMap tm_long,
+              const __grid_constant__ CUtensorMap tm_xl) {
+  using G = G4Geom;
+  constexpr int NB = G::NB;
+  constexpr bool SMALL = SK != SK_NONE;
+  extern __shared__ __align__(128) float sm[];
+  __shared__ uint32_t s_unit;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const RowLaunch& L = p.row;
+  const int rw = SMALL ? p.rhs_width : 0;
+  const bool need_eid = L.lhs.role == ROLE_EID || (rw && L.rhs.role == ROLE_EID);
+  float* sdata = sm;                                                              // NB x DF
+  float* ssmall = sm + static_cast<size_t>(NB) * G::DF;                           // NB x SF
+  uint32_t* sid = reinterpret_cast<uint32_t*>(ssmall + static_cast<size_t>(NB) * G::SF);  // 2NB x MR
+  uint32_t* seid = sid + 2 * NB * G::MR;                                          // 2NB x MR
+  uint64_t* full = reinterpret_cast<uint64_t*>(seid + 2 * NB * G::MR);
+  uint64_t* empty = full + NB;
+  if (tid == 0) {
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], kG4Consumers);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t gs0 = 0;  // stages run before the current unit (ring position)
+
+  for (;;) {
+    if (tid == 0) s_unit = atomicAdd(p.counter, 1u);
+    __syncthreads();
+    const uint32_t unit = s_unit;
+    __syncthreads();
+    if (unit >= p.n_units) break;
+    const unsigned long long t0 = p.trace ? globaltimer_ns() : 0ull;
+    uint32_t li, slc;
+    int sw, bw;
+    const bool xl = unit < p.n_xl_units;
+    if (xl) {
+      li = unit / p.xl_slices;
+      slc = unit - li * p.xl_slices;
+      sw = p.xl_sw;
+      bw = p.g4_box_xl;
+    } else {
+      const uint32_t v = unit - p.n_xl_units;
+      li = p.n_xl + v / p.long_slices;
+      slc = v - (li - p.n_xl) * p.long_slices;
+      sw = p.long_sw;
+      bw = p.g4_box;
+    }
+    const uint32_t r = __ldg(p.long_rows + li);
+    const int c0 = static_cast<int>(slc) * sw;
+    const int cw = min(sw, L.width - c0);
+    const int h0 = (SMALL && rw > 1) ? c0 / L.rhs.group : 0;
+    const int nh = SMALL ? ((rw > 1) ? (c0 + cw - 1) / L.rhs.group - h0 + 1 : 1) : 1;
+    uint32_t R = static_cast<uint32_t>(G::DF / bw);
+    if (R > static_cast<uint32_t>(G::MR)) R = G::MR;
+    if (SMALL && R * nh > static_cast<uint32_t>(G::SF)) R = G::SF / nh;
+    R &= ~3u;
+    const uint32_t e0 = __ldg(L.indptr + r), e1 = __ldg(L.indptr + r + 1);
+    const uint32_t n = e1 - e0;
+    const uint32_t rounds = (n + R - 1) / R;
+
+    if (warp == 0) {
+      const CUtensorMap* tm = xl ? &tm_xl : &tm_long;
+      const int32_t lrole = L.lhs.role;
+      auto fetch_ids = [&](uint32_t m) {  // ids of unit stage m -> id slot (gs0 + m) % 2NB
+        if (m < rounds) {
+          const uint32_t slot = (gs0 + m) % (2 * NB);
+          for (uint32_t t = static_cast<uint32_t>(lane); t < R; t += 32) {
+            const uint32_t j = e0 + m * R + t;
+            if (j < e1) {
+              cp_async_4(sid + slot * G::MR + t, L.indices + j);
+              if (need_eid) cp_async_4(seid + slot * G::MR + t, L.eids + j);
+            }
+          }
+        }
+        cp_async_commit();  // one group per stage, possibly empty
+      };
+      for (uint32_t m = 0; m < static_cast<uint32_t>(NB); ++m) fetch_ids(m);
+      constexpr bool small1 = SK == SK_WIN || SK == SK_SCALE;
+      const float* s1base = (SK == SK_SCALE) ? L.other_scale : L.rhs.base;
+      const int64_t s1ld = (SK == SK_SCALE) ? 1 : L.rhs.ld;
+      const int32_t s1role = (SK == SK_SCALE) ? static_cast<int32_t>(ROLE_OTHER) : L.rhs.role;
+      const uint32_t row_b = static_cast<uint32_t>(bw) * 4u;
+      for (uint32_t s = 0; s < rounds; ++s) {
+        const uint32_t gsi = gs0 + s;
+        const int b = static_cast<int>(gsi % NB);
+        if (gsi >= static_cast<uint32_t>(NB)) mbar_wait(&empty[b], ((gsi / NB) - 1) & 1u);
+        cp_async_wait_group<NB - 1>();  // ids of stage s landed (this lane's)
+        __syncwarp();                    // ... and every lane's
+        const uint32_t islot = gsi % (2 * NB);
+        const uint32_t* io = sid + islot * G::MR;
+        const uint32_t* ie = seid + islot * G::MR;
+        const uint32_t jr0 = s * R;
+        const uint32_t cnt = min(R, n - jr0);
+        const uint32_t ng = (cnt + 3) >> 2;
+        if (lane == 0) mbar_expect_tx(&full[b], ng * 4u * row_b);
+        __syncwarp();
+        const uint32_t sd = smem_u32(sdata + static_cast<size_t>(b) * G::DF);
+        for (uint32_t g = static_cast<uint32_t>(lane); g < ng; g += 32) {
+          int rr[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t q = min(4 * g + k, cnt - 1);  // a tail group repeats its last row
+            const uint32_t o = io[q];
+            if (lrole == ROLE_OTHER) {
+              rr[k] = static_cast<int>(o);
+            } else {
+              const uint32_t e = need_eid ? ie[q] : 0u;
+              rr[k] = static_cast<int>(operand_row(lrole, 0, o, e, e0 + jr0 + q));
+            }
+          }
+          tma_gather4(sd + 4 * g * row_b, tm, c0, rr[0], rr[1], rr[2], rr[3], &full[b]);
+        }
+        if constexpr (SMALL) {
+          float* bs = ssmall + static_cast<size_t>(b) * G::SF;
+          for (uint32_t q = static_cast<uint32_t>(lane); q < cnt; q += 32) {
+            const uint32_t j = e0 + jr0 + q;
+            const uint32_t o = io[q];
+            const uint32_t e = need_eid ? ie[q] : 0u;
+            if (small1) {
+              const uint32_t sr = s1role == ROLE_POS ? j : s1role == ROLE_EID ? e : o;
+              cp_async_4(bs + q, s1base + static_cast<int64_t>(sr) * s1ld);
+            } else {
+              const float* sp = L.rhs.base + operand_row(L.rhs.role, 0, o, e, j) * L.rhs.ld + h0;
+              for (int h = 0; h < nh; ++h) cp_async_4(bs + q * nh + h, sp + h);
+            }
+          }
+        }
+        fetch_ids(s + NB);
+        if constexpr (SMALL) cp_async_arrive(&full[b]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[b]);
+      }
+      cp_async_wait_group<0>();
+    } else {
+      const int ctid = tid - 32;  // 0 .. 127
+      auto run = [&](auto fw_tag) {
+        constexpr int FW = decltype(fw_tag)::value;
+        const int cc = ctid * FW;
+        const bool own = cc < cw;
+        const int hrel = (SMALL && rw > 1) ? (c0 + cc) / L.rhs.group - h0 : 0;
+        float acc[FW];
+        uint32_t arg[FW];
+#pragma unroll
+        for (int t = 0; t < FW; ++t) {
+          acc[t] = red_identity<ROP>();
+          arg[t] = 0xffffffffu;
+        }
+        for (uint32_t s = 0; s < rounds; ++s) {
+          const uint32_t gsi = gs0 + s;
+          const int b = static_cast<int>(gsi % NB);
+          mbar_wait(&full[b], (gsi / NB) & 1u);
+          if (own) {
+            const uint32_t cnt = min(R, n - s * R);
+            const float* col = sdata + static_cast<size_t>(b) * G::DF + cc;
+            const float* sv = ssmall + static_cast<size_t>(b) * G::SF + hrel;
+#pragma unroll 8
+            for (uint32_t e = 0; e < cnt; ++e) {
+              float x[FW];
+              if constexpr (FW == 2) {
+                const float2 v = *reinterpret_cast<const float2*>(col + static_cast<size_t>(e) * bw);
+                x[0] = v.x;
+                x[1] = v.y;
+              } else {
+                x[0] = col[static_cast<size_t>(e) * bw];
+              }
+              float sval = 0.0f;
+              if constexpr (SMALL) sval = sv[e * nh];
+#pragma unroll
+              for (int t = 0; t < FW; ++t) {
+                float m;
+                if constexpr (SK == SK_SCALE) m = __fmul_rn(bin_apply<BOP>(x[t], 0.0f), sval);
+                else if constexpr (SK == SK_NONE) m = bin_apply<BOP>(x[t], 0.0f);
+                else m = bin_apply<BOP>(x[t], sval);
+                if constexpr (ARG) {
+                  if (red_wins<ROP>(acc[t], m)) {
+                    acc[t] = m;
+                    arg[t] = e0 + s * R + e;
+                  }
+                } else {
+                  acc[t] = red_combine<ROP>(acc[t], m);
+                }
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[b]);
+        }
+        if (own) {
+#pragma unroll
+          for (int t = 0; t < FW; ++t) {
+            if (cc + t >= cw) break;
+            float a = acc[t];
+            if constexpr (ROP == R_MAX || ROP == R_MIN) {
+              if (n == 0) a = 0.0f;
+            }
+            if (L.mean) a = n ? __fdiv_rn(a, __uint2float_rn(n)) : 0.0f;
+            L.out[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t] = a;
+            if constexpr (ARG) {
+              const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + cc + t;
+              const bool none = arg[t] == 0xffffffffu;
+              if (L.arg_other)
+                L.arg_other[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.indices + arg[t]));
+              if (L.arg_edge)
+                L.arg_edge[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.eids + arg[t]));
+            }
+          }
+        }
+      };
+      if (cw > 128) run(std::integral_constant<int, 2>{});
+      else run(std::integral_constant<int, 1>{});
+      if (p.trace && ctid == 0) {
+        unsigned long long* t = p.trace + 4ull * unit;
+        t[0] = t0;
+        t[1] = globaltimer_ns();
+        t[2] = (static_cast<unsigned long long>(smid()) << 32) | 0xfffbu;
+        t[3] = n;
+      }
+    }
+    gs0 += rounds;
+    __syncthreads();  // next unit: the id ring's first slots are rewritten
+  }
+}
+
 // ------------------------------------------------------ LONG ROWS via TMA
 // Warp-specialised variant for slices of >= 512 B: warp 8 is the producer
 // (lane 0 issues one cp.async.bulk per edge into a shared-memory ring of
@@ -1002,7 +1278,6 @@ template <int VPL, int U, int BOP, int ROP, bool ARG, int SK, bool LO>
 __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : GATHER_MINB2) k_gather(const StreamLaunch p) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int warps = kThreads / 32;
   const RowLaunch& L = p.row;
   const bool need_eid = L.lhs.role == ROLE_EID ||
                         ((SK == SK_WIN || SK == SK_HEAD) && L.rhs.role == ROLE_EID);
@@ -1011,12 +1286,21 @@ __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : GATHER_MIN
   const int64_t sld = SK == SK_SCALE ? 1 : L.rhs.ld;
   const int32_t srole = SK == SK_SCALE ? static_cast<int32_t>(ROLE_OTHER) : L.rhs.role;
 
-  const uint32_t n_static = gridDim.x * warps;
-  uint32_t next_unit = blockIdx.x + gridDim.x * static_cast<uint32_t>(warp);
+  // Every unit, the first included, comes from the counter in arrival
+  // order: blocks that are not resident at launch -- the long-row CTAs hold
+  // part of the SMs -- must not own statically assigned early (heavy) units,
+  // and consecutive heavy units must not land on one SM (a block-wide grab
+  // of 8 units measured 10% slower on cfg4).  Measured against the static
+  // interleave: cfg2 forward 2.10 -> 1.81 ms, cfg4 7.9 -> 7.2 ms, cfg3 mean
+  // 5.60 -> 5.44 ms; cfg1 (uniform, no long rows) +5% from the 4.7k
+  // same-address atomics at launch.
+  uint32_t next_unit = 0;
+  if (lane == 0) next_unit = atomicAdd(p.counter, 1u);
+  next_unit = __shfl_sync(kFull, next_unit, 0);
   for (;;) {
     const uint32_t unit = next_unit;
     if (unit >= p.n_units) break;
-    if (lane == 0) next_unit = atomicAdd(p.counter, 1u) + n_static;
+    if (lane == 0) next_unit = atomicAdd(p.counter, 1u);
     next_unit = __shfl_sync(kFull, next_unit, 0);
     const unsigned long long t0 = p.trace ? globaltimer_ns() : 0ull;
 
@@ -1063,6 +1347,24 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
     if (grid > p.n_units) grid = p.n_units;
     k_long_tma<BOP, ROP, ARG, SMALL><<<grid, kLtThreads, lt_smem_bytes(), s>>>(p);
+  } else if (p.mode == 1 && p.long_g4) {
+    static int configured_g = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_g != dev) {
+      e = cudaFuncSetAttribute(k_long_g4<BOP, ROP, ARG, SK>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(G4Geom::smem_bytes()));
+      if (e != cudaSuccess) return e;
+      configured_g = dev;
+    }
+    CUtensorMap tl, tx;
+    if (!encode_rows_tmap(&tl, p.row.lhs, p.row.width, p.g4_box) ||
+        !encode_rows_tmap(&tx, p.row.lhs, p.row.width, p.n_xl_units ? p.g4_box_xl : p.g4_box))
+      return cudaErrorInvalidValue;
+    unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
+    if (grid > p.n_units) grid = p.n_units;
+    k_long_g4<BOP, ROP, ARG, SK><<<grid, kG4Threads, G4Geom::smem_bytes(), s>>>(p, tl, tx);
   } else if (p.mode == 1 && p.long_ws) {
     const bool small = SMALL;
     static int configured_w = -1;

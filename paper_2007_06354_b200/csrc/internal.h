@@ -30,6 +30,7 @@ struct OperandDesc {
   int32_t role = ROLE_OTHER;
   int32_t mode = MODE_FULL;
   int32_t group = 1;
+  int64_t rows = 0;  // entity rows (the gather4 tensor map's extent)
 };
 
 enum BinOp : int32_t { B_ADD = 0, B_SUB = 1, B_MUL = 2, B_DIV = 3, B_DOT = 4, B_COPY = 5 };

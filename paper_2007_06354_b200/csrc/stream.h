@@ -1,6 +1,8 @@
 // stream.h -- launch descriptor of the TMA-staged streaming row kernel.
 #pragma once
 
+#include <cuda.h>
+
 #include "internal.h"
 
 namespace gspmm_b200 {
@@ -27,6 +29,10 @@ struct StreamLaunch {
   uint32_t n_xl = 0, xl_slices = 1, n_xl_units = 0;
   int xl_sw = 32;
   bool long_tma = false;  // GSPMM_LONG_TMA=1: warp-specialised TMA long rows
+  // long rows through TMA tile::gather4 (k_long_g4, the default): box
+  // widths (floats, multiples of 8, >= the slice width) of the two tensor maps
+  bool long_g4 = false;
+  int g4_box = 0, g4_box_xl = 0;
   bool long_ws = true;  // long rows: k_long_ws (default) or k_long (GSPMM_LONG_KERNEL=ldg)
   // Units whose gathered slice is narrower than this many bytes stage rows
   // with per-lane 16-byte cp.async (LSU path) instead of one TMA bulk copy
@@ -41,5 +47,10 @@ struct StreamLaunch {
 // register-staged kernel (gather.cu).  Same descriptor, same results.
 cudaError_t launch_stream(const StreamLaunch& p, cudaStream_t s);
 cudaError_t launch_gather(const StreamLaunch& p, cudaStream_t s);
+
+// 2-D tensor map over the rows of a full-width operand (dims {width, rows},
+// row pitch ld), box {box, 1}: the source of the gather4 long-row kernel.
+// False if the driver rejects it.
+bool encode_rows_tmap(CUtensorMap* map, const OperandDesc& d, int width, int box);
 
 }  // namespace gspmm_b200
