@@ -241,7 +241,7 @@ constexpr int kEd4CW = 128;
 constexpr int kEd4Stride = kEd4CW + 4;
 constexpr int kEd4U = 8;
 
-__global__ void __launch_bounds__(kEd4Warps * 32) k_dot_edges4(const RowLaunch p,
+__global__ void __launch_bounds__(kEd4Warps * 32, 3) k_dot_edges4(const RowLaunch p,
                                                                const uint32_t* __restrict__ rowof,
                                                                uint64_t m) {
   extern __shared__ __align__(16) float tiles4[];
@@ -255,69 +255,109 @@ __global__ void __launch_bounds__(kEd4Warps * 32) k_dot_edges4(const RowLaunch p
   const uint32_t lldb = static_cast<uint32_t>(p.lhs.ld) * 4u, rldb = static_cast<uint32_t>(p.rhs.ld) * 4u;
   const char* lbase = reinterpret_cast<const char*>(p.lhs.base);
   const char* rbase = reinterpret_cast<const char*>(p.rhs.base);
+  // head boundaries on float4 groups: the fold runs whole head segments
+  // without a per-column boundary test (measured: the per-column test made
+  // the fold ~4 instructions per column and the kernel issue-bound)
+  const bool vfold = D % 4 == 0;
   for (uint64_t bt = static_cast<uint64_t>(blockIdx.x) * kEd4Warps + warp; bt < n_batches;
        bt += stride) {
     const uint64_t jb = bt * 32;
     const int n = static_cast<int>(m - jb < 32 ? m - jb : 32);
-    uint32_t my_o = 0, my_e = 0, my_r = 0;
+    // lane k resolves edge k's operand rows once per batch
+    uint32_t my_e = 0, my_l = 0, my_r = 0;
     if (lane < n) {
-      my_o = __ldg(p.indices + jb + lane);
-      my_e = __ldg(p.eids + jb + lane);
-      my_r = __ldg(rowof + jb + lane);
+      const uint32_t j = static_cast<uint32_t>(jb) + static_cast<uint32_t>(lane);
+      const uint32_t o = __ldg(p.indices + j);
+      my_e = __ldg(p.eids + j);
+      const uint32_t r = __ldg(rowof + j);
+      my_l = static_cast<uint32_t>(operand_row(lrole, r, o, my_e, j));
+      my_r = static_cast<uint32_t>(operand_row(rrole, r, o, my_e, j));
     }
     float acc = 0.0f;
     int head = 0, left = D;  // columns left in the current head
-    for (int cb = 0; cb < G; cb += kEd4CW) {
-      const int c0 = cb + lane * 4;
-      const bool cok = c0 < G;
-      const uint32_t coff = static_cast<uint32_t>(cok ? c0 : 0) * 4u;
-      for (int i0 = 0; i0 < n; i0 += kEd4U) {
-        float4 lv[kEd4U], rv[kEd4U];
+    // steps t = (chunk, sub-batch of kEd4U edges); the loads of step t+1 are
+    // issued before step t's products are parked (register ping-pong), so a
+    // warp keeps two steps in flight, also across a chunk's fold
+    const int nsub = (n + kEd4U - 1) / kEd4U;
+    const int S = ((G + kEd4CW - 1) / kEd4CW) * nsub;
+    auto load = [&](int t, float4(&lv)[kEd4U], float4(&rv)[kEd4U]) {
+      const int c = t / nsub, sub = t - c * nsub;
+      const int c0 = c * kEd4CW + lane * 4;
+      const uint32_t coff = static_cast<uint32_t>(c0 < G ? c0 : 0) * 4u;
 #pragma unroll
-        for (int k = 0; k < kEd4U; ++k) {
-          const int i = min(i0 + k, n - 1);  // a tail re-reads the last edge
-          const uint32_t o = __shfl_sync(kFull, my_o, i);
-          const uint32_t e = __shfl_sync(kFull, my_e, i);
-          const uint32_t r = __shfl_sync(kFull, my_r, i);
-          const uint32_t j = static_cast<uint32_t>(jb) + static_cast<uint32_t>(i);
-          const uint32_t lr = static_cast<uint32_t>(operand_row(lrole, r, o, e, j));
-          const uint32_t rr = static_cast<uint32_t>(operand_row(rrole, r, o, e, j));
-          lv[k] = __ldg(reinterpret_cast<const float4*>(lbase + static_cast<uint64_t>(lr) * lldb + coff));
-          rv[k] = __ldg(reinterpret_cast<const float4*>(rbase + static_cast<uint64_t>(rr) * rldb + coff));
-        }
+      for (int k = 0; k < kEd4U; ++k) {
+        const int i = min(sub * kEd4U + k, n - 1);  // a tail re-reads the last edge
+        const uint32_t lr = __shfl_sync(kFull, my_l, i);
+        const uint32_t rr = __shfl_sync(kFull, my_r, i);
+        lv[k] = __ldg(reinterpret_cast<const float4*>(lbase + static_cast<uint64_t>(lr) * lldb + coff));
+        rv[k] = __ldg(reinterpret_cast<const float4*>(rbase + static_cast<uint64_t>(rr) * rldb + coff));
+      }
+    };
+    auto park_fold = [&](int t, const float4(&lv)[kEd4U], const float4(&rv)[kEd4U]) {
+      const int c = t / nsub, sub = t - c * nsub;
 #pragma unroll
-        for (int k = 0; k < kEd4U; ++k) {
-          const int i = i0 + k;
-          if (i < n) {
-            float4 pr;
-            pr.x = __fmul_rn(lv[k].x, rv[k].x);
-            pr.y = __fmul_rn(lv[k].y, rv[k].y);
-            pr.z = __fmul_rn(lv[k].z, rv[k].z);
-            pr.w = __fmul_rn(lv[k].w, rv[k].w);
-            *reinterpret_cast<float4*>(tile + i * kEd4Stride + lane * 4) = pr;
-          }
+      for (int k = 0; k < kEd4U; ++k) {
+        const float4 lc = lv[k], rc = rv[k];
+        const int i = sub * kEd4U + k;
+        if (i < n) {
+          float4 pr;
+          pr.x = __fmul_rn(lc.x, rc.x);
+          pr.y = __fmul_rn(lc.y, rc.y);
+          pr.z = __fmul_rn(lc.z, rc.z);
+          pr.w = __fmul_rn(lc.w, rc.w);
+          *reinterpret_cast<float4*>(tile + i * kEd4Stride + lane * 4) = pr;
         }
       }
+      if (sub != nsub - 1) return;
       __syncwarp();
       if (lane < n) {
-        const int cend = min(kEd4CW, G - cb);  // a multiple of 4
+        const int cend = min(kEd4CW, G - c * kEd4CW);  // a multiple of 4
         const float* row = tile + lane * kEd4Stride;
-        for (int c = 0; c < cend; c += 4) {
-          const float4 v = *reinterpret_cast<const float4*>(row + c);
-          const float xs[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            acc = __fadd_rn(acc, xs[t]);
-            if (--left == 0) {
+        if (vfold) {
+          for (int cc = 0; cc < cend;) {
+            const int seg = min(cend - cc, left);  // columns to the head's end
+#pragma unroll 4
+            for (int q = 0; q < seg; q += 4) {
+              const float4 v = *reinterpret_cast<const float4*>(row + cc + q);
+              acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v.x), v.y), v.z), v.w);
+            }
+            cc += seg;
+            left -= seg;
+            if (left == 0) {
               p.out[static_cast<int64_t>(my_e) * p.out_ld + head] = acc;
               acc = 0.0f;
               ++head;
               left = D;
             }
           }
+        } else {
+          for (int cc = 0; cc < cend; cc += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(row + cc);
+            const float xs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              acc = __fadd_rn(acc, xs[u]);
+              if (--left == 0) {
+                p.out[static_cast<int64_t>(my_e) * p.out_ld + head] = acc;
+                acc = 0.0f;
+                ++head;
+                left = D;
+              }
+            }
+          }
         }
       }
       __syncwarp();
+    };
+    float4 al[kEd4U], ar[kEd4U], bl[kEd4U], br[kEd4U];
+    load(0, al, ar);
+    for (int t = 0; t < S; t += 2) {
+      if (t + 1 < S) load(t + 1, bl, br);
+      park_fold(t, al, ar);
+      if (t + 1 < S) {
+        if (t + 2 < S) load(t + 2, al, ar);
+        park_fold(t + 1, bl, br);
+      }
     }
   }
 }

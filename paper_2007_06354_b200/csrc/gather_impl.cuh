@@ -551,6 +551,12 @@ __global__ void __launch_bounds__(kLongThreads, 1) k_long(const StreamLaunch p) 
 #ifndef WS_P
 #define WS_P 12
 #endif
+// LONG_WS_MINB=2 caps the CTA at 64 registers so that two segment blocks
+// (instead of one) fit beside it: measured no faster (cfg3 mean 5.46 ->
+// 5.71 ms, cfg4 7.1 -> 7.1 ms), so the default stays 1
+#ifndef LONG_WS_MINB
+#define LONG_WS_MINB 1
+#endif
 constexpr int kWsProducers = WS_P, kWsConsumers = 4;
 constexpr int kWsThreads = 32 * (kWsProducers + kWsConsumers);
 struct WsGeom {
@@ -565,7 +571,7 @@ struct WsGeom {
 };
 
 template <int BOP, int ROP, bool ARG, int SK>
-__global__ void __launch_bounds__(kWsThreads, 1) k_long_ws(const StreamLaunch p) {
+__global__ void __launch_bounds__(kWsThreads, LONG_WS_MINB) k_long_ws(const StreamLaunch p) {
   using G = WsGeom;
   constexpr int NB = G::NB;
   constexpr bool SMALL = SK != SK_NONE;
