@@ -169,6 +169,20 @@ int gspmm_graph_permute_edges(gspmm_graph g, const float* src_by_id,
                               int64_t dim, int64_t src_ld, float* dst_by_pos,
                               int64_t dst_ld, void* stream);
 
+/* Source blocking (the paper's Alg. 3 / BlockPlan, block_plan.hpp:39-75 and
+ * run_blocked kernels.cpp:278-326, which the reference shows is byte-identical
+ * to Pull): an aggregation that gathers neighbour rows runs as nblocks passes,
+ * pass b folding only the neighbours in id block b into the partial rows left
+ * by pass b-1, so each pass's gathered rows fit the 126 MB L2.  Canonical
+ * rows are sorted by neighbour, so the passes replay every row's fold order:
+ * results stay bit-identical.  nblocks: 0 = automatic (default; blocks when
+ * the gathered operand is several times the L2 and the rows are dense
+ * enough to amortise the partial-row traffic), 1 = never, >= 2 = that many
+ * blocks whenever the call admits it (sum / mean / max / min without argmax,
+ * gathered lhs, no CSR-position edge operand).  Block CSRs are built on the
+ * device on first use. */
+int gspmm_graph_set_source_blocks(gspmm_graph g, int nblocks);
+
 /* ---- compute (device pointers, asynchronous on stream) ---- */
 int gspmm_binary_reduce(gspmm_graph g, const gspmm_config* cfg,
                         const gspmm_mat* u, const gspmm_mat* v,

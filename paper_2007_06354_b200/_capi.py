@@ -89,6 +89,7 @@ SIGNATURES = {
     "gspmm_graph_info": (_i32, [_vp, _P(_i32), _P(_u32), _P(_u32), _P(_u64), _P(_u32)]),
     "gspmm_graph_device_csr": (_i32, [_vp, _P(_vp), _P(_vp), _P(_vp)]),
     "gspmm_graph_permute_edges": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64, _vp]),
+    "gspmm_graph_set_source_blocks": (_i32, [_vp, _i32]),
     "gspmm_binary_reduce": (_i32, [_vp, _P(Config), _P(Mat), _P(Mat), _P(Mat), _P(Out), _vp]),
     "gspmm_binary_reduce_ex": (_i32, [_vp, _P(Config), _P(Mat), _P(Mat), _P(Mat), _P(Out),
                                       _P(Options), _vp]),
@@ -123,6 +124,8 @@ def _load():
             "there is no CPU fallback")
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
+        if os.environ.get("GSPMM_LIB_PATH") and not hasattr(lib, name):
+            continue  # an older library under A/B comparison (development aid)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

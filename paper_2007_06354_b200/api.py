@@ -138,6 +138,14 @@ class Graph:
             return self.num_cols if src_major else self.num_rows
         return self.num_edges
 
+    def set_source_blocks(self, nblocks):
+        """Source blocking (the paper's Alg. 3 / BlockPlan): 0 = automatic
+        (default), 1 = never, >= 2 = that many neighbour-id blocks, folded
+        pass by pass into the partial rows so each pass's gathered rows fit
+        in L2.  Results are bit-identical either way."""
+        check(A.LIB.gspmm_graph_set_source_blocks(self.handle, int(nblocks)), "set_source_blocks")
+        return self
+
     def permute_edges(self, e, stream=None):
         """Edge operand in edge-id order -> this handle's CSR position order
         (device, untimed setup like the reference's BlockPlan)."""

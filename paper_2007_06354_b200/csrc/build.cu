@@ -45,6 +45,58 @@ __global__ void k_rows_of(const uint32_t* __restrict__ indptr, uint32_t rows,
     for (uint32_t j = __ldg(indptr + r); j < __ldg(indptr + r + 1); ++j) rowof[j] = r;
 }
 
+// Source blocks (the paper's source blocking, block_plan.cpp:25-69): the
+// canonical row ranges are sorted by neighbour, so the edges of row r whose
+// neighbour lies in block b = [b*bs, (b+1)*bs) form one contiguous sub-range
+// [bpos[b][r], bpos[b+1][r]); concatenating the blocks in ascending order
+// replays every row's canonical order.
+__global__ void k_block_bounds(const uint32_t* __restrict__ indptr,
+                               const uint32_t* __restrict__ indices, uint32_t rows, uint32_t nb,
+                               uint32_t bs, uint32_t* __restrict__ bpos) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride) {
+    const uint32_t lo = __ldg(indptr + r), hi = __ldg(indptr + r + 1);
+    bpos[r] = lo;
+    uint32_t a = lo;
+    for (uint32_t b = 1; b < nb; ++b) {
+      const uint64_t key = static_cast<uint64_t>(b) * bs;
+      uint32_t l = a, h = hi;  // first position with indices[pos] >= key
+      while (l < h) {
+        const uint32_t mid = l + ((h - l) >> 1);
+        if (__ldg(indices + mid) < key) l = mid + 1;
+        else h = mid;
+      }
+      bpos[static_cast<uint64_t>(b) * rows + r] = l;
+      a = l;
+    }
+    bpos[static_cast<uint64_t>(nb) * rows + r] = hi;
+  }
+}
+
+__global__ void k_block_counts(const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi,
+                               uint32_t rows, uint32_t* __restrict__ counts) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r <= rows; r += stride)
+    counts[r] = r < rows ? __ldg(hi + r) - __ldg(lo + r) : 0u;
+}
+
+// warp per row: copy the row's block sub-range to the block CSR
+__global__ void k_block_copy(const uint32_t* __restrict__ lo, const uint32_t* __restrict__ indptr_b,
+                             uint32_t rows, const uint32_t* __restrict__ indices,
+                             const uint32_t* __restrict__ eids, uint32_t* __restrict__ idx_b,
+                             uint32_t* __restrict__ eid_b) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const uint32_t src = __ldg(lo + r), dst = __ldg(indptr_b + r);
+    const uint32_t n = __ldg(indptr_b + r + 1) - dst;
+    for (uint32_t k = lane; k < n; k += 32) {
+      idx_b[dst + k] = __ldg(indices + src + k);
+      eid_b[dst + k] = __ldg(eids + src + k);
+    }
+  }
+}
+
 int bits_for(uint32_t n) {
   int b = 1;
   while (b < 32 && (1ull << b) < n) ++b;
@@ -121,6 +173,36 @@ cudaError_t launch_transpose_csr(uint32_t num_rows, uint32_t num_cols, uint64_t 
   }
   e = sort_build(num_cols, num_rows, m, indices, rowof, eids, t_indptr, t_indices, t_eids, s);
   cudaFreeAsync(rowof, s);
+  return e;
+}
+
+cudaError_t launch_block_bounds(const uint32_t* indptr, const uint32_t* indices, uint32_t rows,
+                                uint32_t nb, uint32_t bs, uint32_t* bpos, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  k_block_bounds<<<148 * 8, 256, 0, s>>>(indptr, indices, rows, nb, bs, bpos);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_csr(const uint32_t* lo, const uint32_t* hi, uint32_t rows,
+                             const uint32_t* indices, const uint32_t* eids, uint32_t* indptr_b,
+                             uint32_t* idx_b, uint32_t* eid_b, cudaStream_t s) {
+  cudaError_t e;
+  uint32_t* counts = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  if ((e = cudaMallocAsync(&counts, sizeof(uint32_t) * (rows + 1ull), s))) return e;
+  k_block_counts<<<148 * 8, 256, 0, s>>>(lo, hi, rows, counts);
+  note_launch();
+  if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, indptr_b, rows + 1, s))) goto out;
+  if ((e = cudaMallocAsync(&tmp, tb, s))) goto out;
+  if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, counts, indptr_b, rows + 1, s))) goto out;
+  k_block_copy<<<148 * 8, 256, 0, s>>>(lo, indptr_b, rows, indices, eids, idx_b, eid_b);
+  note_launch();
+  e = cudaGetLastError();
+out:
+  if (tmp) cudaFreeAsync(tmp, s);
+  cudaFreeAsync(counts, s);
   return e;
 }
 

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -98,6 +99,11 @@ struct gspmm_graph_s {
   std::mutex mu;  // guards the host-call workspace
   void* ws = nullptr;
   size_t ws_bytes = 0;
+  // source blocks (gspmm_graph_set_source_blocks): sub-graphs over neighbour
+  // id ranges, built on first use for block_nb blocks
+  int blocks_pref = 0;  // 0 auto, 1 never, >= 2 forced
+  uint32_t block_nb = 0;
+  std::vector<gspmm_graph_s*> blocks;
 };
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no
@@ -339,11 +345,100 @@ int plan_kernel(const RowLaunch& L, int* rhs_width) {
   return k;
 }
 
+int launch(gspmm_graph_s* g, Bound& b, void* stream);
+void destroy_graph(gspmm_graph_s* g);
+
+// Number of source blocks for this call: 1 = a single pass.
+uint32_t source_blocks_for(const gspmm_graph_s* g, const RowLaunch& L) {
+  if (g->blocks_pref == 1 || L.acc_in || L.epi) return 1;
+  int rw = 0;
+  if (plan_kernel(L, &rw) == 0) return 1;
+  if (L.lhs.role != ROLE_OTHER || L.arg_other || L.arg_edge) return 1;
+  if (L.reduce != R_SUM && L.reduce != R_MAX && L.reduce != R_MIN) return 1;
+  if (L.rhs.base && L.rhs.role == ROLE_POS) return 1;
+  if (g->blocks_pref >= 2) return std::min<uint32_t>(g->blocks_pref, 64);
+  // automatic: blocks of <= GSPMM_SRC_BLOCK_MB of gathered rows (default
+  // 48 MB, a share of the 126 MB L2) when the gathered operand exceeds 1.5x
+  // the L2 and each row has >= 8 edges per block (the partial-row read +
+  // write per pass is then small against the row's gathers).  Measured on
+  // cfg5 (232,965 x 602 fp32 = 561 MB, 495 edges per row): 12 blocks,
+  // 35.4 -> 18.2 ms; 32 / 64 / 96 / 160 MB blocks: 19.2 / 18.9 / 22.7 / 32.8 ms
+  const double bytes = static_cast<double>(g->num_cols) * L.width * 4.0;
+  static const double target = env_u32("GSPMM_SRC_BLOCK_MB", 48) * 1048576.0;
+  if (bytes < 1.5 * 126.0 * 1048576.0) return 1;
+  const uint32_t nb = static_cast<uint32_t>(std::ceil(bytes / target));
+  const double avg = g->num_rows ? static_cast<double>(g->m) / g->num_rows : 0.0;
+  if (nb < 2 || avg < 8.0 * nb) return 1;
+  return std::min<uint32_t>(nb, 64);
+}
+
+int build_source_blocks(gspmm_graph_s* g, uint32_t nb) {
+  if (g->block_nb == nb) return GSPMM_OK;
+  for (auto* sg : g->blocks) destroy_graph(sg);
+  g->blocks.clear();
+  g->block_nb = 0;
+  const uint32_t rows = g->num_rows;
+  const uint32_t bs = (g->num_cols + nb - 1) / nb;
+  uint32_t *bpos = nullptr, *ip = nullptr, *ix = nullptr, *ie = nullptr;
+  auto done = [&](int st) {
+    cudaFree(bpos);
+    cudaFree(ip);
+    cudaFree(ix);
+    cudaFree(ie);
+    return st;
+  };
+  CUDA_TRY(cudaMalloc(&bpos, sizeof(uint32_t) * (nb + 1ull) * rows), "block bounds");
+  CUDA_TRY(launch_block_bounds(g->d_indptr, g->d_indices, rows, nb, bs, bpos, nullptr),
+           "block bounds");
+  if (cudaMalloc(&ip, sizeof(uint32_t) * (rows + 1ull)) != cudaSuccess ||
+      cudaMalloc(&ix, sizeof(uint32_t) * std::max<uint64_t>(g->m, 1)) != cudaSuccess ||
+      cudaMalloc(&ie, sizeof(uint32_t) * std::max<uint64_t>(g->m, 1)) != cudaSuccess)
+    return done(cuda_fail(cudaErrorMemoryAllocation, "block CSR"));
+  for (uint32_t b = 0; b < nb; ++b) {
+    const cudaError_t e = launch_block_csr(bpos + static_cast<uint64_t>(b) * rows,
+                                           bpos + static_cast<uint64_t>(b + 1) * rows, rows,
+                                           g->d_indices, g->d_eids, ip, ix, ie, nullptr);
+    if (e != cudaSuccess) return done(cuda_fail(e, "block CSR"));
+    gspmm_graph sg = nullptr;
+    const int st = gspmm_graph_create_device(g->device, g->orientation, rows, g->num_cols, ip,
+                                             ix, ie, &sg);
+    if (st) return done(st);
+    sg->blocks_pref = 1;
+    g->blocks.push_back(sg);
+  }
+  g->block_nb = nb;
+  return done(GSPMM_OK);
+}
+
+// Source-blocked passes: pass b folds block b's neighbours into the partial
+// rows of passes < b (bit-identical: the canonical rows are neighbour-sorted).
+int launch_blocked(gspmm_graph_s* g, Bound& b, void* stream, uint32_t nb) {
+  int st = build_source_blocks(g, nb);
+  if (st) return st;
+  for (uint32_t k = 0; k < nb; ++k) {
+    gspmm_graph_s* sg = g->blocks[k];
+    Bound bb = b;
+    bb.L.indptr = sg->d_indptr;
+    bb.L.indices = sg->d_indices;
+    bb.L.eids = sg->d_eids;
+    bb.L.acc_in = k ? b.L.out : nullptr;
+    bb.L.epi = k + 1 == nb ? 2 : 1;
+    bb.L.deg_indptr = k + 1 == nb ? g->d_indptr : nullptr;
+    st = launch(sg, bb, stream);
+    if (st) return st;
+  }
+  return GSPMM_OK;
+}
+
 int launch(gspmm_graph_s* g, Bound& b, void* stream) {
   cudaError_t err;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int rw = 0;
   int kind = 0;
+  if (!b.L.out_edge && b.L.binop != GSPMM_DOT) {
+    const uint32_t nb = source_blocks_for(g, b.L);
+    if (nb > 1) return launch_blocked(g, b, stream, nb);
+  }
   if (b.L.binop == GSPMM_DOT && b.L.out_edge &&
       (b.L.lhs.mode != MODE_FULL || (b.L.lhs.ld % 2 == 0 && aligned(b.L.lhs.base, 8))) &&
       (b.L.rhs.mode != MODE_FULL || (b.L.rhs.ld % 2 == 0 && aligned(b.L.rhs.base, 8)))) {
@@ -794,7 +889,23 @@ int gspmm_transpose_device(uint32_t num_rows, uint32_t num_cols, int64_t m,
 
 int gspmm_graph_destroy(gspmm_graph g) {
   if (!g) return GSPMM_OK;
+  destroy_graph(g);
+  return GSPMM_OK;
+}
+
+int gspmm_graph_set_source_blocks(gspmm_graph g, int nblocks) {
+  if (!g) return fail(GSPMM_ERR_ARG, "null graph handle");
+  if (nblocks < 0) return fail(GSPMM_ERR_ARG, "nblocks must be >= 0");
+  g->blocks_pref = nblocks;
+  return GSPMM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+void destroy_graph(gspmm_graph_s* g) {
   cudaSetDevice(g->device);
+  for (auto* sg : g->blocks) destroy_graph(sg);
   cudaFree(g->d_indptr);
   cudaFree(g->d_indices);
   cudaFree(g->d_eids);
@@ -811,8 +922,10 @@ int gspmm_graph_destroy(gspmm_graph g) {
   }
   cudaFree(g->ws);
   delete g;
-  return GSPMM_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int gspmm_graph_info(gspmm_graph g, int* orientation, uint32_t* num_rows,
                      uint32_t* num_cols, uint64_t* num_edges,

@@ -85,7 +85,10 @@ struct RowCursor {
   }
 };
 
-template <int VPL, int ROP, bool ARG>
+// PART: the kernel instance serves source-blocked passes (acc_in / epi /
+// deg_indptr honoured); the plain instances compile those paths out
+// (measured: the runtime checks cost up to 8% on cfg3 max + argmax).
+template <int VPL, int ROP, bool ARG, bool PART>
 struct Acc {
   float a[VPL][4];
   uint32_t arg[VPL][4];
@@ -111,18 +114,41 @@ struct Acc {
       }
     }
   }
+  // Start of owner row r: the identity, or (source-blocked passes after the
+  // first) the partial fold of the earlier passes.
+  __device__ __forceinline__ void begin(const RowLaunch& L, uint32_t r, int c0, int cw, int lane) {
+    reset();
+    if (!PART || L.acc_in == nullptr) return;
+    const float* prow = L.acc_in + static_cast<int64_t>(r) * L.out_ld + c0;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const int c = lane * 4 + v * 128;
+      if (c + 4 <= cw) {
+        const float4 q = *reinterpret_cast<const float4*>(prow + c);
+        a[v][0] = q.x;
+        a[v][1] = q.y;
+        a[v][2] = q.z;
+        a[v][3] = q.w;
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (c + t < cw) a[v][t] = prow[c + t];
+      }
+    }
+  }
   // Epilogue of owner row r over columns [c0 + c, ...) of this lane.
   __device__ __forceinline__ void store(const RowLaunch& L, uint32_t r, uint32_t deg, int c0,
                                         int cw, int v, int c) {
     if (c >= cw) return;
     float o[4];
+    const bool fix = !PART || L.epi != 1;  // a partial pass stores the raw fold
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       float x = a[v][t];
       if constexpr (ROP == R_MAX || ROP == R_MIN) {
-        if (deg == 0) x = 0.0f;
+        if (fix && deg == 0) x = 0.0f;
       }
-      if (L.mean) x = deg ? __fdiv_rn(x, __uint2float_rn(deg)) : 0.0f;
+      if (fix && L.mean) x = deg ? __fdiv_rn(x, __uint2float_rn(deg)) : 0.0f;
       o[t] = x;
     }
     float* orow = L.out + static_cast<int64_t>(r) * L.out_ld + c0;
@@ -170,7 +196,7 @@ __device__ __forceinline__ float small_value(const RowLaunch& L, int rw, uint32_
 // kept the SMs ~70% issue-busy at 2.5 TB/s of DRAM traffic.
 enum SmallKind : int { SK_NONE = 0, SK_WIN = 1, SK_SCALE = 2, SK_HEAD = 3 };
 
-template <int VPL, int U, int BOP, int ROP, bool ARG, int SK, bool LO>
+template <int VPL, int U, int BOP, int ROP, bool ARG, int SK, bool LO, bool PART>
 __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, bool need_eid,
                                           const float* sbase, int64_t sld, int32_t srole,
                                           int lane) {
@@ -195,8 +221,8 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
 
   RowCursor rc;
   rc.init(L.indptr, u.r0, u.r1, u.e0, lane);
-  Acc<VPL, ROP, ARG> acc;
-  acc.reset();
+  Acc<VPL, ROP, ARG, PART> acc;
+  acc.begin(L, rc.r, u.c0, u.cw, lane);
 
   // id windows: lane k <-> edge e0 + 32w + k; the next window is in flight
   uint32_t win_o = 0, win_e = 0, nxt_o = 0, nxt_e = 0;
@@ -218,10 +244,11 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
   const uint32_t n_batches = (u.e1 - u.e0 + U - 1) / U;
 
   auto flush = [&]() {
+    const uint32_t deg = PART && L.deg_indptr
+                             ? __ldg(L.deg_indptr + rc.r + 1) - __ldg(L.deg_indptr + rc.r)
+                             : rc.row_end - rc.row_start;
 #pragma unroll
-    for (int v = 0; v < VPL; ++v)
-      acc.store(L, rc.r, rc.row_end - rc.row_start, u.c0, u.cw, v, lane * 4 + v * 128);
-    acc.reset();
+    for (int v = 0; v < VPL; ++v) acc.store(L, rc.r, deg, u.c0, u.cw, v, lane * 4 + v * 128);
   };
 
   uint32_t j = u.e0;  // next edge to fold
@@ -286,6 +313,7 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
           while (j == rc.row_end) {
             flush();
             rc.advance(L.indptr, lane);
+            acc.begin(L, rc.r, u.c0, u.cw, lane);
           }
           fold_edge(k, j);
           ++j;
@@ -298,6 +326,7 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
     flush();
     if (rc.r + 1 < u.r1) {
       rc.advance(L.indptr, lane);
+      acc.begin(L, rc.r, u.c0, u.cw, lane);
     } else {
       ++rc.r;
     }
@@ -728,6 +757,8 @@ __global__ void __launch_bounds__(kWsThreads, LONG_WS_MINB) k_long_ws(const Stre
         for (int t = 0; t < FW; ++t) {
           acc[t] = red_identity<ROP>();
           arg[t] = 0xffffffffu;
+          if (L.acc_in && own && cc + t < cw)  // source-blocked pass: the partial
+            acc[t] = L.acc_in[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t];
         }
         for (uint32_t s = 0; s < rounds; ++s) {
           const uint32_t gsi = gs0 + s;
@@ -769,14 +800,16 @@ __global__ void __launch_bounds__(kWsThreads, LONG_WS_MINB) k_long_ws(const Stre
           if (lane == 0) mbar_arrive(&empty[b]);
         }
         if (own) {
+          const uint32_t deg = L.deg_indptr ? __ldg(L.deg_indptr + r + 1) - __ldg(L.deg_indptr + r) : n;
+          const bool fix = L.epi != 1;  // a partial pass stores the raw fold
 #pragma unroll
           for (int t = 0; t < FW; ++t) {
             if (cc + t >= cw) break;
             float a = acc[t];
             if constexpr (ROP == R_MAX || ROP == R_MIN) {
-              if (n == 0) a = 0.0f;
+              if (fix && deg == 0) a = 0.0f;
             }
-            if (L.mean) a = n ? __fdiv_rn(a, __uint2float_rn(n)) : 0.0f;
+            if (fix && L.mean) a = deg ? __fdiv_rn(a, __uint2float_rn(deg)) : 0.0f;
             L.out[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t] = a;
             if constexpr (ARG) {
               const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + cc + t;
@@ -1003,6 +1036,8 @@ __global__ void __launch_bounds__(kG4Threads, 1)
         for (int t = 0; t < FW; ++t) {
           acc[t] = red_identity<ROP>();
           arg[t] = 0xffffffffu;
+          if (L.acc_in && own && cc + t < cw)  // source-blocked pass: the partial
+            acc[t] = L.acc_in[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t];
         }
         for (uint32_t s = 0; s < rounds; ++s) {
           const uint32_t gsi = gs0 + s;
@@ -1045,14 +1080,16 @@ __global__ void __launch_bounds__(kG4Threads, 1)
           if (lane == 0) mbar_arrive(&empty[b]);
         }
         if (own) {
+          const uint32_t deg = L.deg_indptr ? __ldg(L.deg_indptr + r + 1) - __ldg(L.deg_indptr + r) : n;
+          const bool fix = L.epi != 1;  // a partial pass stores the raw fold
 #pragma unroll
           for (int t = 0; t < FW; ++t) {
             if (cc + t >= cw) break;
             float a = acc[t];
             if constexpr (ROP == R_MAX || ROP == R_MIN) {
-              if (n == 0) a = 0.0f;
+              if (fix && deg == 0) a = 0.0f;
             }
-            if (L.mean) a = n ? __fdiv_rn(a, __uint2float_rn(n)) : 0.0f;
+            if (fix && L.mean) a = deg ? __fdiv_rn(a, __uint2float_rn(deg)) : 0.0f;
             L.out[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t] = a;
             if constexpr (ARG) {
               const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + cc + t;
@@ -1280,7 +1317,7 @@ __global__ void __launch_bounds__(kLtThreads, 1) k_long_tma(const StreamLaunch p
 }
 
 // -------------------------------------------------------------- segments
-template <int VPL, int U, int BOP, int ROP, bool ARG, int SK, bool LO>
+template <int VPL, int U, int BOP, int ROP, bool ARG, int SK, bool LO, bool PART>
 __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : GATHER_MINB2) k_gather(const StreamLaunch p) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -1320,7 +1357,7 @@ __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : GATHER_MIN
     u.cw = min(p.seg_sw, L.width - u.c0);
     u.e0 = __ldg(L.indptr + u.r0);
     u.e1 = __ldg(L.indptr + u.r1);
-    wide_unit<VPL, U, BOP, ROP, ARG, SK, LO>(L, u, need_eid, sbase, sld, srole, lane);
+    wide_unit<VPL, U, BOP, ROP, ARG, SK, LO, PART>(L, u, need_eid, sbase, sld, srole, lane);
     if (p.trace && lane == 0) {
       unsigned long long* t = p.trace + 4ull * unit;
       t[0] = t0;
@@ -1410,11 +1447,19 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
-                                                    k_gather<VPL, U, BOP, ROP, ARG, SK, LO>,
+                                                    k_gather<VPL, U, BOP, ROP, ARG, SK, LO, false>,
                                                     kThreads, 0);
       if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
-    k_gather<VPL, U, BOP, ROP, ARG, SK, LO><<<sms * blocks_per_sm, kThreads, 0, s>>>(p);
+    const unsigned grid = static_cast<unsigned>(sms * blocks_per_sm);
+    if constexpr (!ARG) {  // argmax never runs source-blocked
+      if (p.row.acc_in || p.row.epi) {
+        k_gather<VPL, U, BOP, ROP, ARG, SK, LO, true><<<grid, kThreads, 0, s>>>(p);
+        note_launch();
+        return cudaGetLastError();
+      }
+    }
+    k_gather<VPL, U, BOP, ROP, ARG, SK, LO, false><<<grid, kThreads, 0, s>>>(p);
   }
   note_launch();
   return cudaGetLastError();

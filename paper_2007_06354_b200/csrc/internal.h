@@ -62,6 +62,14 @@ struct RowLaunch {
   uint32_t num_long = 0;
   uint32_t long_threshold = 0xffffffffu;
   int num_sms = 148;
+  // Source-blocked passes (the paper's source blocking, Alg. 3 /
+  // block_plan.cpp): rows start from the partial result in acc_in (== out)
+  // instead of the reduce identity; epi = 1 stores the raw fold (a partial
+  // for the next pass), epi = 2 is the last pass, whose mean / zero-degree
+  // fixup takes the degree from deg_indptr (the whole graph's row pointer).
+  const float* acc_in = nullptr;
+  const uint32_t* deg_indptr = nullptr;
+  int32_t epi = 0;
 };
 
 // Kernel launchers (rows.cu, dot.cu, aux.cu).  Return cudaGetLastError().
@@ -99,6 +107,16 @@ cudaError_t launch_transpose_csr(uint32_t num_rows, uint32_t num_cols, uint64_t 
                                  const uint32_t* indptr, const uint32_t* indices,
                                  const uint32_t* eids, uint32_t* t_indptr, uint32_t* t_indices,
                                  uint32_t* t_eids, cudaStream_t s);
+
+// Source blocks (build.cu): bpos[(nb + 1) x rows] = per-row sub-range
+// bounds of nb neighbour blocks of bs ids; then, per block, the block's CSR
+// (indptr_b[rows + 1], idx_b / eid_b) from the bounds lo = bpos[b], hi =
+// bpos[b + 1].
+cudaError_t launch_block_bounds(const uint32_t* indptr, const uint32_t* indices, uint32_t rows,
+                                uint32_t nb, uint32_t bs, uint32_t* bpos, cudaStream_t s);
+cudaError_t launch_block_csr(const uint32_t* lo, const uint32_t* hi, uint32_t rows,
+                             const uint32_t* indices, const uint32_t* eids, uint32_t* indptr_b,
+                             uint32_t* idx_b, uint32_t* eid_b, cudaStream_t s);
 
 // Launch counter (evidence of native execution), bumped by each launcher.
 void note_launch(uint64_t n = 1);

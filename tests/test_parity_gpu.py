@@ -447,3 +447,52 @@ def test_narrow_slices_of_heaviest_rows(xl, monkeypatch):
         v2, au2, _ = O.copy_max_argmax(g, x)
         assert O.bit_equal(val, v2) and (au == au2).all()
         g.__dict__.pop("_dev", None)
+
+
+@pytest.mark.parametrize("nb", [2, 3, 7])
+def test_source_blocks_bit_exact(nb, monkeypatch):
+    # Source blocking (the paper's Alg. 3): nb passes, each folding one
+    # neighbour-id block into the partial rows of the previous passes, must
+    # give the single-pass result bit for bit -- sums, mean, max / min with
+    # the zero-degree fixup, per-edge weights by edge id, the mean backward's
+    # per-neighbour scale, and long rows (the hub) on both kernels.
+    monkeypatch.setenv("GSPMM_LONG_EDGES", "300")
+    rng = np.random.default_rng(nb)
+    n = 3000
+    src = np.concatenate([rng.integers(0, n, 40000), rng.integers(0, n, 3000),
+                          np.full(2000, 7)]).astype(np.uint32)
+    dst = np.concatenate([rng.integers(0, n // 2, 40000), np.zeros(3000, np.int64),
+                          rng.integers(0, n, 2000)]).astype(np.uint32)
+    g = O.Graph(n, src, dst)  # rows >= n/2 get few in-edges: empty block ranges
+    x = O.normal_features(n, 200, nb)
+    w = O.gcn_weights(n, src, dst)
+    gy = O.normal_features(n, 200, nb + 3)
+    deg = O.in_degree(g)
+    inv = np.zeros(n, np.float32)
+    inv[deg > 0] = np.float32(1) / deg[deg > 0].astype(np.float32)
+    cases = [((O.U, O.E, O.MUL, O.SUM, O.V), dict(u=x, e=w), None),
+             ((O.V, O.E, O.MUL, O.SUM, O.U), dict(v=x, e=w), None),
+             ((O.U, O.NONE, O.COPY, O.MAX, O.V), dict(u=x), None),
+             ((O.U, O.NONE, O.COPY, O.MIN, O.V), dict(u=x), None),
+             ((O.U, O.NONE, O.COPY, P.MEAN, O.V), dict(u=x), O.mean(g, x)),
+             ((O.V, O.NONE, O.COPY, O.SUM, O.U), dict(v=gy), O.mean_backward(g, gy))]
+    for cfg, kw, want in cases:
+        orientation = O.SRC_MAJOR if cfg[4] == O.U else O.DST_MAJOR
+        h = dev_graph(g, orientation)
+        extra = {}
+        if want is not None and cfg[4] == O.U:
+            extra["other_scale"] = torch.from_numpy(inv).cuda()
+        h.set_source_blocks(1)
+        plain = P.binary_reduce(h, cfg, *(cuda(kw.get(k)) for k in ("u", "v", "e")), **extra)
+        torch.cuda.synchronize()
+        h.set_source_blocks(nb)
+        before = P.launch_count()
+        got = P.binary_reduce(h, cfg, *(cuda(kw.get(k)) for k in ("u", "v", "e")), **extra)
+        torch.cuda.synchronize()
+        assert P.launch_count() - before >= nb, "blocked passes did not run"
+        h.set_source_blocks(0)
+        if want is None:
+            want = O.binary_reduce(g, cfg, **kw)
+        got, plain = got.cpu().numpy(), plain.cpu().numpy()
+        assert O.bit_equal(plain, want), cfg
+        assert O.bit_equal(got, want), (nb, cfg)
