@@ -478,7 +478,19 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
     p.counter = g->d_counter;
     p.rhs_width = rw;
     const int W = b.L.width;
-    p.seg_sw = W <= 256 ? W : 256;
+    // one unit covers up to 640 columns for copy / scalar-weighted sums of
+    // gathered rows (gather_impl.cuh launch_wide), else <= 256-column slices
+    // (measured on cfg5, W = 602: 18.2 -> 16.0 ms)
+    static const bool wide_on = [] {
+      const char* v = std::getenv("GSPMM_WIDE_UNITS");
+      return !(v && std::strcmp(v, "0") == 0);
+    }();
+    // (W > 384: narrower rows would leave over 40% of the wide unit's
+    // lanes idle -- measured slower than two slices at W = 304)
+    const bool wide = wide_on && W > 384 && W <= 640 && b.L.reduce == R_SUM && !b.L.arg_other &&
+                      !b.L.arg_edge && b.L.lhs.role == ROLE_OTHER &&
+                      ((b.L.binop == B_COPY && !b.L.rhs.base) || (b.L.binop == B_MUL && rw == 1));
+    p.seg_sw = wide ? W : W <= 256 ? W : 256;
     p.seg_slices = static_cast<uint32_t>((W + p.seg_sw - 1) / p.seg_sw);
     static const uint32_t tma_min = env_u32("GSPMM_TMA_MIN_BYTES", 512);
     p.tma_min_bytes = tma_min;

@@ -49,6 +49,14 @@ constexpr int kThreads = 256;
 #endif
 #ifndef GATHER_MINB2
 #define GATHER_MINB2 4
+#endif
+// wide rows (VPL 5: up to 640 columns in one unit, e.g. cfg5's 602): copy /
+// scalar-weighted sums only
+#ifndef GATHER_U5
+#define GATHER_U5 2
+#endif
+#ifndef GATHER_MINB5
+#define GATHER_MINB5 2
 
 #endif
 
@@ -1318,7 +1326,7 @@ __global__ void __launch_bounds__(kLtThreads, 1) k_long_tma(const StreamLaunch p
 
 // -------------------------------------------------------------- segments
 template <int VPL, int U, int BOP, int ROP, bool ARG, int SK, bool LO, bool PART>
-__global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : GATHER_MINB2) k_gather(const StreamLaunch p) {
+__global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : VPL == 5 ? GATHER_MINB5 : GATHER_MINB2) k_gather(const StreamLaunch p) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const RowLaunch& L = p.row;
@@ -1443,7 +1451,7 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     if (grid > p.n_units) grid = p.n_units;
     k_long<VPL, BOP, ROP, ARG, SMALL><<<grid, kLongThreads, smem, s>>>(p);
   } else {
-    constexpr int U = VPL == 1 ? GATHER_U1 : GATHER_U2;
+    constexpr int U = VPL == 1 ? GATHER_U1 : VPL == 5 ? GATHER_U5 : GATHER_U2;
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
@@ -1504,9 +1512,25 @@ cudaError_t launch_red(const StreamLaunch& p, cudaStream_t s) {
   }
 }
 
+// Segment units wider than 256 columns (the host selects them for copy and
+// scalar-weighted sums of gathered rows, W <= 640): one pass over the edges
+// instead of ceil(W / 256) column slices.
+template <int BOP>
+cudaError_t launch_wide(const StreamLaunch& p, cudaStream_t s) {
+  if constexpr (BOP == B_COPY) {
+    if (p.row.other_scale) return launch_k<5, BOP, R_SUM, false, SK_SCALE, true>(p, s);
+    return launch_k<5, BOP, R_SUM, false, SK_NONE, true>(p, s);
+  } else if constexpr (BOP == B_MUL) {
+    return launch_k<5, BOP, R_SUM, false, SK_WIN, true>(p, s);
+  } else {
+    return cudaErrorNotSupported;
+  }
+}
+
 template <int BOP>
 cudaError_t launch_bop(const StreamLaunch& p, cudaStream_t s) {
   const int sw = p.mode == 1 ? p.long_sw : p.seg_sw;
+  if (p.mode == 0 && sw > 256) return launch_wide<BOP>(p, s);
   return sw > 128 ? launch_red<2, BOP>(p, s) : launch_red<1, BOP>(p, s);
 }
 
