@@ -91,8 +91,20 @@ struct FeatureMatrix {
   float at(std::int64_t i, std::int64_t j) const { return data[i * dim + j]; }
 };
 
-// Placeholder for the reference's Alg.-3 schedule; the device plan replaces it.
-struct BlockPlan {};
+// The reference's Alg.-3 schedule (block_plan.hpp:39-75) reduced to what the
+// device needs: kb source nodes per block -> num_blocks neighbour-id blocks.
+// Strategy::BlockedPull with a plan runs that many source-blocked passes
+// (gspmm_graph_set_source_blocks); the device builds the block CSRs itself.
+// nb (the output column panel) is accepted and ignored: the device slices
+// columns per unit.
+struct BlockPlan {
+  NodeId kb = 0;
+  std::int64_t nb = 0;
+  NodeId num_rows = 0, num_cols = 0;
+  NodeId num_blocks = 0;
+};
+// build_block_plan (block_plan.cpp:25-69): kb, nb >= 1.
+BlockPlan build_block_plan(const CsrGraph& g, NodeId kb, std::int64_t nb);
 
 void validate_config(const BrConfig& cfg);
 BrConfig named_config(std::string_view name);

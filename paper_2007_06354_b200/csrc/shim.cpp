@@ -151,6 +151,17 @@ std::string config_name(const BrConfig& cfg) {
   return s;
 }
 
+BlockPlan build_block_plan(const CsrGraph& g, NodeId kb, std::int64_t nb) {
+  if (kb < 1 || nb < 1) throw ConfigError("build_block_plan: kb and nb must be >= 1");
+  BlockPlan p;
+  p.kb = kb;
+  p.nb = nb;
+  p.num_rows = g.num_rows;
+  p.num_cols = g.num_cols;
+  p.num_blocks = g.num_cols ? (g.num_cols + kb - 1) / kb : 0;
+  return p;
+}
+
 Orientation required_orientation(Strategy s, Operand out) {
   const int o = gspmm_required_orientation(static_cast<int>(s), static_cast<int>(out));
   if (o < 0) throw ConfigError(gspmm_last_error());
@@ -177,6 +188,12 @@ FeatureMatrix binary_reduce(Strategy strategy, const CsrGraph& g, const BrConfig
     view_g = owner.get();
   }
   const gspmm_graph h = handle_for(*view_g);
+  // BlockedPull: the plan's neighbour-id blocks as source-blocked passes
+  // (bit-identical to Pull, like the reference's); otherwise automatic
+  const int blocks = strategy == Strategy::BlockedPull && plan->num_blocks >= 1
+                         ? static_cast<int>(plan->num_blocks)
+                         : 0;
+  throw_status(gspmm_graph_set_source_blocks(h, blocks));
   const gspmm_config c = to_c(cfg);
   gspmm_mat mu = view(u_feats), mv = view(v_feats), me = view(e_feats);
   int64_t rows = 0, dim = 0;

@@ -1,9 +1,10 @@
 """Summarise ncu --set full reports of the bench's kernels into profiles/
 (development tool, run in the container: ncu -i reads the .ncu-rep files).
 
-python scripts/ncu_summary.py <round-tag> <gather.ncu-rep> <long.ncu-rep>
-writes profiles/<tag>_ncu_full.txt and profiles/traffic.json (fwd pass =
-k_gather + k_long_ws, dram read + write bytes per launch)."""
+python scripts/ncu_summary.py <round-tag> fwd:<gather.ncu-rep> fwd:<long.ncu-rep> \
+    bwd:<gather.ncu-rep> bwd:<long.ncu-rep>
+writes profiles/<tag>_ncu_full.txt and profiles/traffic.json (per pass =
+k_gather + k_long_ws of that pass, dram read + write bytes per launch)."""
 import csv
 import io
 import json
@@ -30,14 +31,16 @@ def raw(rep):
 
 def main():
     tag, reps = sys.argv[1], sys.argv[2:]
-    lines = [f"# {tag} ncu --set full summaries (one launch each, bench.py cfg2 forward pass)"]
-    per_kernel = {}
-    for rep in reps:
+    lines = [f"# {tag} ncu --set full summaries (one launch each, bench.py cfg2 forward / "
+             f"backward pass)"]
+    per_pass = {"fwd": {}, "bwd": {}}
+    for spec in reps:
+        pas, rep = spec.split(":", 1) if ":" in spec else ("fwd", spec)
         for d in raw(rep):
             name = d["Kernel Name"][1]
             short = "k_long_ws" if "k_long_ws" in name else "k_long" if "k_long" in name else \
                 "k_gather" if "k_gather" in name else name[:30]
-            lines.append(f"## {short}")
+            lines.append(f"## {pas} {short}")
             lines.append(f"  Kernel Name = {name}")
             byt = 0.0
             for m in METRICS:
@@ -46,11 +49,12 @@ def main():
                     lines.append(f"  {m} = {val} {unit}")
                     if m.startswith("dram__bytes_"):
                         byt += float(val.replace(",", "")) * SCALE.get(unit, 1)
-            per_kernel[short] = byt
+            per_pass[pas][short] = byt
     open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full.txt"), "w").write("\n".join(lines) + "\n")
-    json.dump({"fwd": sum(per_kernel.values()), "bwd": None, "per_kernel": per_kernel,
+    json.dump({"fwd": sum(per_pass["fwd"].values()) or None,
+               "bwd": sum(per_pass["bwd"].values()) or None, "per_kernel": per_pass,
                "note": f"dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full, "
-                       f"cfg2 forward pass = {' + '.join(per_kernel)} ({tag})"},
+                       f"cfg2 pass = k_gather + k_long_ws of that pass ({tag})"},
               open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
     print("\n".join(lines))
 

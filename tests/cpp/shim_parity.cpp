@@ -142,7 +142,11 @@ int main() {
         const B::Strategy bs_ = static_cast<B::Strategy>(s);
         const B::Orientation need = B::required_orientation(bs_, to_b(cfg).out);
         const B::CsrGraph& g = need == B::Orientation::DstMajor ? bd : bs;
-        B::BlockPlan plan;
+        // BlockedPull: a 3-block plan, run as source-blocked device passes
+        const B::BlockPlan plan =
+            s == R::Strategy::BlockedPull
+                ? B::build_block_plan(g, g.num_cols > 3 ? (g.num_cols + 2) / 3 : 1, 8)
+                : B::BlockPlan{};
         const B::FeatureMatrix got = B::binary_reduce(bs_, g, B::named_config(name), &bu, &bv,
                                                       &be, &plan);
         CHECK(same_bits(got, want));
