@@ -96,7 +96,11 @@ struct RowCursor {
 // PART: the kernel instance serves source-blocked passes (acc_in / epi /
 // deg_indptr honoured); the plain instances compile those paths out
 // (measured: the runtime checks cost up to 8% on cfg3 max + argmax).
-template <int VPL, int ROP, bool ARG, bool PART>
+// ARG: 0 = no argmax; 1 = track the CSR position of the winner (the ids are
+// looked up at the row's flush); 2 = track the winning neighbour id itself
+// (gathered-row kernels with only arg_other requested: no lookup latency at
+// the flush, measured 0.6 ms of cfg3's 7.7).
+template <int VPL, int ROP, int ARG, bool PART>
 struct Acc {
   float a[VPL][4];
   uint32_t arg[VPL][4];
@@ -173,10 +177,14 @@ struct Acc {
       for (int t = 0; t < 4; ++t) {
         if (c + t >= cw) break;
         const bool none = arg[v][t] == 0xffffffffu;
-        if (L.arg_other)
-          L.arg_other[ab + t] = none ? -1 : static_cast<int32_t>(__ldg(L.indices + arg[v][t]));
-        if (L.arg_edge)
-          L.arg_edge[ab + t] = none ? -1 : static_cast<int32_t>(__ldg(L.eids + arg[v][t]));
+        if constexpr (ARG == 2) {
+          L.arg_other[ab + t] = none ? -1 : static_cast<int32_t>(arg[v][t]);
+        } else {
+          if (L.arg_other)
+            L.arg_other[ab + t] = none ? -1 : static_cast<int32_t>(__ldg(L.indices + arg[v][t]));
+          if (L.arg_edge)
+            L.arg_edge[ab + t] = none ? -1 : static_cast<int32_t>(__ldg(L.eids + arg[v][t]));
+        }
       }
     }
   }
@@ -204,7 +212,7 @@ __device__ __forceinline__ float small_value(const RowLaunch& L, int rw, uint32_
 // kept the SMs ~70% issue-busy at 2.5 TB/s of DRAM traffic.
 enum SmallKind : int { SK_NONE = 0, SK_WIN = 1, SK_SCALE = 2, SK_HEAD = 3 };
 
-template <int VPL, int U, int BOP, int ROP, bool ARG, int SK, bool LO, bool PART>
+template <int VPL, int U, int BOP, int ROP, int ARG, int SK, bool LO, bool PART>
 __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, bool need_eid,
                                           const float* sbase, int64_t sld, int32_t srole,
                                           int lane) {
@@ -271,6 +279,7 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
     const uint32_t n = min(static_cast<uint32_t>(U), u.e1 - jb);
     float4 x[U][VPL];
     float r[U][SK == SK_HEAD ? VPL : 1];
+    uint32_t okey[ARG == 2 ? U : 1];  // ARG 2: the neighbour id of each edge
     // loads: unconditional (a tail batch re-reads its last edge), so the
     // batch is straight-line code
 #pragma unroll
@@ -283,6 +292,7 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
         if (need_eid) e = __shfl_sync(kFull, win_e, sl);
       }
       if constexpr (SK == SK_WIN || SK == SK_SCALE) r[k][0] = __shfl_sync(kFull, win_r, sl);
+      if constexpr (ARG == 2) okey[k] = o;
       const uint32_t lr = LO ? o : static_cast<uint32_t>(operand_row(lrole, 0, o, e, jb + kk));
 #pragma unroll
       for (int v = 0; v < VPL; ++v)
@@ -306,7 +316,8 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
           else if constexpr (SK == SK_WIN) m[t] = bin_apply<BOP>(xs[t], r[k][0]);
           else m[t] = bin_apply<BOP>(xs[t], r[k][v]);
         }
-        acc.fold(v, m, jpos);
+        if constexpr (ARG == 2) acc.fold(v, m, okey[k]);
+        else acc.fold(v, m, jpos);
       }
     };
     if (n == static_cast<uint32_t>(U) && rc.row_end - j >= static_cast<uint32_t>(U)) {
@@ -1325,7 +1336,7 @@ __global__ void __launch_bounds__(kLtThreads, 1) k_long_tma(const StreamLaunch p
 }
 
 // -------------------------------------------------------------- segments
-template <int VPL, int U, int BOP, int ROP, bool ARG, int SK, bool LO, bool PART>
+template <int VPL, int U, int BOP, int ROP, int ARG, int SK, bool LO, bool PART>
 __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : VPL == 5 ? GATHER_MINB5 : GATHER_MINB2) k_gather(const StreamLaunch p) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -1377,8 +1388,9 @@ __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : VPL == 5 ?
 }
 
 // p.mode: 0 = row segments (k_gather), 1 = long rows (k_long)
-template <int VPL, int BOP, int ROP, bool ARG, int SK, bool LO>
+template <int VPL, int BOP, int ROP, int ARG, int SK, bool LO>
 cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
+  constexpr bool LARG = ARG != 0;  // the long-row kernels track positions
   constexpr bool SMALL = SK != SK_NONE;
   cudaError_t e = cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
@@ -1389,7 +1401,7 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured_t != dev) {
-      e = cudaFuncSetAttribute(k_long_tma<BOP, ROP, ARG, SMALL>,
+      e = cudaFuncSetAttribute(k_long_tma<BOP, ROP, LARG, SMALL>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(lt_smem_bytes()));
       if (e != cudaSuccess) return e;
@@ -1397,13 +1409,13 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     }
     unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
     if (grid > p.n_units) grid = p.n_units;
-    k_long_tma<BOP, ROP, ARG, SMALL><<<grid, kLtThreads, lt_smem_bytes(), s>>>(p);
+    k_long_tma<BOP, ROP, LARG, SMALL><<<grid, kLtThreads, lt_smem_bytes(), s>>>(p);
   } else if (p.mode == 1 && p.long_g4) {
     static int configured_g = -1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured_g != dev) {
-      e = cudaFuncSetAttribute(k_long_g4<BOP, ROP, ARG, SK>,
+      e = cudaFuncSetAttribute(k_long_g4<BOP, ROP, LARG, SK>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(G4Geom::smem_bytes()));
       if (e != cudaSuccess) return e;
@@ -1415,14 +1427,14 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
       return cudaErrorInvalidValue;
     unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
     if (grid > p.n_units) grid = p.n_units;
-    k_long_g4<BOP, ROP, ARG, SK><<<grid, kG4Threads, G4Geom::smem_bytes(), s>>>(p, tl, tx);
+    k_long_g4<BOP, ROP, LARG, SK><<<grid, kG4Threads, G4Geom::smem_bytes(), s>>>(p, tl, tx);
   } else if (p.mode == 1 && p.long_ws) {
     const bool small = SMALL;
     static int configured_w = -1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured_w != dev) {
-      e = cudaFuncSetAttribute(k_long_ws<BOP, ROP, ARG, SK>,
+      e = cudaFuncSetAttribute(k_long_ws<BOP, ROP, LARG, SK>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(WsGeom::smem_bytes(small)));
       if (e != cudaSuccess) return e;
@@ -1430,7 +1442,7 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     }
     unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
     if (grid > p.n_units) grid = p.n_units;
-    k_long_ws<BOP, ROP, ARG, SK><<<grid, kWsThreads, WsGeom::smem_bytes(small), s>>>(p);
+    k_long_ws<BOP, ROP, LARG, SK><<<grid, kWsThreads, WsGeom::smem_bytes(small), s>>>(p);
   } else if (p.mode == 1) {
     const int rws = SMALL ? (p.rhs_width > 0 ? p.rhs_width : 1) : 0;
     const size_t smem = LongGeom<VPL>::smem_bytes(rws);
@@ -1438,7 +1450,7 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured != dev) {
-      e = cudaFuncSetAttribute(k_long<VPL, BOP, ROP, ARG, SMALL>,
+      e = cudaFuncSetAttribute(k_long<VPL, BOP, ROP, LARG, SMALL>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(LongGeom<VPL>::smem_bytes(LongGeom<VPL>::kMaxSmall)));
       if (e != cudaSuccess) return e;
@@ -1449,7 +1461,7 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     // SMs and absorb these ones when they finish
     unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
     if (grid > p.n_units) grid = p.n_units;
-    k_long<VPL, BOP, ROP, ARG, SMALL><<<grid, kLongThreads, smem, s>>>(p);
+    k_long<VPL, BOP, ROP, LARG, SMALL><<<grid, kLongThreads, smem, s>>>(p);
   } else {
     constexpr int U = VPL == 1 ? GATHER_U1 : VPL == 5 ? GATHER_U5 : GATHER_U2;
     static int blocks_per_sm = 0;
@@ -1487,9 +1499,15 @@ cudaError_t launch_red(const StreamLaunch& p, cudaStream_t s) {
     constexpr bool A = decltype(argt)::value;
     constexpr int K = decltype(skt)::value;
     // copy_u / u_op_e with the gathered neighbour rows: the specialised
-    // instances; copy_e and other layouts: the generic-role instance
-    if (lo) return launch_k<VPL, BOP, R, A, K, true>(p, s);
-    return launch_k<VPL, BOP, R, A, K, false>(p, s);
+    // instances (argmax of the neighbour id alone: tracked directly);
+    // copy_e and other layouts: the generic-role instance
+    if (lo) {
+      if constexpr (A) {
+        if (!L.arg_edge) return launch_k<VPL, BOP, R, 2, K, true>(p, s);
+      }
+      return launch_k<VPL, BOP, R, A ? 1 : 0, K, true>(p, s);
+    }
+    return launch_k<VPL, BOP, R, A ? 1 : 0, K, false>(p, s);
   };
   auto by_sk = [&](auto rop, auto argt) -> cudaError_t {
     using std::integral_constant;
@@ -1518,10 +1536,10 @@ cudaError_t launch_red(const StreamLaunch& p, cudaStream_t s) {
 template <int BOP>
 cudaError_t launch_wide(const StreamLaunch& p, cudaStream_t s) {
   if constexpr (BOP == B_COPY) {
-    if (p.row.other_scale) return launch_k<5, BOP, R_SUM, false, SK_SCALE, true>(p, s);
-    return launch_k<5, BOP, R_SUM, false, SK_NONE, true>(p, s);
+    if (p.row.other_scale) return launch_k<5, BOP, R_SUM, 0, SK_SCALE, true>(p, s);
+    return launch_k<5, BOP, R_SUM, 0, SK_NONE, true>(p, s);
   } else if constexpr (BOP == B_MUL) {
-    return launch_k<5, BOP, R_SUM, false, SK_WIN, true>(p, s);
+    return launch_k<5, BOP, R_SUM, 0, SK_WIN, true>(p, s);
   } else {
     return cudaErrorNotSupported;
   }

@@ -67,6 +67,12 @@ CASES = {
     "cfg2dot": ("rmat", 1_000_000, 16_000_000, 256, True, False, "dot"),
     "cfg4dot": ("rmat", 1_000_000, 32_000_000, 512, False, False, "dotheads"),
     "cfg4softmax": ("rmat", 1_000_000, 32_000_000, 8, False, False, "softmax"),
+    # backward passes (src-major handle)
+    "cfg2bwd": ("rmat", 1_000_000, 16_000_000, 256, True, False, "gcnbwd"),
+    "cfg3meanbwd": ("rmat", 2_449_029, 61_859_140, 100, False, True, "meanbwd"),
+    "cfg3maxbwd": ("rmat", 2_449_029, 61_859_140, 100, False, True, "maxbwd"),
+    "cfg4bwdx": ("rmat", 1_000_000, 32_000_000, 512, False, False, "headsbwd"),
+    "cfg5meanbwd": ("powerlaw", 232_965, 0, 602, False, False, "meanbwd604"),
     "cfg4softmaxbwd": ("rmat", 1_000_000, 32_000_000, 8, False, False, "softmaxbwd"),
 }
 
@@ -125,11 +131,48 @@ def run(name):
             gl = torch.empty_like(a)
             fn = lambda: P.edge_softmax_backward(g, a, ga, out=gl, e_order=P.EDGE_BY_POS)
             eb = E * F * 4  # reads a and grad_a
+    elif op in ("gcnbwd", "meanbwd", "headsbwd", "meanbwd604"):
+        # grad_u = sum over out-edges (u -> v) of grad_out[v] (x a weight), on
+        # the transposed CSR
+        scsr = P.transpose(n, n, *dcsr)
+        gs = P.Graph(*scsr, orientation=P.SRC_MAJOR)
+        del g
+        cfg = (P.V, P.E, P.MUL, P.SUM, P.U)
+        if op == "gcnbwd":
+            w = torch.from_numpy(P.synth_gcn_weights(n, src, dst)).cuda()
+            wp = gs.permute_edges(w)
+            fn = lambda: P.binary_reduce(gs, cfg, v=x, e=wp, out=out, e_order=P.EDGE_BY_POS)
+            eb = E * 4
+        elif op == "headsbwd":
+            a = torch.rand(E, 8, device="cuda")
+            ap = gs.permute_edges(a)
+            fn = lambda: P.binary_reduce(gs, cfg, v=x, e=ap, out=out, e_order=P.EDGE_BY_POS,
+                                         heads=8)
+            eb = E * 32
+        else:
+            inv = torch.from_numpy(np.where(deg > 0, 1.0 / np.maximum(deg, 1), 0).astype(np.float32)).cuda()
+            cfgc = (P.V, P.NONE, P.COPY, P.SUM, P.U)
+            if op == "meanbwd":
+                fn = lambda: P.binary_reduce(gs, cfgc, v=x, out=out, other_scale=inv)
+            else:
+                xp = torch.zeros(n, 604, device="cuda")
+                xp[:, :F] = x
+                op_ = torch.empty(n, 604, device="cuda")
+                fn = lambda: P.binary_reduce(gs, cfgc, v=xp[:, :F], out=op_[:, :F], other_scale=inv)
+            eb = E * 4
+        g = gs
+    elif op == "maxbwd":
+        _, au, _ = P.binary_reduce(g, "u_copy_max_v", u=x, want_arg_other=True)
+        gy = torch.randn(n, F, device="cuda")
+        fn = lambda: P.argmax_backward(au, gy, n)
+        eb = 0
     else:
         fn = lambda: P.binary_reduce(g, "u_copy_add_v", u=x, out=out)
         eb = 0
     ms = time_pass(fn)
     byts = E * F * 4 + (n + 1) * 4 + E * 4 + eb + n * F * 4
+    if op == "maxbwd":  # read arg + grad_out, write grad (scatter): N x F each
+        byts = n * F * 4 * 3
     if op in ("softmax", "softmaxbwd"):  # read logits (a, grad_a) once, write once; indptr
         byts = E * F * 4 * 2 + eb + (n + 1) * 4
     gbs = byts / ms / 1e6

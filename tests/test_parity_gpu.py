@@ -317,6 +317,9 @@ def test_max_argmax_and_backward(seed):
     assert O.bit_equal(val, v2)
     assert O.bit_equal(val, O.binary_reduce(g, O.named_config("u_copy_max_v"), u=x))
     assert (au == au2).all() and (ae == ae2).all()
+    # neighbour argmax alone: the kernels track the winning id directly
+    val1, au1, _ = gpu_reduce(g, (O.U, O.NONE, O.COPY, O.MAX, O.V), u=x, want_arg_other=True)
+    assert O.bit_equal(val1, v2) and (au1 == au2).all()
     gy = O.normal_features(3000, 100, seed + 3)
     grad = P.argmax_backward(torch.from_numpy(au).cuda(), cuda(gy), 3000).cpu().numpy()
     want = O.argmax_backward(au2, gy, 3000)
