@@ -1044,12 +1044,21 @@ static int softmax_common(gspmm_graph g, bool backward, const gspmm_mat* l, cons
     return fail(GSPMM_ERR_ARG, "null data");
   CUDA_TRY(cudaSetDevice(g->device), "cudaSetDevice");
   const auto& lv = g->level[0];
+  if (lv.num_long && !g->side) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking), "side stream");
+    CUDA_TRY(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming), "event");
+    CUDA_TRY(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming), "event");
+  }
+  SideStream side;
+  side.stream = g->side;
+  side.fork = g->ev_fork;
+  side.join = g->ev_join;
   const cudaError_t e = launch_edge_softmax(
       backward, g->d_indptr, g->d_eids, g->num_rows, static_cast<int>(heads),
       l->edge_order == GSPMM_EDGE_BY_POS, l->data, l->ld ? l->ld : heads,
       backward ? ga->data : nullptr, backward ? (ga->ld ? ga->ld : heads) : 0, out->data,
       out->ld ? out->ld : heads, lv.d_long, lv.num_long, lv.threshold, g->num_sms,
-      static_cast<cudaStream_t>(stream));
+      static_cast<cudaStream_t>(stream), side);
   if (e != cudaSuccess) return cuda_fail(e, "edge_softmax");
   return GSPMM_OK;
 }

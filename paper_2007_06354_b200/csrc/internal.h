@@ -90,6 +90,13 @@ cudaError_t launch_argmax_backward(const int32_t* arg, int64_t rows,
                                    int64_t src_ld, double* acc,
                                    cudaStream_t s);
 
+// A handle's side stream and fork / join events (hub-row kernels run there,
+// concurrently with the warp-per-row kernels).  stream == nullptr: serial.
+struct SideStream {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
 // Fused edge softmax over in-edges (softmax.cu): forward (l -> out = a) or
 // backward (l = a, g = grad_a -> out = grad_l).  Rows above long_threshold
 // edges are listed in long_rows and run one CTA per row.
@@ -97,7 +104,8 @@ cudaError_t launch_edge_softmax(bool backward, const uint32_t* indptr, const uin
                                 uint32_t rows, int heads, bool by_pos, const float* l,
                                 int64_t l_ld, const float* g, int64_t g_ld, float* out,
                                 int64_t out_ld, const uint32_t* long_rows, uint32_t n_long,
-                                uint32_t long_threshold, int num_sms, cudaStream_t s);
+                                uint32_t long_threshold, int num_sms, cudaStream_t s,
+                                const SideStream& side = SideStream{});
 
 // Device-side canonical CSR build / transpose (build.cu).
 cudaError_t launch_build_csr(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,

@@ -182,15 +182,37 @@ __device__ __forceinline__ void store_heads(float* p, bool vec, const float (&v)
   for (int h = 0; h < H; ++h) p[h] = v[h];
 }
 
+// All-reduce of H per-lane values over the warp, every lane ending with all H
+// totals.  Recursive halving first (offsets 16, 8, ...: each step a lane
+// keeps half of its heads and folds in its partner's copy of them), so lane
+// L ends with the partial of head L >> log2(32 / H) over H lanes; then a
+// butterfly over the remaining lane bits, then one broadcast per head.
+// 2H + log2(32/H) - 1 shuffles instead of 5H (H = 8: 17 against 40; the
+// previous butterfly kept the rows kernel ~65% issue-busy).  Fixed order:
+// deterministic run to run.
 template <int H, bool MAX>
 __device__ __forceinline__ void lane_reduce(float (&v)[H]) {
+  const int lane = threadIdx.x & 31;
+  auto op = [](float a, float b) { return MAX ? max_ref(a, b) : __fadd_rn(a, b); };
+  constexpr int kLanesPerHead = 32 / H;
+  constexpr int kLog2H = H >= 16 ? 4 : H >= 8 ? 3 : H >= 4 ? 2 : H >= 2 ? 1 : 0;
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1)
+  for (int st = 0; st < kLog2H; ++st) {
+    const int half = H >> (st + 1), off = 16 >> st;
+    const bool up = (lane & off) != 0;
 #pragma unroll
-    for (int h = 0; h < H; ++h) {
-      const float o = __shfl_xor_sync(kFull, v[h], off);
-      v[h] = MAX ? max_ref(v[h], o) : __fadd_rn(v[h], o);
+    for (int i = 0; i < half; ++i) {
+      const float send = up ? v[i] : v[i + half];
+      const float keep = up ? v[i + half] : v[i];
+      v[i] = op(keep, __shfl_xor_sync(kFull, send, off));
     }
+  }
+#pragma unroll
+  for (int off = kLanesPerHead / 2; off >= 1; off >>= 1)
+    v[0] = op(v[0], __shfl_xor_sync(kFull, v[0], off));
+  const float mine = v[0];
+#pragma unroll
+  for (int h = 0; h < H; ++h) v[h] = __shfl_sync(kFull, mine, h * kLanesPerHead);
 }
 
 template <int H, bool MAX>
@@ -209,9 +231,10 @@ __device__ __forceinline__ void warps_reduce(float (&v)[H], int w, int nw, float
   }
 }
 
-template <int H, bool BWD>
-__device__ __forceinline__ void row_softmax_vec(const SoftmaxArgs& p, uint32_t r, int w, int nw,
+template <int H, bool BWD, int NW>
+__device__ __forceinline__ void row_softmax_vec(const SoftmaxArgs& p, uint32_t r, int w,
                                                 float* red, bool vec) {
+  constexpr int nw = NW;
   const int lane = threadIdx.x & 31;
   const uint32_t e0 = __ldg(p.indptr + r), e1 = __ldg(p.indptr + r + 1);
   const uint32_t n = e1 - e0;
@@ -222,10 +245,57 @@ __device__ __forceinline__ void row_softmax_vec(const SoftmaxArgs& p, uint32_t r
     const uint32_t j = e0 + k;
     return p.by_pos ? static_cast<int64_t>(j) : static_cast<int64_t>(__ldg(p.eids + j));
   };
+  if (NW == 1 && n <= step) {
+    // one step covers the row: every value is loaded once and kept in
+    // registers (exp computed once); same reductions, same results
+    const bool has = first < n;
+    const int64_t er = has ? erow(first) : 0;
+    if constexpr (!BWD) {
+      float x[H], m[H], z[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) x[h] = -__int_as_float(0x7f800000);
+      if (has) load_heads<H>(p.l + er * p.l_ld, vec, x);
+#pragma unroll
+      for (int h = 0; h < H; ++h) m[h] = max_ref(-__int_as_float(0x7f800000), x[h]);  // as the loop
+      lane_reduce<H, true>(m);
+      warps_reduce<H, true>(m, w, nw, red);
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        x[h] = has ? expf(__fsub_rn(x[h], m[h])) : 0.0f;
+        z[h] = __fadd_rn(0.0f, x[h]);  // as the loop
+      }
+      lane_reduce<H, false>(z);
+      warps_reduce<H, false>(z, w, nw, red);
+      if (has) {
+#pragma unroll
+        for (int h = 0; h < H; ++h) x[h] = __fdiv_rn(x[h], z[h]);
+        store_heads<H>(p.out + er * p.out_ld, vec, x);
+      }
+    } else {
+      float a[H], g[H], sacc[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) a[h] = g[h] = 0.0f;
+      if (has) {
+        load_heads<H>(p.l + er * p.l_ld, vec, a);
+        load_heads<H>(p.g + er * p.g_ld, vec, g);
+      }
+#pragma unroll
+      for (int h = 0; h < H; ++h) sacc[h] = __fadd_rn(0.0f, __fmul_rn(a[h], g[h]));  // as the loop
+      lane_reduce<H, false>(sacc);
+      warps_reduce<H, false>(sacc, w, nw, red);
+      if (has) {
+#pragma unroll
+        for (int h = 0; h < H; ++h) a[h] = __fmul_rn(a[h], __fsub_rn(g[h], sacc[h]));
+        store_heads<H>(p.out + er * p.out_ld, vec, a);
+      }
+    }
+    return;
+  }
   if constexpr (!BWD) {
     float m[H];
 #pragma unroll
     for (int h = 0; h < H; ++h) m[h] = -__int_as_float(0x7f800000);
+#pragma unroll 4
     for (uint32_t k = first; k < n; k += step) {
       float x[H];
       load_heads<H>(p.l + erow(k) * p.l_ld, vec, x);
@@ -237,6 +307,7 @@ __device__ __forceinline__ void row_softmax_vec(const SoftmaxArgs& p, uint32_t r
     float z[H];
 #pragma unroll
     for (int h = 0; h < H; ++h) z[h] = 0.0f;
+#pragma unroll 4
     for (uint32_t k = first; k < n; k += step) {
       float x[H];
       load_heads<H>(p.l + erow(k) * p.l_ld, vec, x);
@@ -286,7 +357,7 @@ __global__ void __launch_bounds__(kSmWarps * 32) k_softmax_vec_rows(const Softma
   for (uint32_t r = blockIdx.x * kSmWarps + warp; r < p.rows; r += stride) {
     const uint32_t deg = __ldg(p.indptr + r + 1) - __ldg(p.indptr + r);
     if (deg > p.long_threshold) continue;
-    row_softmax_vec<H, BWD>(p, r, 0, 1, nullptr, vec);
+    row_softmax_vec<H, BWD, 1>(p, r, 0, nullptr, vec);
   }
 }
 
@@ -299,36 +370,59 @@ __global__ void __launch_bounds__(kSmLongWarps * 32) k_softmax_vec_long(const So
   __shared__ float red[kSmLongWarps * 32];
   const int warp = threadIdx.x >> 5;
   for (uint32_t i = blockIdx.x; i < n_long; i += gridDim.x) {
-    row_softmax_vec<H, BWD>(p, __ldg(long_rows + i), warp, kSmLongWarps, red, vec);
+    row_softmax_vec<H, BWD, kSmLongWarps>(p, __ldg(long_rows + i), warp, red, vec);
     __syncthreads();
   }
 }
 
+// The hub rows (one CTA each) run on the side stream, concurrently with the
+// warp-per-row kernel (measured on cfg4: 1.15 + 0.92 ms back to back).
 template <int H, bool BWD>
 void launch_vec(const SoftmaxArgs& p, bool vec, const uint32_t* long_rows, uint32_t n_long,
-                int sms, cudaStream_t s) {
+                int sms, cudaStream_t s, const SideStream& side) {
+  const bool fork = n_long && side.stream;
+  if (fork) {
+    cudaEventRecord(side.fork, s);
+    cudaStreamWaitEvent(side.stream, side.fork, 0);
+  }
+  // persistent grids of exactly one wave (measured: the 8-blocks-per-SM grid
+  // ran in two waves at ~32% achieved occupancy)
+  static int occ_rows = 0, occ_long = 0;
+  if (!occ_rows) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_rows, k_softmax_vec_rows<H, BWD>,
+                                                  kSmWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_long, k_softmax_vec_long<H, BWD>,
+                                                  kSmLongWarps * 32, 0);
+    occ_rows = std::max(occ_rows, 1);
+    occ_long = std::max(occ_long, 1);
+  }
+  if (n_long) {
+    const unsigned grid = std::min<unsigned>(n_long, static_cast<unsigned>(sms * occ_long));
+    k_softmax_vec_long<H, BWD><<<grid, kSmLongWarps * 32, 0, fork ? side.stream : s>>>(
+        p, vec, long_rows, n_long);
+    note_launch();
+  }
   if (p.rows) {
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((p.rows + kSmWarps - 1) / kSmWarps,
-                                                                   static_cast<uint64_t>(sms) * 8));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
+        (p.rows + kSmWarps - 1) / kSmWarps, static_cast<uint64_t>(sms) * occ_rows));
     k_softmax_vec_rows<H, BWD><<<grid, kSmWarps * 32, 0, s>>>(p, vec);
     note_launch();
   }
-  if (n_long) {
-    const unsigned grid = std::min<unsigned>(n_long, static_cast<unsigned>(sms) * 2);
-    k_softmax_vec_long<H, BWD><<<grid, kSmLongWarps * 32, 0, s>>>(p, vec, long_rows, n_long);
-    note_launch();
+  if (fork) {
+    cudaEventRecord(side.join, side.stream);
+    cudaStreamWaitEvent(s, side.join, 0);
   }
 }
 
 template <bool BWD>
 bool dispatch_vec(const SoftmaxArgs& p, bool vec, const uint32_t* lr, uint32_t nl, int sms,
-                  cudaStream_t s) {
+                  cudaStream_t s, const SideStream& side) {
   switch (p.heads) {
-    case 1: launch_vec<1, BWD>(p, vec, lr, nl, sms, s); return true;
-    case 2: launch_vec<2, BWD>(p, vec, lr, nl, sms, s); return true;
-    case 4: launch_vec<4, BWD>(p, vec, lr, nl, sms, s); return true;
-    case 8: launch_vec<8, BWD>(p, vec, lr, nl, sms, s); return true;
-    case 16: launch_vec<16, BWD>(p, vec, lr, nl, sms, s); return true;
+    case 1: launch_vec<1, BWD>(p, vec, lr, nl, sms, s, side); return true;
+    case 2: launch_vec<2, BWD>(p, vec, lr, nl, sms, s, side); return true;
+    case 4: launch_vec<4, BWD>(p, vec, lr, nl, sms, s, side); return true;
+    case 8: launch_vec<8, BWD>(p, vec, lr, nl, sms, s, side); return true;
+    case 16: launch_vec<16, BWD>(p, vec, lr, nl, sms, s, side); return true;
     default: return false;
   }
 }
@@ -339,15 +433,16 @@ cudaError_t launch_edge_softmax(bool backward, const uint32_t* indptr, const uin
                                 uint32_t rows, int heads, bool by_pos, const float* l,
                                 int64_t l_ld, const float* g, int64_t g_ld, float* out,
                                 int64_t out_ld, const uint32_t* long_rows, uint32_t n_long,
-                                uint32_t long_threshold, int num_sms, cudaStream_t s) {
+                                uint32_t long_threshold, int num_sms, cudaStream_t s,
+                                const SideStream& side) {
   SoftmaxArgs p{indptr, eids, rows, heads, by_pos, l, l_ld, g, g_ld, out, out_ld,
                 n_long ? long_threshold : 0xffffffffu};
   const int sms = num_sms > 0 ? num_sms : 148;
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
   const bool vec = heads % 4 == 0 && l_ld % 4 == 0 && out_ld % 4 == 0 && al16(l) && al16(out) &&
                    (!backward || (g_ld % 4 == 0 && al16(g)));
-  if (backward ? dispatch_vec<true>(p, vec, long_rows, n_long, sms, s)
-               : dispatch_vec<false>(p, vec, long_rows, n_long, sms, s))
+  if (backward ? dispatch_vec<true>(p, vec, long_rows, n_long, sms, s, side)
+               : dispatch_vec<false>(p, vec, long_rows, n_long, sms, s, side))
     return cudaGetLastError();
   if (rows) {
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((rows + kSmWarps - 1) / kSmWarps,
