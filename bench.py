@@ -299,29 +299,26 @@ def run_ours(args, rank, world, dist):
         w_pin = torch.from_numpy(w).pin_memory()
         xn, gyn, wn = x_h.numpy(), gy_h.numpy(), w_pin.numpy()
 
-        # Steps are streamed: the forward calls of all steps run back to back
-        # in one host thread (stream A), the backward calls in another
-        # (stream B); each call still copies its inputs in and its result out.
-        # The two independent calls of a step overlap, so their H2D and D2H
-        # copies use both PCIe directions at once (handles own their
-        # workspaces; the C-ABI releases the GIL).
-        from concurrent.futures import ThreadPoolExecutor
-        pool = ThreadPoolExecutor(2)
+        # Steps are streamed through the enqueue-only host entry
+        # (gspmm_binary_reduce_host_async): forward calls on stream A, backward
+        # calls on stream B, each copying its inputs in and its result out.
+        # The uploads alternate (each waits for the other stream's previous
+        # upload), so one upload is always in flight while the other call's
+        # kernel and download run: both PCIe directions stay busy.
         s_f, s_b = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        ev_f, ev_b = torch.cuda.Event(), torch.cuda.Event()
+        ev_f.record(s_f)
+        ev_b.record(s_b)
         on, gxn = out_h.numpy(), gx_h.numpy()
 
         def run_steps(k):
-            def fwd_chain():
-                for _ in range(k):
-                    P.binary_reduce_host(gd, cfg_f, u=xn, e=wn, out=on, stream=s_f.cuda_stream)
-
-            def bwd_chain():
-                for _ in range(k):
-                    P.binary_reduce_host(gs, cfg_b, v=gyn, e=wn, out=gxn, stream=s_b.cuda_stream)
-            f = pool.submit(fwd_chain)
-            b = pool.submit(bwd_chain)
-            f.result()
-            b.result()
+            for i in range(k):
+                P.binary_reduce_host_async(gd, cfg_f, u=xn, e=wn, out=on, stream=s_f,
+                                           wait_event=ev_b if i else None, upload_event=ev_f)
+                P.binary_reduce_host_async(gs, cfg_b, v=gyn, e=wn, out=gxn, stream=s_b,
+                                           wait_event=ev_f, upload_event=ev_b)
+            s_f.synchronize()
+            s_b.synchronize()
         run_steps(max(1, min(args.warmup, 2)))
         torch.cuda.synchronize(dev)
         if dist:
@@ -335,12 +332,33 @@ def run_ours(args, rank, world, dist):
         if dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_s = float(te.item())
+        # the synchronous host entry (the reference's call shape) for
+        # comparison: fwd calls in one host thread, bwd calls in another
+        from concurrent.futures import ThreadPoolExecutor
+        pool = ThreadPoolExecutor(2)
+
+        def sync_steps(k):
+            f = pool.submit(lambda: [P.binary_reduce_host(gd, cfg_f, u=xn, e=wn, out=on,
+                                                          stream=s_f.cuda_stream)
+                                     for _ in range(k)])
+            b = pool.submit(lambda: [P.binary_reduce_host(gs, cfg_b, v=gyn, e=wn, out=gxn,
+                                                          stream=s_b.cuda_stream)
+                                     for _ in range(k)])
+            f.result()
+            b.result()
+        sync_steps(1)
+        t0 = time.perf_counter()
+        sync_steps(n_e2e)
+        sync_s = (time.perf_counter() - t0) / n_e2e
+        pool.shutdown()
         h2d = (x_h.numel() + gy_h.numel() + 2 * w.size) * 4
         d2h = (out_h.numel() + gx_h.numel()) * 4
         e2e = {"value": 2 * E / e2e_s, "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
-               "path": "gspmm_binary_reduce_host (C-ABI host entry), pinned host buffers; "
-                       "steps streamed: fwd calls in one host thread, bwd calls in another"}
+               "sync_entry_ms_per_step": sync_s * 1e3,
+               "path": "gspmm_binary_reduce_host_async (C-ABI host entry, enqueue-only), pinned "
+                       "host buffers; fwd calls on one stream, bwd calls on another, uploads "
+                       "alternating between them"}
 
     # --- CPU baseline (rank 0, N=1): the reference library, bounded sample ----
     cpu = None

@@ -227,6 +227,20 @@ int gspmm_binary_reduce_host(gspmm_graph g, const gspmm_config* cfg,
                              const gspmm_mat* u, const gspmm_mat* v,
                              const gspmm_mat* e, const gspmm_out* out,
                              const gspmm_options* opt, void* stream);
+/* The same host-buffer call, returning once the copies and kernels are
+ * enqueued on `stream` (the outputs are valid after the stream synchronizes;
+ * host buffers must be pinned and stay untouched until then).  The uploads
+ * start after `wait_event` (a cudaEvent_t, or NULL), and `upload_event` (or
+ * NULL) is recorded once the inputs are on the device: callers that stream
+ * several independent calls on two streams use the pair to keep one upload
+ * in flight at a time while the other call's kernel and download run, so
+ * both PCIe directions stay busy.  Calls on one handle must use one stream
+ * (the handle's device workspace is reused in stream order). */
+int gspmm_binary_reduce_host_async(gspmm_graph g, const gspmm_config* cfg,
+                                   const gspmm_mat* u, const gspmm_mat* v,
+                                   const gspmm_mat* e, const gspmm_out* out,
+                                   const gspmm_options* opt, void* stream,
+                                   void* wait_event, void* upload_event);
 
 /* Output shape of a config on a handle (rows, width), after the full
  * reference validation (binary_reduce kernels.cpp:418-456). */

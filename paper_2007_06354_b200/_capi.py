@@ -99,6 +99,8 @@ SIGNATURES = {
     "gspmm_edge_softmax_backward": (_i32, [_vp, _P(Mat), _P(Mat), _P(Out), _vp]),
     "gspmm_binary_reduce_host": (_i32, [_vp, _P(Config), _P(Mat), _P(Mat), _P(Mat), _P(Out),
                                         _P(Options), _vp]),
+    "gspmm_binary_reduce_host_async": (_i32, [_vp, _P(Config), _P(Mat), _P(Mat), _P(Mat),
+                                              _P(Out), _P(Options), _vp, _vp, _vp]),
     "gspmm_out_shape": (_i32, [_vp, _P(Config), _P(Mat), _P(Mat), _P(Mat), _P(Options),
                                _P(_i64), _P(_i64)]),
     "gspmm_launch_count": (_u64, []),

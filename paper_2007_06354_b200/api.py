@@ -17,7 +17,8 @@ from ._capi import (ADD, COPY, COPY_LAST, DIV, DOT, DST_MAJOR, E, EDGE_BY_ID, ED
                     MEAN, MIN, MUL, NONE, PROD, SRC_MAJOR, SUB, SUM, U, V, check)
 
 __all__ = [
-    "Graph", "binary_reduce", "binary_reduce_host", "copy_reduce", "argmax_backward",
+    "Graph", "binary_reduce", "binary_reduce_host", "binary_reduce_host_async", "copy_reduce",
+    "argmax_backward",
     "named_config", "validate_config", "required_orientation", "out_shape",
     "synth_rmat", "synth_er", "build_csr", "transpose", "synth_uniform", "synth_normal",
     "synth_gcn_weights", "synth_powerlaw", "launch_count", "edge_softmax", "edge_softmax_backward",
@@ -321,6 +322,28 @@ def binary_reduce_host(graph, cfg, u=None, v=None, e=None, *, out=None, want_arg
           "binary_reduce_host")
     if want_arg_other or want_arg_edge:
         return out, ao, ae
+    return out
+
+
+def binary_reduce_host_async(graph, cfg, u=None, v=None, e=None, *, out, heads=1, stream,
+                             wait_event=None, upload_event=None):
+    """Enqueue-only form of binary_reduce_host (gspmm_binary_reduce_host_async):
+    pinned host arrays in and out, valid once `stream` synchronizes; uploads
+    start after `wait_event` and `upload_event` is recorded when they are done
+    (torch.cuda.Event objects or raw handles)."""
+    cfg = as_config(cfg)
+    mu, mv, me = _host_mat(u), _host_mat(v), _host_mat(e)
+    rows, dim = out_shape(graph, cfg, u, v, e, heads, host=True)
+    if out.shape != (rows, dim):
+        raise A.ShapeError(f"out must be {rows} x {dim}")
+    mo = A.Out(out.ctypes.data, rows, dim, dim)
+    opts = _opts(heads, None, None)
+    ev = lambda x: None if x is None else (x if isinstance(x, int) else x.cuda_event)  # noqa: E731
+    st = stream if isinstance(stream, int) else stream.cuda_stream
+    check(A.LIB.gspmm_binary_reduce_host_async(graph.handle, C.byref(cfg), _ref(mu), _ref(mv),
+                                               _ref(me), C.byref(mo), C.byref(opts), st,
+                                               ev(wait_event), ev(upload_event)),
+          "binary_reduce_host_async")
     return out
 
 

@@ -1090,10 +1090,30 @@ int gspmm_argmax_backward(const int32_t* arg, int64_t rows, int64_t dim,
   return GSPMM_OK;
 }
 
+static int host_call(gspmm_graph g, const gspmm_config* cfg, const gspmm_mat* u,
+                     const gspmm_mat* v, const gspmm_mat* e, const gspmm_out* out,
+                     const gspmm_options* opt, void* stream, bool sync, void* wait_event,
+                     void* upload_event);
+
 int gspmm_binary_reduce_host(gspmm_graph g, const gspmm_config* cfg,
                              const gspmm_mat* u, const gspmm_mat* v,
                              const gspmm_mat* e, const gspmm_out* out,
                              const gspmm_options* opt, void* stream) {
+  return host_call(g, cfg, u, v, e, out, opt, stream, true, nullptr, nullptr);
+}
+
+int gspmm_binary_reduce_host_async(gspmm_graph g, const gspmm_config* cfg,
+                                   const gspmm_mat* u, const gspmm_mat* v,
+                                   const gspmm_mat* e, const gspmm_out* out,
+                                   const gspmm_options* opt, void* stream,
+                                   void* wait_event, void* upload_event) {
+  return host_call(g, cfg, u, v, e, out, opt, stream, false, wait_event, upload_event);
+}
+
+static int host_call(gspmm_graph g, const gspmm_config* cfg, const gspmm_mat* u,
+                     const gspmm_mat* v, const gspmm_mat* e, const gspmm_out* out,
+                     const gspmm_options* opt, void* stream, bool sync, void* wait_event,
+                     void* upload_event) {
   if (!g || !out) return fail(GSPMM_ERR_ARG, "null argument");
   // Validate against the host views first (shapes only; no pointer use).
   Bound probe;
@@ -1124,6 +1144,8 @@ int gspmm_binary_reduce_host(gspmm_graph g, const gspmm_config* cfg,
     g->ws_bytes = total;
   }
   char* p = static_cast<char*>(g->ws);
+  if (wait_event)
+    CUDA_TRY(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(wait_event), 0), "wait event");
   gspmm_mat dev[3];
   const gspmm_mat* dptr[3] = {nullptr, nullptr, nullptr};
   for (int i = 0; i < 3; ++i) {
@@ -1134,6 +1156,8 @@ int gspmm_binary_reduce_host(gspmm_graph g, const gspmm_config* cfg,
     dptr[i] = &dev[i];
     p += round_up(sz[i]);
   }
+  if (upload_event)
+    CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(upload_event), s), "upload event");
   gspmm_out dout = *out;
   dout.data = reinterpret_cast<float*>(p);
   p += round_up(out_bytes);
@@ -1156,7 +1180,7 @@ int gspmm_binary_reduce_host(gspmm_graph g, const gspmm_config* cfg,
   if (ae)
     CUDA_TRY(cudaMemcpyAsync(opt->arg_edge, dopt.arg_edge, arg_bytes, cudaMemcpyDeviceToHost, s),
              "D2H arg");
-  CUDA_TRY(cudaStreamSynchronize(s), "synchronize");
+  if (sync) CUDA_TRY(cudaStreamSynchronize(s), "synchronize");
   return GSPMM_OK;
 }
 

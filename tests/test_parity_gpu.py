@@ -286,6 +286,39 @@ def test_host_entry_matches_device_entry():
     assert O.bit_equal(val, v2) and (au == au2).all() and (ae == ae2).all()
 
 
+def test_async_host_entry_streams_steps():
+    # gspmm_binary_reduce_host_async: forward and backward calls streamed on
+    # two streams with alternating uploads (the bench's e2e schedule); every
+    # step's outputs equal the synchronous entry's bit for bit
+    src, dst = O.gen_rmat(2000, 30000, seed=8)
+    g = O.Graph(2000, src, dst)
+    w = O.gcn_weights(2000, src, dst)
+    hd, hs = dev_graph(g, O.DST_MAJOR), dev_graph(g, O.SRC_MAJOR)
+    cf, cb = (O.U, O.E, O.MUL, O.SUM, O.V), (O.V, O.E, O.MUL, O.SUM, O.U)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    ea, eb = torch.cuda.Event(), torch.cuda.Event()
+    ea.record(sa)
+    eb.record(sb)
+    wp = torch.from_numpy(w).pin_memory().numpy()
+    outs = []
+    for step in range(3):
+        x = torch.from_numpy(O.normal_features(2000, 64, 10 + step)).pin_memory().numpy()
+        gy = torch.from_numpy(O.normal_features(2000, 64, 20 + step)).pin_memory().numpy()
+        of = torch.empty((2000, 64), pin_memory=True).numpy()
+        ob = torch.empty((2000, 64), pin_memory=True).numpy()
+        P.binary_reduce_host_async(hd, cf, u=x, e=wp, out=of, stream=sa,
+                                   wait_event=eb if step else None, upload_event=ea)
+        P.binary_reduce_host_async(hs, cb, v=gy, e=wp, out=ob, stream=sb, wait_event=ea,
+                                   upload_event=eb)
+        outs.append((x, gy, of, ob))
+    sa.synchronize()
+    sb.synchronize()
+    for x, gy, of, ob in outs:
+        assert O.bit_equal(of, P.binary_reduce_host(hd, cf, u=x, e=w))
+        assert O.bit_equal(ob, P.binary_reduce_host(hs, cb, v=gy, e=w))
+        assert O.bit_equal(of, O.binary_reduce(g, cf, u=x, e=w))
+
+
 # ------------------------------------------- extensions
 @pytest.mark.parametrize("seed", range(5))
 def test_mean_and_mean_backward(seed):
