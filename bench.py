@@ -215,12 +215,19 @@ def cpu_info():
 
 
 # --------------------------------------------------------------- our arm
+def local_device():
+    """This rank's GPU: LOCAL_RANK (modulo the visible devices, for the
+    single-GPU functional test of the multi-rank path)."""
+    import torch
+    return int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count())
+
+
 def run_ours(args, rank, world, dist):
     import torch
     import paper_2007_06354_b200 as P
     from paper_2007_06354_b200.shard import balanced_row_ranges, slice_csr
 
-    dev = int(os.environ.get("LOCAL_RANK", 0))
+    dev = local_device()
     torch.cuda.set_device(dev)
     src, dst, w, dcsr, scsr = make_inputs()
     E = len(src)
@@ -296,8 +303,18 @@ def run_ours(args, rank, world, dist):
     if not args.skip_e2e:
         out_h = torch.empty((d_hi - d_lo, FEAT), dtype=torch.float32, pin_memory=True)
         gx_h = torch.empty((s_hi - s_lo, FEAT), dtype=torch.float32, pin_memory=True)
-        w_pin = torch.from_numpy(w).pin_memory()
-        xn, gyn, wn = x_h.numpy(), gy_h.numpy(), w_pin.numpy()
+        # edge weights as the reference lays them out (edge-id order) on one
+        # GPU; a shard's handles hold global edge ids, so each rank passes its
+        # weights in its handles' CSR order instead (EDGE_BY_POS)
+        if world == 1:
+            wf_h = wb_h = torch.from_numpy(w).pin_memory()
+            e_ord = P.EDGE_BY_ID
+        else:
+            wf_h = torch.from_numpy(w[dsl[2]]).pin_memory()
+            wb_h = torch.from_numpy(w[ssl[2]]).pin_memory()
+            e_ord = P.EDGE_BY_POS
+        xn, gyn = x_h.numpy(), gy_h.numpy()
+        wfn, wbn = wf_h.numpy(), wb_h.numpy()
 
         # Steps are streamed through the enqueue-only host entry
         # (gspmm_binary_reduce_host_async): forward calls on stream A, backward
@@ -313,10 +330,11 @@ def run_ours(args, rank, world, dist):
 
         def run_steps(k):
             for i in range(k):
-                P.binary_reduce_host_async(gd, cfg_f, u=xn, e=wn, out=on, stream=s_f,
-                                           wait_event=ev_b if i else None, upload_event=ev_f)
-                P.binary_reduce_host_async(gs, cfg_b, v=gyn, e=wn, out=gxn, stream=s_b,
-                                           wait_event=ev_f, upload_event=ev_b)
+                P.binary_reduce_host_async(gd, cfg_f, u=xn, e=wfn, out=on, stream=s_f,
+                                           wait_event=ev_b if i else None, upload_event=ev_f,
+                                           e_order=e_ord)
+                P.binary_reduce_host_async(gs, cfg_b, v=gyn, e=wbn, out=gxn, stream=s_b,
+                                           wait_event=ev_f, upload_event=ev_b, e_order=e_ord)
             s_f.synchronize()
             s_b.synchronize()
         run_steps(max(1, min(args.warmup, 2)))
@@ -338,11 +356,11 @@ def run_ours(args, rank, world, dist):
         pool = ThreadPoolExecutor(2)
 
         def sync_steps(k):
-            f = pool.submit(lambda: [P.binary_reduce_host(gd, cfg_f, u=xn, e=wn, out=on,
-                                                          stream=s_f.cuda_stream)
+            f = pool.submit(lambda: [P.binary_reduce_host(gd, cfg_f, u=xn, e=wfn, out=on,
+                                                          stream=s_f.cuda_stream, e_order=e_ord)
                                      for _ in range(k)])
-            b = pool.submit(lambda: [P.binary_reduce_host(gs, cfg_b, v=gyn, e=wn, out=gxn,
-                                                          stream=s_b.cuda_stream)
+            b = pool.submit(lambda: [P.binary_reduce_host(gs, cfg_b, v=gyn, e=wbn, out=gxn,
+                                                          stream=s_b.cuda_stream, e_order=e_ord)
                                      for _ in range(k)])
             f.result()
             b.result()
@@ -351,7 +369,7 @@ def run_ours(args, rank, world, dist):
         sync_steps(n_e2e)
         sync_s = (time.perf_counter() - t0) / n_e2e
         pool.shutdown()
-        h2d = (x_h.numel() + gy_h.numel() + 2 * w.size) * 4
+        h2d = (x_h.numel() + gy_h.numel() + wf_h.numel() + wb_h.numel()) * 4
         d2h = (out_h.numel() + gx_h.numel()) * 4
         e2e = {"value": 2 * E / e2e_s, "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
@@ -457,7 +475,7 @@ def run_cfg5(args, rank, world, dist):
     import paper_2007_06354_b200 as P
     from paper_2007_06354_b200.dist import ShardPlan, ShardedMean
 
-    dev = int(os.environ.get("LOCAL_RANK", 0))
+    dev = local_device()
     torch.cuda.set_device(dev)
     t0 = time.time()
     src, dst = P.synth_powerlaw(C5_NODES, C5_DMIN, C5_DMAX, SEEDS["graph"])
@@ -624,8 +642,10 @@ def main():
         if world > 1:
             import torch
             import torch.distributed as tdist
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-            tdist.init_process_group("nccl")
+            torch.cuda.set_device(local_device())
+            # NCCL in production; BENCH_DIST_BACKEND=gloo lets a functional
+            # test run several ranks on one GPU (its timings are meaningless)
+            tdist.init_process_group(os.environ.get("BENCH_DIST_BACKEND", "nccl"))
             dist = tdist
         res = (run_cfg5 if args.workload == "cfg5" else run_ours)(args, rank, world, dist)
         if dist:

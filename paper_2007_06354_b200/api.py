@@ -152,7 +152,9 @@ class Graph:
         (device, untimed setup like the reference's BlockPlan)."""
         import torch
         e2 = e.reshape(e.shape[0], -1)
-        out = torch.empty_like(e2)
+        # one row per CSR position of this handle (a shard's edge ids index a
+        # larger, global edge operand)
+        out = torch.empty((self.num_edges, e2.shape[1]), dtype=e2.dtype, device=e2.device)
         check(A.LIB.gspmm_graph_permute_edges(self.handle, e2.data_ptr(), e2.shape[1],
                                               e2.stride(0), out.data_ptr(), out.stride(0),
                                               _stream(stream, e2)), "permute_edges")
@@ -305,11 +307,11 @@ def edge_softmax_backward(graph, a, grad_a, *, out=None, e_order=EDGE_BY_ID, str
 
 
 def binary_reduce_host(graph, cfg, u=None, v=None, e=None, *, out=None, want_arg_other=False,
-                       want_arg_edge=False, heads=1, stream=None):
+                       want_arg_edge=False, heads=1, stream=None, e_order=EDGE_BY_ID):
     """The reference's synchronous call shape: numpy in, numpy out, through
     the C-ABI host entry (H2D, kernel, D2H)."""
     cfg = as_config(cfg)
-    mu, mv, me = _host_mat(u), _host_mat(v), _host_mat(e)
+    mu, mv, me = _host_mat(u), _host_mat(v), _host_mat(e, e_order)
     rows, dim = out_shape(graph, cfg, u, v, e, heads, host=True)
     if out is None:
         out = np.empty((rows, dim), np.float32)
@@ -326,13 +328,13 @@ def binary_reduce_host(graph, cfg, u=None, v=None, e=None, *, out=None, want_arg
 
 
 def binary_reduce_host_async(graph, cfg, u=None, v=None, e=None, *, out, heads=1, stream,
-                             wait_event=None, upload_event=None):
+                             wait_event=None, upload_event=None, e_order=EDGE_BY_ID):
     """Enqueue-only form of binary_reduce_host (gspmm_binary_reduce_host_async):
     pinned host arrays in and out, valid once `stream` synchronizes; uploads
     start after `wait_event` and `upload_event` is recorded when they are done
     (torch.cuda.Event objects or raw handles)."""
     cfg = as_config(cfg)
-    mu, mv, me = _host_mat(u), _host_mat(v), _host_mat(e)
+    mu, mv, me = _host_mat(u), _host_mat(v), _host_mat(e, e_order)
     rows, dim = out_shape(graph, cfg, u, v, e, heads, host=True)
     if out.shape != (rows, dim):
         raise A.ShapeError(f"out must be {rows} x {dim}")
