@@ -532,3 +532,30 @@ def test_source_blocks_bit_exact(nb, monkeypatch):
         got, plain = got.cpu().numpy(), plain.cpu().numpy()
         assert O.bit_equal(plain, want), cfg
         assert O.bit_equal(got, want), (nb, cfg)
+
+
+def test_row_shards_with_global_edge_ids():
+    # a rank's handle over a row shard keeps global neighbour and edge ids
+    # (bench.py / shard.py): edge operands in edge-id order must be permuted
+    # to the shard's CSR positions (one row per shard edge), and the shard's
+    # rows of every result equal the whole graph's, bit for bit
+    from paper_2007_06354_b200.shard import balanced_row_ranges, slice_csr
+    src, dst = O.gen_rmat(3000, 40000, seed=11)
+    src, dst = O.add_self_loops(3000, src, dst)
+    g = O.Graph(3000, src, dst)
+    x = O.normal_features(3000, 64, 3)
+    w = O.gcn_weights(3000, src, dst)
+    cfg = (O.U, O.E, O.MUL, O.SUM, O.V)
+    want = O.binary_reduce(g, cfg, u=x, e=w)
+    ip, ix, ei = g.csr(O.DST_MAJOR)
+    bounds = balanced_row_ranges(ip, 3)
+    for k in range(3):
+        lo, hi = int(bounds[k]), int(bounds[k + 1])
+        sip, six, sei = slice_csr(ip, ix, ei, lo, hi)
+        h = P.Graph(sip, six, sei, num_rows=hi - lo, num_cols=3000, orientation=P.DST_MAJOR)
+        wp = h.permute_edges(cuda(w))
+        assert wp.shape[0] == h.num_edges
+        got = P.binary_reduce(h, cfg, u=cuda(x), e=wp, e_order=P.EDGE_BY_POS).cpu().numpy()
+        assert O.bit_equal(got, want[lo:hi])
+        got_h = P.binary_reduce_host(h, cfg, u=x, e=w[sei], e_order=P.EDGE_BY_POS)
+        assert O.bit_equal(got_h, want[lo:hi])
