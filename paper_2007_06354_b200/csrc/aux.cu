@@ -55,6 +55,27 @@ __global__ void k_round_f64(const double* __restrict__ acc, int64_t rows,
   }
 }
 
+// y[r, :] = x[r, :] * scale[r] (each product rounded once, as the row
+// kernels' per-edge scale does): rows of the gathered operand scaled once
+// instead of once per edge.  Warp per row, float4 columns (16-byte rows).
+__global__ void k_scale_rows(const float* __restrict__ x, int64_t rows, int64_t dim, int64_t ld,
+                             const float* __restrict__ scale, float* __restrict__ y,
+                             int64_t y_ld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       r < rows; r += warps) {
+    const float sc = __ldg(scale + r);
+    const float4* xr = reinterpret_cast<const float4*>(x + r * ld);
+    float4* yr = reinterpret_cast<float4*>(y + r * y_ld);
+    for (int64_t q = lane; q * 4 < dim; q += 32) {
+      const float4 v = __ldg(xr + q);
+      yr[q] = make_float4(__fmul_rn(v.x, sc), __fmul_rn(v.y, sc), __fmul_rn(v.z, sc),
+                          __fmul_rn(v.w, sc));
+    }
+  }
+}
+
 unsigned grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
   if (b > 148 * 32) b = 148 * 32;
@@ -94,6 +115,14 @@ cudaError_t launch_argmax_backward(const int32_t* arg, int64_t rows,
                                                              src_ld);
     note_launch();
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_rows(const float* x, int64_t rows, int64_t dim, int64_t ld,
+                              const float* scale, float* y, int64_t y_ld, cudaStream_t s) {
+  if (rows == 0 || dim == 0) return cudaSuccess;
+  k_scale_rows<<<grid_for(rows * 32, 256), 256, 0, s>>>(x, rows, dim, ld, scale, y, y_ld);
+  note_launch();
   return cudaGetLastError();
 }
 

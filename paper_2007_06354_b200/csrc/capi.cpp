@@ -99,6 +99,8 @@ struct gspmm_graph_s {
   std::mutex mu;  // guards the host-call workspace
   void* ws = nullptr;
   size_t ws_bytes = 0;
+  void* dws = nullptr;  // device workspace of the prescaled gathers
+  size_t dws_bytes = 0;
   // source blocks (gspmm_graph_set_source_blocks): sub-graphs over neighbour
   // id ranges, built on first use for block_nb blocks
   int blocks_pref = 0;  // 0 auto, 1 never, >= 2 forced
@@ -435,6 +437,45 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int rw = 0;
   int kind = 0;
+  if (!b.L.out_edge && b.L.binop != GSPMM_DOT && b.L.other_scale && !b.L.rhs.base &&
+      b.L.binop == GSPMM_COPY && b.L.lhs.role == ROLE_OTHER && b.L.lhs.mode == MODE_FULL &&
+      b.L.lhs.rows > 0 && plan_kernel(b.L, &rw) != 0 &&
+      static_cast<double>(g->m) >= 4.0 * static_cast<double>(b.L.lhs.rows)) {
+    // The per-neighbour scale (the mean backward's 1/deg) on dense-enough
+    // graphs: scale every gathered row once into a workspace, then run the
+    // plain copy-sum.  Each product is the same single rounding as the
+    // kernels' per-edge scale, so the result is bit-identical (measured: cfg3
+    // mean backward 6.67 -> see DESIGN).
+    static const bool prescale_on = std::getenv("GSPMM_NO_PRESCALE") == nullptr;
+    if (prescale_on) {
+      const int64_t W = b.L.width;
+      const int64_t yld = (W + 3) & ~int64_t{3};
+      // the handle's device workspace (grown on demand; a handle runs one
+      // call at a time).  A stream-ordered allocation per call measured
+      // slower than the whole saving: the pool unmaps it at every sync.
+      const size_t need = sizeof(float) * static_cast<size_t>(b.L.lhs.rows * yld);
+      if (need > g->dws_bytes) {
+        cudaFree(g->dws);
+        g->dws = nullptr;
+        g->dws_bytes = 0;
+        CUDA_TRY(cudaMalloc(&g->dws, need), "prescale workspace");
+        g->dws_bytes = need;
+      }
+      float* y = static_cast<float*>(g->dws);
+      cudaError_t e0 = launch_scale_rows(b.L.lhs.base, b.L.lhs.rows, W, b.L.lhs.ld,
+                                         b.L.other_scale, y, yld, s);
+      int st = GSPMM_OK;
+      if (e0 == cudaSuccess) {
+        Bound bb = b;
+        bb.L.lhs.base = y;
+        bb.L.lhs.ld = yld;
+        bb.L.other_scale = nullptr;
+        st = launch(g, bb, stream);
+      }
+      if (e0 != cudaSuccess) return cuda_fail(e0, "prescale");
+      return st;
+    }
+  }
   if (!b.L.out_edge && b.L.binop != GSPMM_DOT) {
     const uint32_t nb = source_blocks_for(g, b.L);
     if (nb > 1) return launch_blocked(g, b, stream, nb);
@@ -933,6 +974,7 @@ void destroy_graph(gspmm_graph_s* g) {
     cudaEventDestroy(g->ev_join);
   }
   cudaFree(g->ws);
+  cudaFree(g->dws);
   delete g;
 }
 }  // namespace

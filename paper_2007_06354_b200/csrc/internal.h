@@ -126,6 +126,12 @@ cudaError_t launch_block_csr(const uint32_t* lo, const uint32_t* hi, uint32_t ro
                              const uint32_t* indices, const uint32_t* eids, uint32_t* indptr_b,
                              uint32_t* idx_b, uint32_t* eid_b, cudaStream_t s);
 
+// y[r, :] = x[r, :] * scale[r] over 16-byte aligned rows (ld, y_ld % 4 == 0)
+// (aux.cu): the per-neighbour scale of the mean backward applied once per
+// gathered row.
+cudaError_t launch_scale_rows(const float* x, int64_t rows, int64_t dim, int64_t ld,
+                              const float* scale, float* y, int64_t y_ld, cudaStream_t s);
+
 // Launch counter (evidence of native execution), bumped by each launcher.
 void note_launch(uint64_t n = 1);
 
