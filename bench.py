@@ -568,6 +568,180 @@ def run_cfg5(args, rank, world, dist):
     }
 
 
+# ------------------------------------------------ cfg1 / cfg3 / cfg4 steps
+CFG_WORKLOADS = {
+    "cfg1": "cfg1: copy_u+sum fwd, Erdos-Renyi 100,000 nodes / 1.6M edges (no self-loops), "
+            "x fp32 [100000 x 128] U(-1,1), seed 0; L2 flushed between steps",
+    "cfg3": "cfg3: copy_u+max with argmax and copy_u+mean, fwd+bwd, R-MAT(.57,.19,.19,.05) "
+            "2,449,029 nodes / 61,859,140 edges symmetrised to 123,718,280, x fp32 [N x 100] "
+            "U(-1,1), grad N(0,1)",
+    "cfg4": "cfg4: 8-head u_mul_e+sum (GAT aggregation) fwd+bwd (grad_x, grad_a), R-MAT 1M nodes "
+            "/ 32M edges, x fp32 [1M x 8 x 64] N(0,1), a = edge softmax of N(0,1) logits [E x 8]",
+}
+
+
+def run_config(args, rank, world, dist):
+    """--workload cfg1 / cfg3 / cfg4: one step = every pass of the config
+    (SURVEY 8d), owner rows of each orientation sharded over the ranks
+    (edge-balanced), features replicated (no data-path collective, except the
+    cfg3 max backward's scatter, summed over ranks with one all-reduce).
+    value = E x (edge aggregation passes) / step time, max over ranks."""
+    import torch
+    import paper_2007_06354_b200 as P
+    from paper_2007_06354_b200.shard import balanced_row_ranges, slice_csr
+
+    dev = local_device()
+    torch.cuda.set_device(dev)
+    wl = args.workload
+    t0 = time.time()
+    if wl == "cfg1":
+        n, F = 100_000, 128
+        src, dst = P.synth_er(n, 1_600_000, -1.0, 0)
+    elif wl == "cfg3":
+        n, F = 2_449_029, 100
+        src, dst = P.synth_rmat(n, 61_859_140, 0.57, 0.19, 0.19, 0.05, 0)
+        src, dst = np.concatenate([src, dst]), np.concatenate([dst, src])
+    else:
+        n, F = 1_000_000, 512
+        src, dst = P.synth_rmat(n, 32_000_000, 0.57, 0.19, 0.19, 0.05, 0)
+    E = len(src)
+    dcsr = P.build_csr(n, src, dst, P.DST_MAJOR)
+    scsr = P.transpose(n, n, *dcsr)
+    db, sb = balanced_row_ranges(dcsr[0], world), balanced_row_ranges(scsr[0], world)
+    d_lo, d_hi, s_lo, s_hi = int(db[rank]), int(db[rank + 1]), int(sb[rank]), int(sb[rank + 1])
+    gd = P.Graph(*slice_csr(*dcsr, d_lo, d_hi), num_rows=d_hi - d_lo, num_cols=n,
+                 orientation=P.DST_MAJOR, device=dev)
+    gs = P.Graph(*slice_csr(*scsr, s_lo, s_hi), num_rows=s_hi - s_lo, num_cols=n,
+                 orientation=P.SRC_MAJOR, device=dev)
+    x = torch.empty((n, F), dtype=torch.float32)
+    if wl == "cfg4":
+        P.synth_normal(n, F, 1, out=x.numpy())
+    else:
+        P.synth_uniform(n, F, 0 if wl == "cfg1" else 1, out=x.numpy())
+    x = x.cuda(dev)
+    log(f"[bench] {wl} rank {rank}: {E} edges, dst rows [{d_lo},{d_hi}), src rows "
+        f"[{s_lo},{s_hi}); inputs {time.time() - t0:.1f}s")
+    stream = torch.cuda.current_stream(dev)
+    rd, rs = d_hi - d_lo, s_hi - s_lo
+    U_, V_, E_, NONE_ = P.U, P.V, P.E, P.NONE
+    passes = []  # (name, fn, algorithmic bytes, aggregates edges)
+    csr_b = lambda rows, m: (rows + 1) * 4 + m * 4  # noqa: E731
+    if wl == "cfg1":
+        out = torch.empty((rd, F), device=dev)
+        passes.append(("fwd copy_u+sum", lambda: P.binary_reduce(gd, "u_copy_add_v", u=x, out=out),
+                       gd.num_edges * F * 4 + csr_b(rd, gd.num_edges) + rd * F * 4, True))
+    elif wl == "cfg3":
+        gy = torch.randn((n, F), device=dev, generator=torch.Generator(dev).manual_seed(3))
+        mx = torch.empty((rd, F), device=dev)
+        mean = torch.empty((rd, F), device=dev)
+        gxm = torch.empty((rs, F), device=dev)
+        gmax = torch.empty((n, F), device=dev)
+        deg = np.diff(dcsr[0].astype(np.int64))
+        inv = torch.from_numpy(np.where(deg > 0, 1.0 / np.maximum(deg, 1), 0).astype(np.float32)).cuda(dev)
+        base = gd.num_edges * F * 4 + csr_b(rd, gd.num_edges) + rd * F * 4
+        hold = {}
+
+        def max_fwd():
+            hold["au"] = P.binary_reduce(gd, (U_, NONE_, P.COPY, P.MAX, V_), u=x, out=mx,
+                                         want_arg_other=True)[1]
+        passes.append(("fwd copy_u+max+argmax", max_fwd, base + rd * F * 4, True))
+        passes.append(("fwd copy_u+mean", lambda: P.binary_reduce(
+            gd, (U_, NONE_, P.COPY, P.MEAN, V_), u=x, out=mean), base, True))
+        passes.append(("bwd mean (grad_x)", lambda: P.binary_reduce(
+            gs, (V_, NONE_, P.COPY, P.SUM, U_), v=gy, out=gxm, other_scale=inv),
+            gs.num_edges * F * 4 + csr_b(rs, gs.num_edges) + rs * F * 4, True))
+
+        def max_bwd():
+            P.argmax_backward(hold["au"], gy[d_lo:d_hi], n, out=gmax)
+            if dist:
+                dist.all_reduce(gmax)  # each rank scattered its own dst rows
+        passes.append(("bwd max (argmax scatter)", max_bwd, rd * F * 4 * 3, False))
+    else:
+        heads = 8
+        lg = torch.randn((E, heads), device=dev, generator=torch.Generator(dev).manual_seed(2))
+        a_full = torch.empty((E, heads), device=dev)
+        gfull = P.Graph(*dcsr, orientation=P.DST_MAJOR, device=dev)
+        P.edge_softmax(gfull, lg, out=a_full)  # input synthesis (by edge id), untimed
+        gfull.close()
+        del lg
+        a_d = gd.permute_edges(a_full)
+        a_s = gs.permute_edges(a_full)
+        gy = torch.randn((n, F), device=dev, generator=torch.Generator(dev).manual_seed(3))
+        out = torch.empty((rd, F), device=dev)
+        gx = torch.empty((rs, F), device=dev)
+        ga = torch.empty((E, heads), device=dev)
+        cfg_d = (U_, V_, P.DOT, P.COPY_LAST, E_)
+        passes.append(("fwd 8-head u_mul_e+sum", lambda: P.binary_reduce(
+            gd, "u_mul_e_add_v", u=x, e=a_d, out=out, e_order=P.EDGE_BY_POS, heads=heads),
+            gd.num_edges * (F + heads + 1) * 4 + (rd + 1) * 4 + rd * F * 4, True))
+        passes.append(("bwd grad_x", lambda: P.binary_reduce(
+            gs, "v_mul_e_add_u", v=gy, e=a_s, out=gx, e_order=P.EDGE_BY_POS, heads=heads),
+            gs.num_edges * (F + heads + 1) * 4 + (rs + 1) * 4 + rs * F * 4, True))
+        passes.append(("bwd grad_a (8-head u_dot_v)", lambda: P.binary_reduce(
+            gd, cfg_d, u=x, v=gy, out=ga, heads=heads),
+            gd.num_edges * (F + 2 + heads) * 4 + (rd + 1) * 4 + rd * F * 4, True))
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev) if wl == "cfg1" else None
+
+    def step(evs=None):
+        for k, (_, fn, _, _) in enumerate(passes):
+            if evs:
+                evs[k].record(stream)
+            fn()
+        if evs:
+            evs[-1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+        if flush is not None:
+            flush.zero_()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(passes) + 1)]
+           for _ in range(args.steps)]
+    launches0 = P.launch_count()
+    with ClockSampler(dev) as clk:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.zero_()  # 256 MB > L2: every step starts cold (timing rule)
+            step(evs[i])
+        torch.cuda.synchronize(dev)
+    launches = P.launch_count() - launches0
+    pass_ms = [[e[k].elapsed_time(e[k + 1]) for e in evs] for k in range(len(passes))]
+    avg = [sum(v) / len(v) for v in pass_ms]
+    step_ms = sum(avg)
+    t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms = float(t.item())
+    if rank != 0:
+        return None
+    n_edge_passes = sum(1 for p in passes if p[3])
+    peak, peak_src = peaks()
+    k_dom = max(range(len(passes)), key=lambda k: avg[k])
+    achieved = passes[k_dom][2] / (avg[k_dom] * 1e-3) / 1e9
+    return {
+        "metric": f"aggregated edges/s ({wl}, all passes of the step)",
+        "value": n_edge_passes * E / (step_ms * 1e-3), "unit": "edges/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded generators of SURVEY 8d)",
+        "config": {"workload": CFG_WORKLOADS[wl], "edges": E, "nodes": n, "feat": F,
+                   "edge_passes_per_step": n_edge_passes,
+                   "parallelism": f"dst/src-row shards x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed between steps (256 MB write)" if wl == "cfg1" else
+                         "inputs larger than the 126 MB L2; no flush"},
+        "passes_ms": {p[0]: round(a, 4) for p, a in zip(passes, avg)},
+        "roofline": {"bound": "hbm", "kernel": passes[k_dom][0], "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "alg_bytes_per_launch": passes[k_dom][2], "avg_launch_ms": avg[k_dom],
+                     "peak_source": peak_src},
+        "e2e": None, "cpu_baseline": None,
+        "gpu_launches": int(launches // max(1, args.steps)) * args.steps,
+        "clocks": clk.summary(), "impl": "b200",
+    }
+
+
 def run_reference(args, rank, world):
     """--impl reference: the unmodified reference library on the host cores."""
     if rank != 0:
@@ -625,7 +799,7 @@ def main():
     ap.add_argument("--cfg5-chunk", type=int, default=0,
                     help="cfg5: all-gather / aggregation column chunk (0: 640 on one GPU, "
                          "else 256)")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5"],
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
                     help="cfg2 (BASELINE configs[1], the headline) or cfg5 (multi-GPU "
                          "GraphSAGE-mean with source-feature all-gather)")
     args = ap.parse_args()
@@ -647,7 +821,8 @@ def main():
             # test run several ranks on one GPU (its timings are meaningless)
             tdist.init_process_group(os.environ.get("BENCH_DIST_BACKEND", "nccl"))
             dist = tdist
-        res = (run_cfg5 if args.workload == "cfg5" else run_ours)(args, rank, world, dist)
+        res = {"cfg2": run_ours, "cfg5": run_cfg5}.get(args.workload, run_config)(
+            args, rank, world, dist)
         if dist:
             dist.destroy_process_group()
     if rank == 0 and res is not None:

@@ -68,6 +68,25 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
   return x > 0 ? static_cast<uint32_t>(x) : dflt;
 }
 
+// The stream-ordered pool of the current device keeps freed memory mapped
+// across synchronizations (its default release threshold of 0 unmaps it at
+// every sync, which made each call's f64 workspace cost a re-map).
+void retain_pool_memory() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int d : done)
+    if (d == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done.push_back(dev);
+}
+
 }  // namespace
 
 struct gspmm_graph_s {
@@ -1121,6 +1140,7 @@ int gspmm_argmax_backward(const int32_t* arg, int64_t rows, int64_t dim,
                           void* stream) {
   if (!arg || !grad_out || !grad_src) return fail(GSPMM_ERR_ARG, "null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  retain_pool_memory();
   double* acc = nullptr;
   const size_t bytes = sizeof(double) * std::max<int64_t>(src_rows * dim, 1);
   CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&acc), bytes, s), "argmax workspace");
