@@ -55,6 +55,12 @@ constexpr int kThreads = 256;
 #ifndef GATHER_U5
 #define GATHER_U5 2
 #endif
+// L2 prefetch distance of the segment kernel, in batches (0 = off).
+// Measured slower at every distance (cfg2 1.82 -> 1.89 / 1.91 / 2.01 ms at
+// 2 / 4 / 8 batches; uniform er256 2.41 -> 3.96 ms at 8): kept for study.
+#ifndef GATHER_PF
+#define GATHER_PF 0
+#endif
 #ifndef GATHER_MINB5
 #define GATHER_MINB5 2
 
@@ -277,6 +283,22 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
     }
     const uint32_t jb = u.e0 + b * U;
     const uint32_t n = min(static_cast<uint32_t>(U), u.e1 - jb);
+    if constexpr (GATHER_PF > 0 && LO) {
+      // L2 prefetch of the rows GATHER_PF batches ahead: memory-level
+      // parallelism beyond the registers' ping-pong, at one instruction per
+      // lane (lane = (edge, 128-byte line of its slice))
+      constexpr int kLines = VPL * 4;  // 128-byte lines per <= VPL*128-column slice
+      constexpr int kEdges = 32 / kLines < U ? 32 / kLines : U;
+      const uint32_t q = (b + GATHER_PF) * U + static_cast<uint32_t>(lane / kLines);  // unit edge
+      const int line = lane % kLines;
+      const uint32_t src_lane = q & 31u;
+      const uint32_t o_cur = __shfl_sync(kFull, win_o, src_lane);
+      const uint32_t o_nxt = __shfl_sync(kFull, nxt_o, src_lane);
+      const uint32_t wq = q / 32u, wb = b / static_cast<uint32_t>(kPerWin);
+      if (lane / kLines < kEdges && u.e0 + q < u.e1 && line * 32 < u.cw && (wq == wb || wq == wb + 1))
+        prefetch_l2(reinterpret_cast<const char*>(L.lhs.base + u.c0 + line * 32) +
+                    static_cast<uint64_t>(wq == wb ? o_cur : o_nxt) * ldb);
+    }
     float4 x[U][VPL];
     float r[U][SK == SK_HEAD ? VPL : 1];
     uint32_t okey[ARG == 2 ? U : 1];  // ARG 2: the neighbour id of each edge
