@@ -55,7 +55,12 @@ const char* operand_name(int o) {
 // Device plan defaults: cost (edges + 2 per row) per row segment, and the
 // coarsest long-row threshold.  Overridable for experiments with
 // GSPMM_SEG_EDGES / GSPMM_LONG_EDGES (the latter forces a single level).
-constexpr uint32_t kSegEdges = 1024;
+// 256: with every unit pulled from the counter, finer units shorten the
+// segment kernel's drain (measured cost 1024 / 512 / 256 / 128 / 64: cfg2
+// forward 1.87 / 1.72 / 1.70 / 1.69 / 1.69 ms, cfg3 mean 5.54 / 5.48 / 5.45 /
+// 5.46 / 5.51, cfg4 7.18 / 7.19 / 7.01 / 7.12 / 7.00, cfg5 -- / -- / 15.6 /
+// 15.5 / 15.5; 2048: cfg2 2.08)
+constexpr uint32_t kSegEdges = 256;
 constexpr uint32_t kLongEdges = 4096;
 // rows above this many edges are cut into 64-column slices so several CTAs
 // stream one row (the 66k-329k-edge hubs of the power-law configs)
