@@ -559,3 +559,28 @@ def test_row_shards_with_global_edge_ids():
         assert O.bit_equal(got, want[lo:hi])
         got_h = P.binary_reduce_host(h, cfg, u=x, e=w[sei], e_order=P.EDGE_BY_POS)
         assert O.bit_equal(got_h, want[lo:hi])
+
+
+def test_wide_rows_mean_and_mean_backward():
+    # 602-column rows with a 16-byte leading dimension (cfg5's layout): one
+    # wide segment unit per row (up to 640 columns), the fused mean
+    # epilogue, and the mean backward's per-neighbour scale applied once per
+    # gathered row -- all bit-exact
+    src, dst = O.gen_rmat(2500, 60000, seed=4)
+    g = O.Graph(2500, src, dst)
+    x = O.normal_features(2500, 602, 7)
+    gy = O.normal_features(2500, 602, 8)
+    xp = torch.zeros((2500, 604), device="cuda")
+    xp[:, :602] = cuda(x)
+    gp = torch.zeros((2500, 604), device="cuda")
+    gp[:, :602] = cuda(gy)
+    op = torch.empty((2500, 604), device="cuda")
+    hd, hs = dev_graph(g, O.DST_MAJOR), dev_graph(g, O.SRC_MAJOR)
+    P.binary_reduce(hd, (O.U, O.NONE, O.COPY, P.MEAN, O.V), u=xp[:, :602], out=op[:, :602])
+    assert O.bit_equal(op[:, :602].cpu().numpy(), O.mean(g, x))
+    deg = O.in_degree(g)
+    inv = np.zeros(2500, np.float32)
+    inv[deg > 0] = np.float32(1) / deg[deg > 0].astype(np.float32)
+    P.binary_reduce(hs, (O.V, O.NONE, O.COPY, O.SUM, O.U), v=gp[:, :602], out=op[:, :602],
+                    other_scale=torch.from_numpy(inv).cuda())
+    assert O.bit_equal(op[:, :602].cpu().numpy(), O.mean_backward(g, gy))
