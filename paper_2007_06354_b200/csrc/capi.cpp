@@ -546,6 +546,9 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
     // one unit covers up to 640 columns for copy / scalar-weighted sums of
     // gathered rows (gather_impl.cuh launch_wide), else <= 256-column slices
     // (measured on cfg5, W = 602: 18.2 -> 16.0 ms)
+    // per-head weights on wide units: opt-in (GSPMM_WIDE_HEADS), measured
+    // slower on cfg4 (7.04 -> 7.51 ms: 128 registers, 20% idle quads at 512)
+    static const bool wide_heads = std::getenv("GSPMM_WIDE_HEADS") != nullptr;
     static const bool wide_on = [] {
       const char* v = std::getenv("GSPMM_WIDE_UNITS");
       return !(v && std::strcmp(v, "0") == 0);
@@ -554,7 +557,8 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
     // lanes idle -- measured slower than two slices at W = 304)
     const bool wide = wide_on && W > 384 && W <= 640 && b.L.reduce == R_SUM && !b.L.arg_other &&
                       !b.L.arg_edge && b.L.lhs.role == ROLE_OTHER &&
-                      ((b.L.binop == B_COPY && !b.L.rhs.base) || (b.L.binop == B_MUL && rw == 1));
+                      ((b.L.binop == B_COPY && !b.L.rhs.base) ||
+                       (b.L.binop == B_MUL && (rw == 1 || (wide_heads && rw > 1))));
     p.seg_sw = wide ? W : W <= 256 ? W : 256;
     p.seg_slices = static_cast<uint32_t>((W + p.seg_sw - 1) / p.seg_sw);
     static const uint32_t tma_min = env_u32("GSPMM_TMA_MIN_BYTES", 512);

@@ -1561,6 +1561,7 @@ cudaError_t launch_wide(const StreamLaunch& p, cudaStream_t s) {
     if (p.row.other_scale) return launch_k<5, BOP, R_SUM, 0, SK_SCALE, true>(p, s);
     return launch_k<5, BOP, R_SUM, 0, SK_NONE, true>(p, s);
   } else if constexpr (BOP == B_MUL) {
+    if (p.rhs_width > 1) return launch_k<5, BOP, R_SUM, 0, SK_HEAD, true>(p, s);
     return launch_k<5, BOP, R_SUM, 0, SK_WIN, true>(p, s);
   } else {
     return cudaErrorNotSupported;
