@@ -55,6 +55,16 @@ constexpr int kThreads = 256;
 #ifndef GATHER_U5
 #define GATHER_U5 2
 #endif
+// Cache policy of the segment kernel's streams (read or written once per
+// pass): evict-first stores of the output rows / loads of the id windows.
+// Measured on the cfg2 bench step: evict-first output stores 3.79 -> 3.86 ms
+// (off); evict-first id loads 3.79 -> 3.79 (on, neutral).
+#ifndef GATHER_STREAM_OUT
+#define GATHER_STREAM_OUT 0
+#endif
+#ifndef GATHER_STREAM_IN
+#define GATHER_STREAM_IN 1
+#endif
 // L2 prefetch distance of the segment kernel, in batches (0 = off).
 // Measured slower at every distance (cfg2 1.82 -> 1.89 / 1.91 / 2.01 ms at
 // 2 / 4 / 8 batches; uniform er256 2.41 -> 3.96 ms at 8): kept for study.
@@ -171,7 +181,13 @@ struct Acc {
     }
     float* orow = L.out + static_cast<int64_t>(r) * L.out_ld + c0;
     if (c + 4 <= cw) {
+#if GATHER_STREAM_OUT
+      // written once, never re-read by the pass: evict-first, so the output
+      // stream does not displace hot source rows from L2
+      __stcs(reinterpret_cast<float4*>(orow + c), make_float4(o[0], o[1], o[2], o[3]));
+#else
       store_vec<4>(orow + c, o);
+#endif
     } else {
 #pragma unroll
       for (int t = 0; t < 4; ++t)
@@ -252,8 +268,13 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
   auto load_win = [&](uint32_t w, uint32_t& o, uint32_t& e, float& rv) {
     const uint32_t j = u.e0 + 32u * w + lane;
     if (j < u.e1) {
+#if GATHER_STREAM_IN
+      o = __ldcs(indices + j);  // read once: evict-first
+      if (need_eid) e = __ldcs(eids + j);
+#else
       o = __ldg(indices + j);
       if (need_eid) e = __ldg(eids + j);
+#endif
       if constexpr (SK == SK_WIN || SK == SK_SCALE) {
         const uint32_t row = srole == ROLE_POS ? j : srole == ROLE_EID ? e : o;
         rv = __ldg(sbase + static_cast<int64_t>(row) * sld);
