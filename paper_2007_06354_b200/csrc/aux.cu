@@ -44,6 +44,41 @@ __global__ void k_argmax_scatter(const int32_t* __restrict__ arg, int64_t rows,
   }
 }
 
+// Vector forms for dim % 4 == 0 with 16-byte aligned rows: a thread owns
+// four consecutive columns (one LDG.128 of the argmax ids and one of the
+// gradient, four f64 atomics), and the row index comes from a 32-bit
+// division once per four elements instead of a 64-bit one per element.
+__global__ void k_argmax_scatter4(const int32_t* __restrict__ arg, uint32_t rows, uint32_t quads,
+                                  int64_t arg_ld, const float* __restrict__ grad,
+                                  int64_t grad_ld, double* __restrict__ acc, int64_t dim) {
+  const uint32_t total = rows * quads;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const uint32_t r = i / quads, q = i - r * quads;
+    const int4 a = __ldg(reinterpret_cast<const int4*>(arg + r * arg_ld) + q);
+    const float4 g = __ldg(reinterpret_cast<const float4*>(grad + r * grad_ld) + q);
+    const int64_t c = static_cast<int64_t>(q) * 4;
+    if (a.x >= 0) atomicAdd(acc + static_cast<int64_t>(a.x) * dim + c, static_cast<double>(g.x));
+    if (a.y >= 0) atomicAdd(acc + static_cast<int64_t>(a.y) * dim + c + 1, static_cast<double>(g.y));
+    if (a.z >= 0) atomicAdd(acc + static_cast<int64_t>(a.z) * dim + c + 2, static_cast<double>(g.z));
+    if (a.w >= 0) atomicAdd(acc + static_cast<int64_t>(a.w) * dim + c + 3, static_cast<double>(g.w));
+  }
+}
+
+__global__ void k_round_f64x4(const double* __restrict__ acc, uint32_t rows, uint32_t quads,
+                              float* __restrict__ out, int64_t ld) {
+  const uint32_t total = rows * quads;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const uint32_t r = i / quads, q = i - r * quads;
+    const double2 lo = __ldg(reinterpret_cast<const double2*>(acc) + 2 * static_cast<uint64_t>(i));
+    const double2 hi = __ldg(reinterpret_cast<const double2*>(acc) + 2 * static_cast<uint64_t>(i) + 1);
+    reinterpret_cast<float4*>(out + r * ld)[q] =
+        make_float4(__double2float_rn(lo.x), __double2float_rn(lo.y), __double2float_rn(hi.x),
+                    __double2float_rn(hi.y));
+  }
+}
+
 __global__ void k_round_f64(const double* __restrict__ acc, int64_t rows,
                             int64_t dim, float* __restrict__ out, int64_t ld) {
   const int64_t total = rows * dim;
@@ -105,6 +140,26 @@ cudaError_t launch_argmax_backward(const int32_t* arg, int64_t rows,
                                    cudaStream_t s) {
   cudaError_t err = cudaMemsetAsync(acc, 0, sizeof(double) * src_rows * dim, s);
   if (err != cudaSuccess) return err;
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+  const bool vec = dim % 4 == 0 && arg_ld % 4 == 0 && grad_ld % 4 == 0 && src_ld % 4 == 0 &&
+                   al16(arg) && al16(grad_out) && al16(grad_src) &&
+                   rows * (dim / 4) < (int64_t{1} << 32) - (int64_t{1} << 24) &&
+                   src_rows * (dim / 4) < (int64_t{1} << 32) - (int64_t{1} << 24);
+  if (vec) {
+    const int64_t quads = dim / 4;
+    if (rows * quads > 0) {
+      k_argmax_scatter4<<<grid_for(rows * quads, 256), 256, 0, s>>>(
+          arg, static_cast<uint32_t>(rows), static_cast<uint32_t>(quads), arg_ld, grad_out,
+          grad_ld, acc, dim);
+      note_launch();
+    }
+    if (src_rows * quads > 0) {
+      k_round_f64x4<<<grid_for(src_rows * quads, 256), 256, 0, s>>>(
+          acc, static_cast<uint32_t>(src_rows), static_cast<uint32_t>(quads), grad_src, src_ld);
+      note_launch();
+    }
+    return cudaGetLastError();
+  }
   if (rows * dim > 0) {
     k_argmax_scatter<<<grid_for(rows * dim, 256), 256, 0, s>>>(arg, rows, dim, arg_ld,
                                                                grad_out, grad_ld, acc);

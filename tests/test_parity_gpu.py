@@ -584,3 +584,25 @@ def test_wide_rows_mean_and_mean_backward():
     P.binary_reduce(hs, (O.V, O.NONE, O.COPY, O.SUM, O.U), v=gp[:, :602], out=op[:, :602],
                     other_scale=torch.from_numpy(inv).cuda())
     assert O.bit_equal(op[:, :602].cpu().numpy(), O.mean_backward(g, gy))
+
+
+@pytest.mark.parametrize("dim,pad", [(100, 0), (128, 4), (37, 0), (64, 2)])
+def test_argmax_backward_vector_and_scalar_paths(dim, pad):
+    """a17.4 scatter through the argmax: dim % 4 == 0 with 16-byte rows takes
+    the 4-column kernels, other widths / padded leading dims the scalar ones;
+    -1 ids (rows without in-edges) contribute nothing."""
+    rng = np.random.default_rng(dim + pad)
+    rows, src_rows = 5000, 1200
+    arg = rng.integers(-1, src_rows, size=(rows, dim), dtype=np.int32)
+    arg[::7] = -1
+    gy = O.normal_features(rows, dim, dim)
+    want = O.argmax_backward(arg, gy, src_rows)
+    a_full = torch.zeros((rows, dim + pad), dtype=torch.int32, device="cuda")
+    g_full = torch.zeros((rows, dim + pad), dtype=torch.float32, device="cuda")
+    a_full[:, :dim] = torch.from_numpy(arg).cuda()
+    g_full[:, :dim] = cuda(gy)
+    o_full = torch.full((src_rows, dim + pad), 7.0, dtype=torch.float32, device="cuda")
+    got = P.argmax_backward(a_full[:, :dim], g_full[:, :dim], src_rows, out=o_full[:, :dim])
+    assert O.max_rel_error(got.cpu().numpy(), want) <= 1e-6
+    if pad:
+        assert (o_full[:, dim:] == 7.0).all()
