@@ -30,9 +30,17 @@
  *
  * Device entry points take DEVICE pointers and enqueue on `stream`
  * (cudaStream_t, NULL = legacy default stream); they return after launch.
- * Host entry points (`*_host`) take HOST pointers, stage through the
- * handle's device workspace and return after the result is back on the
- * host, like the reference's synchronous call.
+ * Host entry points (`*_host`) take HOST pointers, stage through a
+ * stream-ordered device allocation and return after the result is back on
+ * the host, like the reference's synchronous call.
+ *
+ * Thread safety (the reference's CsrGraph is safe to share, csr.hpp:35): a
+ * graph handle may be used by any number of host threads and streams at
+ * once.  Each caller stream gets its own per-call device state (work
+ * counters, workspaces) and every call waits for the previous call that used
+ * the same state, so concurrent calls never share a counter or a buffer.
+ * Destroying a handle, gspmm_graph_set_plan and gspmm_graph_set_source_blocks
+ * must not race with calls on that handle.
  *
  * Semantics (identical to the reference, bit for bit):
  *   - each output element is a sequential fp32 left fold, from the reduce
@@ -55,7 +63,7 @@
 extern "C" {
 #endif
 
-#define GSPMM_B200_ABI_VERSION 1
+#define GSPMM_B200_ABI_VERSION 2
 
 /* ---- status (error.hpp:22-45 taxonomy, plus device failures) ---- */
 enum {
@@ -121,11 +129,28 @@ typedef struct {
   int32_t heads;
   /* Per-node scale of each edge's OTHER endpoint (the gathered node):
    * message := message * other_scale[other], rounded (used for the mean
-   * backward: e = 1/deg_in(dst)). Device pointer, length = #other nodes. */
+   * backward: e = 1/deg_in(dst)). Device pointer (host pointer in the
+   * *_host entries), length = #other nodes. */
   const float* other_scale;
+  /* Source blocking for this call (see gspmm_graph_set_source_blocks):
+   * 0 = the handle's setting, 1 = never, >= 2 = that many blocks. */
+  int32_t source_blocks;
 } gspmm_options;
 
 typedef struct gspmm_graph_s* gspmm_graph;
+
+/* Device plan options (gspmm_graph_set_plan).  Zero-init = the defaults.
+ * The plan only changes how work is cut into units, never a result: every
+ * output stays the canonical left fold. */
+typedef struct {
+  uint32_t seg_cost;       /* cost (edges + 2 per row) of a segment unit; 0 -> 256 */
+  uint32_t long_threshold; /* 0 -> automatic plan levels; else rows above this
+                              degree always run as long-row column units */
+  uint32_t unit_cols;      /* 0 -> automatic long-row unit widths; else this
+                              many columns per unit (multiple of 4, <= 512) */
+  int32_t kernel;          /* 0 = planned kernels; 1 = the register kernel
+                              (rows.cu) for every call (a reference path) */
+} gspmm_plan;
 
 /* ---- errors ---- */
 const char* gspmm_last_error(void); /* thread-local message of the last failure */
@@ -182,6 +207,8 @@ int gspmm_graph_permute_edges(gspmm_graph g, const float* src_by_id,
  * gathered lhs, no CSR-position edge operand).  Block CSRs are built on the
  * device on first use. */
 int gspmm_graph_set_source_blocks(gspmm_graph g, int nblocks);
+/* Rebuilds the handle's device plan with the given options (NULL: defaults). */
+int gspmm_graph_set_plan(gspmm_graph g, const gspmm_plan* plan);
 
 /* ---- compute (device pointers, asynchronous on stream) ---- */
 int gspmm_binary_reduce(gspmm_graph g, const gspmm_config* cfg,
@@ -203,6 +230,23 @@ int gspmm_argmax_backward(const int32_t* arg, int64_t rows, int64_t dim,
                           int64_t arg_ld, const float* grad_out,
                           int64_t grad_ld, float* grad_src, int64_t src_rows,
                           int64_t src_ld, void* stream);
+/* The same for the source rows [src_lo, src_lo + src_rows) only (grad_src
+ * row i is source row src_lo + i; other targets are skipped): a rank's own
+ * rows in the multi-GPU owner-computes backward. */
+int gspmm_argmax_backward_range(const int32_t* arg, int64_t rows, int64_t dim,
+                                int64_t arg_ld, const float* grad_out,
+                                int64_t grad_ld, float* grad_src, int64_t src_lo,
+                                int64_t src_rows, int64_t src_ld, void* stream);
+/* Host-buffer forms (dense rows): arg / grad_out uploaded, grad_src read
+ * back; on `device`.  _async: enqueue only, with the wait / upload events of
+ * gspmm_binary_reduce_host_async. */
+int gspmm_argmax_backward_host(const int32_t* arg, int64_t rows, int64_t dim,
+                               const float* grad_out, float* grad_src,
+                               int64_t src_rows, int device, void* stream);
+int gspmm_argmax_backward_host_async(const int32_t* arg, int64_t rows, int64_t dim,
+                                     const float* grad_out, float* grad_src,
+                                     int64_t src_rows, int device, void* stream,
+                                     void* wait_event, void* upload_event);
 
 /* Fused GAT edge softmax over the in-edges of each destination (
  * the composite e_copy_max_v -> e_sub_v_copy_e -> exp -> e_copy_add_v ->
@@ -234,8 +278,9 @@ int gspmm_binary_reduce_host(gspmm_graph g, const gspmm_config* cfg,
  * NULL) is recorded once the inputs are on the device: callers that stream
  * several independent calls on two streams use the pair to keep one upload
  * in flight at a time while the other call's kernel and download run, so
- * both PCIe directions stay busy.  Calls on one handle must use one stream
- * (the handle's device workspace is reused in stream order). */
+ * both PCIe directions stay busy.  In the host entries, options.other_scale
+ * is a HOST array (one float per node of the gathered endpoint, num_cols of
+ * the handle) uploaded with the operands. */
 int gspmm_binary_reduce_host_async(gspmm_graph g, const gspmm_config* cfg,
                                    const gspmm_mat* u, const gspmm_mat* v,
                                    const gspmm_mat* e, const gspmm_out* out,

@@ -100,8 +100,10 @@ struct FeatureMatrix {
 struct BlockPlan {
   NodeId kb = 0;
   std::int64_t nb = 0;
+  Orientation built_for = Orientation::DstMajor;  // checked like kernels.cpp:462-467
   NodeId num_rows = 0, num_cols = 0;
   NodeId num_blocks = 0;
+  EdgeId num_edges = 0;
 };
 // build_block_plan (block_plan.cpp:25-69): kb, nb >= 1.
 BlockPlan build_block_plan(const CsrGraph& g, NodeId kb, std::int64_t nb);

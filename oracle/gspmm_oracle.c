@@ -9,6 +9,7 @@
 #include "gspmm_oracle.h"
 
 #include <math.h>
+#include <omp.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -734,6 +735,69 @@ void or_argmax_backward(int64_t rows, int64_t w, const int32_t* arg,
       if (a >= 0) acc[(int64_t)a * w + i] += (double)grad_out[r * w + i];
     }
   for (int64_t i = 0; i < src_rows * w; ++i) grad_src[i] = (float)acc[i];
+  free(acc);
+}
+
+/* a17.2 / a17.4 at BASELINE size: the same arithmetic, threaded (see the
+ * header).  Edge-outer loop per row: column i's comparisons still happen in
+ * canonical edge order, so the winner is the serial loop's winner. */
+int or_copy_max_argmax_mt(uint32_t num_rows, uint32_t num_cols,
+                          const uint32_t* indptr, const uint32_t* indices,
+                          const uint32_t* eids, int lhs, const or_feat* src,
+                          float* out, int32_t* arg_other, int32_t* arg_eid,
+                          int threads) {
+  (void)num_cols;
+  const int64_t w = src->dim;
+  if (threads <= 0) threads = omp_get_max_threads();
+#pragma omp parallel num_threads(threads)
+  {
+    int64_t* arg = (int64_t*)malloc((size_t)(w ? w : 1) * sizeof(int64_t));
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t r = 0; r < (int64_t)num_rows; ++r) {
+      float* best = out + r * w;
+      for (int64_t i = 0; i < w; ++i) {
+        best[i] = -INFINITY;
+        arg[i] = -1;
+      }
+      for (uint32_t j = indptr[r]; j < indptr[r + 1]; ++j) {
+        const int64_t row = lhs == OR_E ? eids[j] : indices[j];
+        const float* x = src->data + row * w;
+        for (int64_t i = 0; i < w; ++i)
+          if (best[i] < x[i]) {
+            best[i] = x[i];
+            arg[i] = j;
+          }
+      }
+      const int empty = indptr[r] == indptr[r + 1];
+      for (int64_t i = 0; i < w; ++i) {
+        if (empty) best[i] = 0.0f;
+        if (arg_other) arg_other[r * w + i] = arg[i] < 0 ? -1 : (int32_t)indices[arg[i]];
+        if (arg_eid) arg_eid[r * w + i] = arg[i] < 0 ? -1 : (int32_t)eids[arg[i]];
+      }
+    }
+    free(arg);
+  }
+  return OR_OK;
+}
+
+void or_argmax_backward_mt(int64_t rows, int64_t w, const int32_t* arg,
+                           const float* grad_out, int64_t src_rows,
+                           float* grad_src, int threads) {
+  if (threads <= 0) threads = omp_get_max_threads();
+  double* acc = (double*)calloc((size_t)(src_rows * w ? src_rows * w : 1), sizeof(double));
+#pragma omp parallel num_threads(threads)
+  {
+    const int64_t t = omp_get_thread_num(), nt = omp_get_num_threads();
+    const int64_t lo = src_rows * t / nt, hi = src_rows * (t + 1) / nt;
+    for (int64_t r = 0; r < rows; ++r)
+      for (int64_t i = 0; i < w; ++i) {
+        const int32_t a = arg[r * w + i];
+        if (a >= lo && a < hi) acc[(int64_t)a * w + i] += (double)grad_out[r * w + i];
+      }
+#pragma omp barrier
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < src_rows * w; ++i) grad_src[i] = (float)acc[i];
+  }
   free(acc);
 }
 

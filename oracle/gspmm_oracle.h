@@ -113,6 +113,23 @@ void or_argmax_backward(int64_t rows, int64_t w, const int32_t* arg,
                         const float* grad_out, int64_t src_rows,
                         float* grad_src);
 
+/* Multithreaded forms of the two a17 extensions for BASELINE-size parity
+ * (OpenMP, `threads` <= 0: all).  Same results as the single-threaded
+ * restatements: or_copy_max_argmax_mt splits rows over threads and walks
+ * each row's edges in canonical order, updating every column (each column
+ * still sees the edges in order, so the first strict maximum wins);
+ * or_argmax_backward_mt gives each thread a contiguous range of source rows
+ * and scans all (row, column) pairs in order, so every accumulator receives
+ * its terms in ascending row order, exactly as the serial loop. */
+int or_copy_max_argmax_mt(uint32_t num_rows, uint32_t num_cols,
+                          const uint32_t* indptr, const uint32_t* indices,
+                          const uint32_t* eids, int lhs, const or_feat* src,
+                          float* out, int32_t* arg_other, int32_t* arg_eid,
+                          int threads);
+void or_argmax_backward_mt(int64_t rows, int64_t w, const int32_t* arg,
+                           const float* grad_out, int64_t src_rows,
+                           float* grad_src, int threads);
+
 /* ---- comparison (compare.hpp:30-54) ---- */
 double or_max_rel_error(int64_t n, const float* got, const float* want);
 int or_bit_equal(int64_t n, const float* a, const float* b);

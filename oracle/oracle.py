@@ -90,6 +90,8 @@ def _load_c():
         "or_mean": (i32, [i32, u32, u32, vp, vp, vp, i32, fp, vp]),
         "or_copy_max_argmax": (i32, [u32, u32, vp, vp, vp, i32, fp, vp, vp, vp]),
         "or_argmax_backward": (None, [i64, i64, vp, vp, i64, vp]),
+        "or_copy_max_argmax_mt": (i32, [u32, u32, vp, vp, vp, i32, fp, vp, vp, vp, i32]),
+        "or_argmax_backward_mt": (None, [i64, i64, vp, vp, i64, vp, i32]),
         "or_max_rel_error": (dbl, [i64, vp, vp]),
         "or_bit_equal": (i32, [i64, vp, vp]),
     }
@@ -124,6 +126,10 @@ def _load_ref():
         "ref_feat_create": (vp, [i64, i64, vp]),
         "ref_feat_free": (None, [vp]),
         "ref_run": (dbl, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, i32, vp]),
+        "ref_graph_create": (vp, [i32, u32, u32, vp, vp, vp]),
+        "ref_graph_free": (None, [vp]),
+        "ref_feat_create_strided": (vp, [i64, i64, vp, i64]),
+        "ref_run_graph": (dbl, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, i32, vp, i64]),
         "ref_bench_case": (dbl, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, i32, i32, i32,
                                  C.POINTER(dbl), C.POINTER(dbl)]),
     }
@@ -373,6 +379,30 @@ def copy_max_argmax(g, src_feats, lhs=U):
     return out, arg_u, arg_e
 
 
+def copy_max_argmax_csr(csr, num_rows, num_cols, src_feats, lhs=U, threads=0):
+    """a17.2 on a given dst-major CSR, threaded (BASELINE sizes): identical to
+    copy_max_argmax (or_copy_max_argmax_mt)."""
+    indptr, indices, eids = (np.ascontiguousarray(a, np.uint32) for a in csr)
+    f = _feat(src_feats)
+    out = np.empty((num_rows, f.dim), np.float32)
+    arg_u = np.empty((num_rows, f.dim), np.int32)
+    arg_e = np.empty((num_rows, f.dim), np.int32)
+    _check(LIB.or_copy_max_argmax_mt(num_rows, num_cols, _ptr(indptr), _ptr(indices),
+                                     _ptr(eids), lhs, f, out.ctypes.data, arg_u.ctypes.data,
+                                     arg_e.ctypes.data, threads))
+    return out, arg_u, arg_e
+
+
+def argmax_backward_mt(arg, grad_out, src_rows, threads=0):
+    """a17.4, threaded over source-row ranges (same per-entry order)."""
+    arg = np.ascontiguousarray(arg, np.int32)
+    grad_out = np.ascontiguousarray(grad_out, np.float32)
+    out = np.empty((src_rows, arg.shape[1]), np.float32)
+    LIB.or_argmax_backward_mt(arg.shape[0], arg.shape[1], arg.ctypes.data,
+                              grad_out.ctypes.data, src_rows, out.ctypes.data, threads)
+    return out
+
+
 def argmax_backward(arg, grad_out, src_rows):
     """a17.4: scatter grad_out through the argmax, f64 accumulation."""
     arg = np.ascontiguousarray(arg, np.int32)
@@ -573,3 +603,67 @@ def ref_oracle_aggregate(g, cfg, u=None, v=None, e=None):
     _check(REF.ref_oracle_aggregate(g.n, g.m, _ptr(g.src), _ptr(g.dst), *cfg, fu, fv, fe,
                                     out.ctypes.data, C.byref(r), C.byref(d)))
     return out
+
+
+class RefGraph:
+    """The reference library (oracle/_ref) on a canonical CSR handed in
+    directly: binary_reduce(strategy, ...) with all host threads, for
+    whole-output parity at the BASELINE sizes.  run() returns the output;
+    run_timed() also the reference's own steady_clock seconds."""
+
+    def __init__(self, orientation, num_rows, num_cols, indptr, indices, eids):
+        if REF is None:
+            raise OSError("oracle/_ref/libgspmm_ref.so not built")
+        self._keep = [np.ascontiguousarray(a, np.uint32) for a in (indptr, indices, eids)]
+        self.orientation, self.num_rows, self.num_cols = orientation, num_rows, num_cols
+        self.h = REF.ref_graph_create(orientation, num_rows, num_cols,
+                                      *(a.ctypes.data for a in self._keep))
+        if not self.h:
+            raise OracleError(9, "ref_graph_create")
+
+    @staticmethod
+    def feat(a):
+        """FeatureMatrix from a 2-D float32 array (a column slice is fine)."""
+        if a is None:
+            return None
+        a = np.asarray(a, np.float32)
+        if a.ndim == 1:
+            a = a.reshape(-1, 1)
+        if a.strides[1] != 4:
+            a = np.ascontiguousarray(a)
+        return REF.ref_feat_create_strided(a.shape[0], a.shape[1], a.ctypes.data,
+                                           a.strides[0] // 4)
+
+    def run_timed(self, cfg, u=None, v=None, e=None, strategy=SPMM, threads=0, out=None):
+        fs = [self.feat(x) for x in (u, v, e)]
+        try:
+            if out is None:
+                rows = self.num_rows if cfg[4] != E else int(self._keep[0][-1])
+                w = (1 if cfg[2] == DOT else
+                     max(x.shape[1] if x.ndim > 1 else 1 for x in (u, v, e) if x is not None)
+                     if cfg[2] != COPY else (u if cfg[0] == U else v if cfg[0] == V else e).shape[1])
+                out = np.empty((rows, w), np.float32)
+            assert out.strides[1] == 4
+            t = REF.ref_run_graph(self.h, strategy, *cfg, *fs, threads, out.ctypes.data,
+                                  out.strides[0] // 4)
+            if t < 0:
+                raise OracleError(int(-t), "ref_run_graph")
+            return out, t
+        finally:
+            for f in fs:
+                if f:
+                    REF.ref_feat_free(f)
+
+    def run(self, cfg, u=None, v=None, e=None, strategy=SPMM, threads=0, out=None):
+        return self.run_timed(cfg, u, v, e, strategy, threads, out)[0]
+
+    def close(self):
+        if self.h:
+            REF.ref_graph_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -308,4 +308,65 @@ double ref_bench_case(void* views, int strategy, int lhs, int rhs, int binop,
   }
 }
 
+// ---- canonical CSR handed in directly (BASELINE-size parity) -------------
+
+// A CsrGraph holding the given canonical CSR (csr.hpp:37-54).  The tests pass
+// the CSR the product's builder made, which test_abi / test_oracle_pins check
+// against build_csr; this skips the reference's single-threaded build
+// (~25 s per orientation at config-3 size).
+void* ref_graph_create(int orientation, uint32_t num_rows, uint32_t num_cols,
+                       const uint32_t* indptr, const uint32_t* indices,
+                       const uint32_t* eids) {
+  try {
+    return new CsrGraph(make_graph(orientation, num_rows, num_cols, indptr, indices, eids));
+  } catch (...) {
+    return nullptr;
+  }
+}
+void ref_graph_free(void* g) { delete static_cast<CsrGraph*>(g); }
+
+// A FeatureMatrix copied from a strided source (ld >= dim floats per row):
+// per-head column slices without a host-side copy first.
+void* ref_feat_create_strided(int64_t rows, int64_t dim, const float* data, int64_t ld) {
+  auto* f = new FeatureMatrix(rows, dim);
+  for (int64_t r = 0; r < rows; ++r)
+    std::memcpy(f->data.data() + r * dim, data + r * ld, dim * sizeof(float));
+  return f;
+}
+
+// binary_reduce(strategy, g, cfg, u, v, e, nullptr, threads) on a graph from
+// ref_graph_create, timed like ref_run; the result (rows x dim) is copied to
+// out with row pitch out_ld (0: dense) outside the timing.  BlockedPull builds
+// its plan with the reference defaults before the clock starts.
+double ref_run_graph(void* graph, int strategy, int lhs, int rhs, int binop, int reduce,
+                     int out_ent, void* u, void* v, void* e, int threads, float* out,
+                     int64_t out_ld) {
+  try {
+    const CsrGraph& g = *static_cast<CsrGraph*>(graph);
+    const BrConfig cfg = make_cfg(lhs, rhs, binop, reduce, out_ent);
+    const Strategy s = static_cast<Strategy>(strategy);
+    const auto* fu = static_cast<FeatureMatrix*>(u);
+    const auto* fe = static_cast<FeatureMatrix*>(e);
+    BlockPlan plan;
+    if (s == Strategy::BlockedPull) {
+      const int64_t dim = fu ? fu->dim : (fe ? fe->dim : 4);
+      plan = build_block_plan(g, default_kb(dim, g.num_cols), default_nb(g.num_rows, dim));
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    const FeatureMatrix res = binary_reduce(
+        s, g, cfg, fu, static_cast<FeatureMatrix*>(v), fe,
+        s == Strategy::BlockedPull ? &plan : nullptr, threads);
+    const double dt =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (out) {
+      const int64_t ld = out_ld ? out_ld : res.dim;
+      for (int64_t r = 0; r < res.rows; ++r)
+        std::memcpy(out + r * ld, res.data.data() + r * res.dim, res.dim * sizeof(float));
+    }
+    return dt;
+  } catch (...) {
+    return -static_cast<double>(status_of(std::current_exception()));
+  }
+}
+
 }  // extern "C"

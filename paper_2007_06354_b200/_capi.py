@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("GSPMM_LIB_PATH") or os.path.join(_HERE, "_lib", "libgspmm_b200.so")
+LIB_PATH = os.path.join(_HERE, "_lib", "libgspmm_b200.so")
 
 # status codes
 OK, ERR_CONFIG, ERR_SHAPE, ERR_STRUCTURE, ERR_CUDA, ERR_ARG = 0, 1, 2, 3, 4, 5
@@ -69,9 +69,14 @@ class Out(C.Structure):
                 ("ld", C.c_int64)]
 
 
+class Plan(C.Structure):
+    _fields_ = [("seg_cost", C.c_uint32), ("long_threshold", C.c_uint32),
+                ("unit_cols", C.c_uint32), ("kernel", C.c_int32)]
+
+
 class Options(C.Structure):
     _fields_ = [("arg_other", C.c_void_p), ("arg_edge", C.c_void_p), ("arg_ld", C.c_int64),
-                ("heads", C.c_int32), ("other_scale", C.c_void_p)]
+                ("heads", C.c_int32), ("other_scale", C.c_void_p), ("source_blocks", C.c_int32)]
 
 
 # Every symbol include/gspmm_b200.h declares, with its prototype.
@@ -90,11 +95,17 @@ SIGNATURES = {
     "gspmm_graph_device_csr": (_i32, [_vp, _P(_vp), _P(_vp), _P(_vp)]),
     "gspmm_graph_permute_edges": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "gspmm_graph_set_source_blocks": (_i32, [_vp, _i32]),
+    "gspmm_graph_set_plan": (_i32, [_vp, _P(Plan)]),
     "gspmm_binary_reduce": (_i32, [_vp, _P(Config), _P(Mat), _P(Mat), _P(Mat), _P(Out), _vp]),
     "gspmm_binary_reduce_ex": (_i32, [_vp, _P(Config), _P(Mat), _P(Mat), _P(Mat), _P(Out),
                                       _P(Options), _vp]),
     "gspmm_copy_reduce": (_i32, [_vp, _P(Mat), _i32, _P(Out), _vp]),
     "gspmm_argmax_backward": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
+    "gspmm_argmax_backward_range": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i64,
+                                           _i64, _vp]),
+    "gspmm_argmax_backward_host": (_i32, [_vp, _i64, _i64, _vp, _vp, _i64, _i32, _vp]),
+    "gspmm_argmax_backward_host_async": (_i32, [_vp, _i64, _i64, _vp, _vp, _i64, _i32, _vp,
+                                                _vp, _vp]),
     "gspmm_edge_softmax": (_i32, [_vp, _P(Mat), _P(Out), _vp]),
     "gspmm_edge_softmax_backward": (_i32, [_vp, _P(Mat), _P(Mat), _P(Out), _vp]),
     "gspmm_binary_reduce_host": (_i32, [_vp, _P(Config), _P(Mat), _P(Mat), _P(Mat), _P(Out),
@@ -126,8 +137,6 @@ def _load():
             "there is no CPU fallback")
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
-        if os.environ.get("GSPMM_LIB_PATH") and not hasattr(lib, name):
-            continue  # an older library under A/B comparison (development aid)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -18,7 +18,7 @@ from ._capi import (ADD, COPY, COPY_LAST, DIV, DOT, DST_MAJOR, E, EDGE_BY_ID, ED
 
 __all__ = [
     "Graph", "binary_reduce", "binary_reduce_host", "binary_reduce_host_async", "copy_reduce",
-    "argmax_backward",
+    "argmax_backward", "argmax_backward_host", "argmax_backward_host_async",
     "named_config", "validate_config", "required_orientation", "out_shape",
     "synth_rmat", "synth_er", "build_csr", "transpose", "synth_uniform", "synth_normal",
     "synth_gcn_weights", "synth_powerlaw", "launch_count", "edge_softmax", "edge_softmax_backward",
@@ -147,6 +147,18 @@ class Graph:
         check(A.LIB.gspmm_graph_set_source_blocks(self.handle, int(nblocks)), "set_source_blocks")
         return self
 
+    def set_plan(self, seg_cost=0, long_threshold=0, unit_cols=0, kernel=0):
+        """Rebuild the device plan (gspmm_graph_set_plan): segment-unit cost,
+        a fixed long-row threshold, a fixed long-row unit width (multiple of
+        4, <= 512) and kernel=1 for the register kernel on every call.  0 =
+        the default of each.  Results never depend on the plan."""
+        p = A.Plan(seg_cost, long_threshold, unit_cols, kernel)
+        check(A.LIB.gspmm_graph_set_plan(self.handle, C.byref(p)), "set_plan")
+        nl = C.c_uint32()
+        check(A.LIB.gspmm_graph_info(self.handle, None, None, None, None, C.byref(nl)))
+        self.num_long_rows = nl.value
+        return self
+
     def permute_edges(self, e, stream=None):
         """Edge operand in edge-id order -> this handle's CSR position order
         (device, untimed setup like the reference's BlockPlan)."""
@@ -179,6 +191,11 @@ def _dev_mat(t, edge_order=EDGE_BY_ID):
     t2 = t.reshape(t.shape[0], -1) if t.dim() != 2 else t
     if t2.shape[1] > 1 and t2.stride(1) != 1:
         raise A.ShapeError("operand rows must be contiguous")
+    if t2.shape[0] > 1 and t2.stride(0) < t2.shape[1]:
+        # an expanded / overlapping view (e.g. bias.expand(n, d), stride 0)
+        # would be read as n distinct rows
+        raise A.ShapeError("operand rows must not overlap (expanded views are not supported; "
+                           "pass a width-1 operand to broadcast, or materialise it)")
     ld = t2.stride(0) if t2.shape[0] > 1 else t2.shape[1]
     m = A.Mat(t2.data_ptr(), t2.shape[0], t2.shape[1], ld, edge_order)
     m._keep = t2
@@ -221,13 +238,26 @@ def out_shape(graph, cfg, u=None, v=None, e=None, heads=1, host=False):
 
 
 # ----------------------------------------------------------------- compute
+def _check_out(t, rows, dim, dtype, dev, what):
+    import torch
+    if t.dtype != dtype or not t.is_cuda or t.device != dev:
+        raise A.ShapeError(f"{what} must be a {dtype} tensor on {dev}")
+    t2 = t if t.dim() == 2 else t.reshape(rows, -1)
+    if tuple(t2.shape) != (rows, dim) or (dim > 1 and t2.stride(1) != 1) or \
+            (rows > 1 and t2.stride(0) < dim):
+        raise A.ShapeError(f"{what} must be a row-major {rows} x {dim} view "
+                           f"(got shape {tuple(t.shape)}, strides {tuple(t.stride())})")
+    return t2
+
+
 def binary_reduce(graph, cfg, u=None, v=None, e=None, *, out=None, e_order=EDGE_BY_ID,
                   want_arg_other=False, want_arg_edge=False, heads=1, other_scale=None,
-                  stream=None):
+                  arg_other_out=None, arg_edge_out=None, stream=None):
     """binary_reduce (kernels.hpp:60-64) on device tensors.
 
     Returns ``out`` (allocated when not given) or ``(out, arg_other,
-    arg_edge)`` when an argmax output is requested."""
+    arg_edge)`` when an argmax output is requested (``arg_*_out``: caller
+    buffers for them)."""
     import torch
     cfg = as_config(cfg)
     mu, mv, me = _dev_mat(u), _dev_mat(v), _dev_mat(e, e_order)
@@ -237,9 +267,24 @@ def binary_reduce(graph, cfg, u=None, v=None, e=None, *, out=None, e_order=EDGE_
     dev = ref_t.device if ref_t is not None else torch.device("cuda", graph.device)
     if out is None:
         out = torch.empty((rows, dim), dtype=torch.float32, device=dev)
-    mo = A.Out(out.data_ptr(), rows, dim, out.stride(0) if out.dim() == 2 else dim)
-    ao = torch.empty((rows, dim), dtype=torch.int32, device=dev) if want_arg_other else None
-    ae = torch.empty((rows, dim), dtype=torch.int32, device=dev) if want_arg_edge else None
+    o2 = _check_out(out, rows, dim, torch.float32, dev, "out")
+    mo = A.Out(o2.data_ptr(), rows, dim, o2.stride(0) if rows > 1 else dim)
+    want_arg_other = want_arg_other or arg_other_out is not None
+    want_arg_edge = want_arg_edge or arg_edge_out is not None
+    ao, ae = arg_other_out, arg_edge_out
+    if want_arg_other and ao is None:
+        ao = torch.empty((rows, dim), dtype=torch.int32, device=dev)
+    if want_arg_edge and ae is None:
+        ae = torch.empty((rows, dim), dtype=torch.int32, device=dev)
+    for t, what in ((ao, "arg_other"), (ae, "arg_edge")):
+        if t is not None and (not t.is_contiguous() or
+                              _check_out(t, rows, dim, torch.int32, dev, what) is None):
+            raise A.ShapeError(f"{what} must be a contiguous int32 {rows} x {dim} tensor")
+    if other_scale is not None:
+        if other_scale.dtype != torch.float32 or other_scale.device != dev or \
+                not other_scale.is_contiguous():
+            raise A.ShapeError("other_scale must be a contiguous float32 tensor on the "
+                               "operands' device")
     opts = _opts(heads, ao.data_ptr() if ao is not None else None,
                  ae.data_ptr() if ae is not None else None,
                  other_scale.data_ptr() if other_scale is not None else None)
@@ -264,16 +309,54 @@ def copy_reduce(graph, src, reduce, *, out=None, stream=None):
     return out
 
 
-def argmax_backward(arg, grad_out, src_rows, *, out=None, stream=None):
-    """grad_src[arg[r,f], f] += grad_out[r,f] (f64 accumulate, fp32 result)."""
+def argmax_backward(arg, grad_out, src_rows, *, out=None, src_lo=0, stream=None):
+    """grad_src[arg[r,f] - src_lo, f] += grad_out[r,f] for the source rows
+    [src_lo, src_lo + src_rows) (f64 accumulate, fp32 result)."""
     import torch
     rows, dim = arg.shape
+    if arg.dtype != torch.int32 or grad_out.dtype != torch.float32 or \
+            tuple(grad_out.shape) != (rows, dim) or arg.stride(1) != 1 or grad_out.stride(1) != 1:
+        raise A.ShapeError("argmax_backward: arg int32 and grad_out float32 [rows x dim] rows")
     if out is None:
         out = torch.empty((src_rows, dim), dtype=torch.float32, device=grad_out.device)
-    check(A.LIB.gspmm_argmax_backward(arg.data_ptr(), rows, dim, arg.stride(0),
-                                      grad_out.data_ptr(), grad_out.stride(0), out.data_ptr(),
-                                      src_rows, out.stride(0), _stream(stream, grad_out)),
+    _check_out(out, src_rows, dim, torch.float32, grad_out.device, "out")
+    check(A.LIB.gspmm_argmax_backward_range(arg.data_ptr(), rows, dim, arg.stride(0),
+                                            grad_out.data_ptr(), grad_out.stride(0),
+                                            out.data_ptr(), src_lo, src_rows, out.stride(0),
+                                            _stream(stream, grad_out)),
           "argmax_backward")
+    return out
+
+
+def argmax_backward_host(arg, grad_out, src_rows, *, out=None, device=0, stream=None):
+    """argmax_backward on host arrays (gspmm_argmax_backward_host)."""
+    arg = np.ascontiguousarray(arg, np.int32)
+    grad_out = np.ascontiguousarray(grad_out, np.float32)
+    rows, dim = arg.shape
+    if out is None:
+        out = np.empty((src_rows, dim), np.float32)
+    check(A.LIB.gspmm_argmax_backward_host(arg.ctypes.data, rows, dim, grad_out.ctypes.data,
+                                           out.ctypes.data, src_rows, device, stream or None),
+          "argmax_backward_host")
+    return out
+
+
+def argmax_backward_host_async(arg, grad_out, src_rows, *, out, device=0, stream,
+                               wait_event=None, upload_event=None):
+    """Enqueue-only argmax_backward_host: pinned arrays, valid after `stream`
+    synchronizes."""
+    rows, dim = arg.shape
+    if arg.dtype != np.int32 or grad_out.dtype != np.float32 or out.shape != (src_rows, dim) \
+            or not (arg.flags.c_contiguous and grad_out.flags.c_contiguous and
+                    out.flags.c_contiguous):
+        raise A.ShapeError("argmax_backward_host_async: contiguous int32 / float32 arrays")
+    ev = lambda x: None if x is None else (x if isinstance(x, int) else x.cuda_event)  # noqa: E731
+    st = stream if isinstance(stream, int) else stream.cuda_stream
+    check(A.LIB.gspmm_argmax_backward_host_async(arg.ctypes.data, rows, dim,
+                                                 grad_out.ctypes.data, out.ctypes.data,
+                                                 src_rows, device, st, ev(wait_event),
+                                                 ev(upload_event)),
+          "argmax_backward_host_async")
     return out
 
 
@@ -328,18 +411,28 @@ def binary_reduce_host(graph, cfg, u=None, v=None, e=None, *, out=None, want_arg
 
 
 def binary_reduce_host_async(graph, cfg, u=None, v=None, e=None, *, out, heads=1, stream,
-                             wait_event=None, upload_event=None, e_order=EDGE_BY_ID):
+                             wait_event=None, upload_event=None, e_order=EDGE_BY_ID,
+                             arg_other=None, other_scale=None):
     """Enqueue-only form of binary_reduce_host (gspmm_binary_reduce_host_async):
-    pinned host arrays in and out, valid once `stream` synchronizes; uploads
-    start after `wait_event` and `upload_event` is recorded when they are done
+    pinned host arrays in and out (``arg_other``: an int32 output array for
+    the argmax; ``other_scale``: a host float32 array over the gathered
+    nodes), valid once `stream` synchronizes; uploads start after
+    `wait_event` and `upload_event` is recorded when they are done
     (torch.cuda.Event objects or raw handles)."""
     cfg = as_config(cfg)
     mu, mv, me = _host_mat(u), _host_mat(v), _host_mat(e, e_order)
     rows, dim = out_shape(graph, cfg, u, v, e, heads, host=True)
-    if out.shape != (rows, dim):
-        raise A.ShapeError(f"out must be {rows} x {dim}")
+    if out.shape != (rows, dim) or out.dtype != np.float32 or not out.flags.c_contiguous:
+        raise A.ShapeError(f"out must be a contiguous float32 {rows} x {dim} array")
+    if arg_other is not None and (arg_other.shape != (rows, dim) or arg_other.dtype != np.int32
+                                  or not arg_other.flags.c_contiguous):
+        raise A.ShapeError(f"arg_other must be a contiguous int32 {rows} x {dim} array")
+    if other_scale is not None and (other_scale.dtype != np.float32 or
+                                    other_scale.shape != (graph.num_cols,) or
+                                    not other_scale.flags.c_contiguous):
+        raise A.ShapeError(f"other_scale must be a float32 array of {graph.num_cols}")
     mo = A.Out(out.ctypes.data, rows, dim, dim)
-    opts = _opts(heads, None, None)
+    opts = _opts(heads, _ptr(arg_other), None, _ptr(other_scale))
     ev = lambda x: None if x is None else (x if isinstance(x, int) else x.cuda_event)  # noqa: E731
     st = stream if isinstance(stream, int) else stream.cuda_stream
     check(A.LIB.gspmm_binary_reduce_host_async(graph.handle, C.byref(cfg), _ref(mu), _ref(mv),

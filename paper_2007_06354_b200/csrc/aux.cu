@@ -7,7 +7,11 @@
 //     result matches the oracle's f64 accumulation independently of the
 //     order in which the atomics land.  Backward only: the forward path
 //     never uses atomics.
+#include <algorithm>
 #include <atomic>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "device_ops.cuh"
 
@@ -29,64 +33,58 @@ __global__ void k_permute_edges(const uint32_t* __restrict__ eids, uint64_t m,
   }
 }
 
-__global__ void k_argmax_scatter(const int32_t* __restrict__ arg, int64_t rows,
-                                 int64_t dim, int64_t arg_ld,
-                                 const float* __restrict__ grad,
-                                 int64_t grad_ld, double* __restrict__ acc) {
-  const int64_t total = rows * dim;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-       i < total; i += stride) {
-    const int64_t r = i / dim, c = i - r * dim;
-    const int32_t a = __ldg(arg + r * arg_ld + c);
-    if (a >= 0) atomicAdd(acc + static_cast<int64_t>(a) * dim + c,
-                          static_cast<double>(__ldg(grad + r * grad_ld + c)));
-  }
-}
-
-// Vector forms for dim % 4 == 0 with 16-byte aligned rows: a thread owns
-// four consecutive columns (one LDG.128 of the argmax ids and one of the
-// gradient, four f64 atomics), and the row index comes from a 32-bit
-// division once per four elements instead of a 64-bit one per element.
-__global__ void k_argmax_scatter4(const int32_t* __restrict__ arg, uint32_t rows, uint32_t quads,
-                                  int64_t arg_ld, const float* __restrict__ grad,
-                                  int64_t grad_ld, double* __restrict__ acc, int64_t dim) {
-  const uint32_t total = rows * quads;
+// Argmax backward in COLUMN CHUNKS: the f64 accumulator of one chunk of C
+// columns (src_rows x C x 8 B, ~80 MB at most, e.g. 4 columns of config 3's
+// 2.45M rows) stays resident in the 126 MB L2 while every row's C argmax ids
+// and gradients are scattered into it; a second kernel rounds the chunk to
+// fp32 once and zeroes it for the next chunk.  One 2 GB accumulator for all
+// columns (round 1) missed L2 on 65% of its reduction sectors and moved
+// 1.84x the algorithmic bytes.  Targets outside [lo, lo + src_rows) are
+// skipped (a rank's own source rows in the multi-GPU owner-computes form).
+template <bool VEC>
+__global__ void k_argmax_chunk(const int32_t* __restrict__ arg, int64_t arg_ld,
+                               const float* __restrict__ grad, int64_t grad_ld, uint32_t rows,
+                               int c0, int cw, int64_t lo, uint32_t src_rows, int C,
+                               double* __restrict__ acc) {
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const uint32_t r = i / quads, q = i - r * quads;
-    const int4 a = __ldg(reinterpret_cast<const int4*>(arg + r * arg_ld) + q);
-    const float4 g = __ldg(reinterpret_cast<const float4*>(grad + r * grad_ld) + q);
-    const int64_t c = static_cast<int64_t>(q) * 4;
-    if (a.x >= 0) atomicAdd(acc + static_cast<int64_t>(a.x) * dim + c, static_cast<double>(g.x));
-    if (a.y >= 0) atomicAdd(acc + static_cast<int64_t>(a.y) * dim + c + 1, static_cast<double>(g.y));
-    if (a.z >= 0) atomicAdd(acc + static_cast<int64_t>(a.z) * dim + c + 2, static_cast<double>(g.z));
-    if (a.w >= 0) atomicAdd(acc + static_cast<int64_t>(a.w) * dim + c + 3, static_cast<double>(g.w));
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride) {
+    const int32_t* ar = arg + static_cast<int64_t>(r) * arg_ld + c0;
+    const float* gr = grad + static_cast<int64_t>(r) * grad_ld + c0;
+    if constexpr (VEC) {  // cw == C, a multiple of 4, 16-byte aligned rows
+      for (int q = 0; q < cw; q += 4) {
+        const int4 a = __ldcs(reinterpret_cast<const int4*>(ar + q));
+        const float4 g = __ldcs(reinterpret_cast<const float4*>(gr + q));
+        const int32_t av[4] = {a.x, a.y, a.z, a.w};
+        const float gv[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int64_t u = static_cast<int64_t>(av[t]) - lo;
+          if (av[t] >= 0 && static_cast<uint64_t>(u) < src_rows)
+            atomicAdd(acc + u * C + q + t, static_cast<double>(gv[t]));
+        }
+      }
+    } else {
+      for (int t = 0; t < cw; ++t) {
+        const int32_t a = __ldg(ar + t);
+        const int64_t u = static_cast<int64_t>(a) - lo;
+        if (a >= 0 && static_cast<uint64_t>(u) < src_rows)
+          atomicAdd(acc + u * C + t, static_cast<double>(__ldg(gr + t)));
+      }
+    }
   }
 }
 
-__global__ void k_round_f64x4(const double* __restrict__ acc, uint32_t rows, uint32_t quads,
-                              float* __restrict__ out, int64_t ld) {
-  const uint32_t total = rows * quads;
+// out[u, c0 : c0 + cw] = (float) acc[u, :cw]; acc zeroed for the next chunk.
+__global__ void k_argmax_round(double* __restrict__ acc, uint32_t src_rows, int C, int cw,
+                               float* __restrict__ out, int64_t ld, int c0) {
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const uint32_t r = i / quads, q = i - r * quads;
-    const double2 lo = __ldg(reinterpret_cast<const double2*>(acc) + 2 * static_cast<uint64_t>(i));
-    const double2 hi = __ldg(reinterpret_cast<const double2*>(acc) + 2 * static_cast<uint64_t>(i) + 1);
-    reinterpret_cast<float4*>(out + r * ld)[q] =
-        make_float4(__double2float_rn(lo.x), __double2float_rn(lo.y), __double2float_rn(hi.x),
-                    __double2float_rn(hi.y));
-  }
-}
-
-__global__ void k_round_f64(const double* __restrict__ acc, int64_t rows,
-                            int64_t dim, float* __restrict__ out, int64_t ld) {
-  const int64_t total = rows * dim;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-       i < total; i += stride) {
-    const int64_t r = i / dim, c = i - r * dim;
-    out[r * ld + c] = __double2float_rn(acc[i]);
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < src_rows; u += stride) {
+    double* a = acc + static_cast<int64_t>(u) * C;
+    float* o = out + static_cast<int64_t>(u) * ld + c0;
+    for (int t = 0; t < cw; ++t) {
+      o[t] = __double2float_rn(a[t]);
+      a[t] = 0.0;
+    }
   }
 }
 
@@ -120,6 +118,22 @@ unsigned grid_for(int64_t work, int threads) {
 }  // namespace
 
 void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// The dynamic shared-memory attribute is per (kernel, device): set it once
+// for each pair, under a lock (host threads may drive several GPUs).
+cudaError_t set_max_dynamic_smem(const void* func, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& d : done)
+    if (d.first == func && d.second == dev) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.emplace_back(func, dev);
+  return e;
+}
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 cudaError_t launch_permute_edges(const uint32_t* eids, uint64_t m,
@@ -132,45 +146,47 @@ cudaError_t launch_permute_edges(const uint32_t* eids, uint64_t m,
   return cudaGetLastError();
 }
 
-cudaError_t launch_argmax_backward(const int32_t* arg, int64_t rows,
-                                   int64_t dim, int64_t arg_ld,
-                                   const float* grad_out, int64_t grad_ld,
-                                   float* grad_src, int64_t src_rows,
-                                   int64_t src_ld, double* acc,
-                                   cudaStream_t s) {
-  cudaError_t err = cudaMemsetAsync(acc, 0, sizeof(double) * src_rows * dim, s);
-  if (err != cudaSuccess) return err;
+cudaError_t launch_argmax_backward(const int32_t* arg, int64_t rows, int64_t dim,
+                                   int64_t arg_ld, const float* grad_out, int64_t grad_ld,
+                                   float* grad_src, int64_t src_lo, int64_t src_rows,
+                                   int64_t src_ld, cudaStream_t s) {
+  if (src_rows <= 0 || dim <= 0) return cudaSuccess;
+  if (rows >= (int64_t{1} << 32) || src_rows >= (int64_t{1} << 32)) return cudaErrorInvalidValue;
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
-  const bool vec = dim % 4 == 0 && arg_ld % 4 == 0 && grad_ld % 4 == 0 && src_ld % 4 == 0 &&
-                   al16(arg) && al16(grad_out) && al16(grad_src) &&
-                   rows * (dim / 4) < (int64_t{1} << 32) - (int64_t{1} << 24) &&
-                   src_rows * (dim / 4) < (int64_t{1} << 32) - (int64_t{1} << 24);
-  if (vec) {
-    const int64_t quads = dim / 4;
-    if (rows * quads > 0) {
-      k_argmax_scatter4<<<grid_for(rows * quads, 256), 256, 0, s>>>(
-          arg, static_cast<uint32_t>(rows), static_cast<uint32_t>(quads), arg_ld, grad_out,
-          grad_ld, acc, dim);
+  const bool vec_layout = dim % 4 == 0 && arg_ld % 4 == 0 && grad_ld % 4 == 0 && al16(arg) &&
+                          al16(grad_out);
+  // chunk width: the widest multiple of 4 whose accumulator fits ~80 MB
+  constexpr double kAccBytes = 80.0 * 1048576.0;
+  int C = static_cast<int>(kAccBytes / (8.0 * static_cast<double>(src_rows))) & ~3;
+  C = std::max(4, std::min<int>(C, static_cast<int>((dim + 3) & ~int64_t{3})));
+  double* acc = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&acc),
+                                  sizeof(double) * static_cast<size_t>(src_rows) * C, s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(acc, 0, sizeof(double) * static_cast<size_t>(src_rows) * C, s);
+  const unsigned gs = grid_for(rows, 256), gr = grid_for(src_rows, 256);
+  for (int64_t c0 = 0; c0 < dim && e == cudaSuccess; c0 += C) {
+    const int cw = static_cast<int>(std::min<int64_t>(C, dim - c0));
+    if (rows > 0) {
+      if (vec_layout && cw % 4 == 0)
+        k_argmax_chunk<true><<<gs, 256, 0, s>>>(arg, arg_ld, grad_out, grad_ld,
+                                                static_cast<uint32_t>(rows), static_cast<int>(c0),
+                                                cw, src_lo, static_cast<uint32_t>(src_rows), C,
+                                                acc);
+      else
+        k_argmax_chunk<false><<<gs, 256, 0, s>>>(arg, arg_ld, grad_out, grad_ld,
+                                                 static_cast<uint32_t>(rows),
+                                                 static_cast<int>(c0), cw, src_lo,
+                                                 static_cast<uint32_t>(src_rows), C, acc);
       note_launch();
     }
-    if (src_rows * quads > 0) {
-      k_round_f64x4<<<grid_for(src_rows * quads, 256), 256, 0, s>>>(
-          acc, static_cast<uint32_t>(src_rows), static_cast<uint32_t>(quads), grad_src, src_ld);
-      note_launch();
-    }
-    return cudaGetLastError();
-  }
-  if (rows * dim > 0) {
-    k_argmax_scatter<<<grid_for(rows * dim, 256), 256, 0, s>>>(arg, rows, dim, arg_ld,
-                                                               grad_out, grad_ld, acc);
+    k_argmax_round<<<gr, 256, 0, s>>>(acc, static_cast<uint32_t>(src_rows), C, cw, grad_src,
+                                      src_ld, static_cast<int>(c0));
     note_launch();
+    e = cudaGetLastError();
   }
-  if (src_rows * dim > 0) {
-    k_round_f64<<<grid_for(src_rows * dim, 256), 256, 0, s>>>(acc, src_rows, dim, grad_src,
-                                                             src_ld);
-    note_launch();
-  }
-  return cudaGetLastError();
+  cudaFreeAsync(acc, s);
+  return e;
 }
 
 cudaError_t launch_scale_rows(const float* x, int64_t rows, int64_t dim, int64_t ld,

@@ -38,6 +38,17 @@ __global__ void k_split_keys(const uint64_t* __restrict__ keys, uint64_t m,
   }
 }
 
+// First edge (lowest edge id) with an endpoint >= n, or ~0 (atomicMin).
+__global__ void k_check_ids(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+                            uint64_t m, uint32_t n, unsigned long long* __restrict__ first_bad) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride)
+    if (__ldg(src + i) >= n || __ldg(dst + i) >= n) {
+      atomicMin(first_bad, static_cast<unsigned long long>(i));
+      return;
+    }
+}
+
 __global__ void k_rows_of(const uint32_t* __restrict__ indptr, uint32_t rows,
                           uint32_t* __restrict__ rowof) {
   const uint32_t stride = gridDim.x * blockDim.x;
@@ -158,6 +169,27 @@ cudaError_t launch_build_csr(uint32_t n, uint64_t m, const uint32_t* src, const 
                              cudaStream_t s) {
   return sort_build(n, n, m, dst_major ? dst : src, dst_major ? src : dst, nullptr, indptr,
                     indices, eids, s);
+}
+
+cudaError_t check_edge_ids(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                           cudaStream_t s, uint64_t* first_bad) {
+  *first_bad = ~0ull;
+  if (m == 0) return cudaSuccess;
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned long long), s);
+  if (e) return e;
+  e = cudaMemsetAsync(d, 0xff, sizeof(unsigned long long), s);
+  if (e == cudaSuccess) {
+    k_check_ids<<<148 * 8, 256, 0, s>>>(src, dst, m, n, d);
+    note_launch();
+    e = cudaGetLastError();
+  }
+  unsigned long long h = ~0ull;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(d, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  *first_bad = h;
+  return e;
 }
 
 cudaError_t launch_transpose_csr(uint32_t num_rows, uint32_t num_cols, uint64_t m,

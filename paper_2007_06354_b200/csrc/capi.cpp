@@ -12,6 +12,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "gspmm_b200.h"
@@ -52,26 +53,23 @@ const char* operand_name(int o) {
   }
 }
 
-// Device plan defaults: cost (edges + 2 per row) per row segment, and the
-// coarsest long-row threshold.  Overridable for experiments with
-// GSPMM_SEG_EDGES / GSPMM_LONG_EDGES (the latter forces a single level).
-// 256: with every unit pulled from the counter, finer units shorten the
-// segment kernel's drain (measured cost 1024 / 512 / 256 / 128 / 64: cfg2
-// forward 1.87 / 1.72 / 1.70 / 1.69 / 1.69 ms, cfg3 mean 5.54 / 5.48 / 5.45 /
-// 5.46 / 5.51, cfg4 7.18 / 7.19 / 7.01 / 7.12 / 7.00, cfg5 -- / -- / 15.6 /
-// 15.5 / 15.5; 2048: cfg2 2.08)
+// Device plan defaults (gspmm_graph_set_plan overrides them): cost (edges +
+// 2 per row) per row segment; with every unit pulled from the counter, finer
+// units shorten the segment kernel's drain (measured cost 1024 / 512 / 256 /
+// 128 / 64: cfg2 forward 1.87 / 1.72 / 1.70 / 1.69 / 1.69 ms, cfg3 mean 5.54
+// / 5.48 / 5.45 / 5.46 / 5.51, cfg4 7.18 / 7.19 / 7.01 / 7.12 / 7.00, cfg5
+// -- / -- / 15.6 / 15.5 / 15.5; 2048: cfg2 2.08).  The long-row thresholds
+// of the plan levels are kLevelThresholds.
 constexpr uint32_t kSegEdges = 256;
-constexpr uint32_t kLongEdges = 4096;
-// rows above this many edges are cut into 64-column slices so several CTAs
-// stream one row (the 66k-329k-edge hubs of the power-law configs)
-constexpr uint32_t kXlEdges = 16384;
-
-uint32_t env_u32(const char* name, uint32_t dflt) {
-  const char* v = std::getenv(name);
-  if (!v || !*v) return dflt;
-  const long x = std::strtol(v, nullptr, 10);
-  return x > 0 ? static_cast<uint32_t>(x) : dflt;
-}
+constexpr uint32_t kLevelThresholds[5] = {1024, 4096, 16384, 32768, 65536};
+// Source blocking: blocks of <= 48 MB of gathered rows (a share of the
+// 126 MB L2), see source_blocks_for.
+constexpr double kSrcBlockBytes = 48.0 * 1048576.0;
+// Long-row column units (k_long_rg): stream rate of one CTA on random rows
+// and the rate of one column's fp32 add chain (one dependent add per ~4
+// cycles at 1.965 GHz), the two bounds of a unit's time.
+constexpr double kUnitBytesPerS = 40.0e9;
+constexpr double kChainEdgesPerS = 490.0e6;
 
 // The stream-ordered pool of the current device keeps freed memory mapped
 // across synchronizations (its default release threshold of 0 unmaps it at
@@ -94,6 +92,31 @@ void retain_pool_memory() {
 
 }  // namespace
 
+// Per-call device state, one context per caller stream: the work-unit
+// counters, the prescale workspace and the `done` event of the context's
+// last call.  Calls on one stream are ordered by the stream; calls on
+// different streams (or host threads) use different contexts, so they can
+// run concurrently on one handle without sharing a counter or a workspace.
+// Every call first waits for the context's previous call (its `done`
+// event), so a context handed to a new stream -- a recycled stream handle,
+// or the LRU context once kMaxContexts are in use -- is never reused while
+// the old call still runs.  The graph's mutex is held while a call is
+// enqueued (not while it runs), which orders the enqueue steps of one
+// context (counter reset, launches, event records) across host threads.
+struct CallCtx {
+  cudaStream_t key = nullptr;
+  uint32_t* d_counter = nullptr;  // [0] segment units, [1] long-row units
+  cudaEvent_t done = nullptr;
+  bool used = false;
+  void* dws = nullptr;  // prescaled gathered rows (mean backward)
+  size_t dws_bytes = 0;
+  uint64_t last_use = 0;
+  // edge softmax: hub rows run on a side stream (created on first use)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+constexpr size_t kMaxContexts = 32;
+
 struct gspmm_graph_s {
   int device = 0;
   int orientation = GSPMM_DST_MAJOR;
@@ -103,60 +126,102 @@ struct gspmm_graph_s {
   uint32_t* d_indices = nullptr;
   uint32_t* d_eids = nullptr;
   // Device plan, one level per long-row threshold (degree above which a row
-  // is folded by a whole CTA): picked per call from the row bytes.
+  // runs as long-row column units): picked per call from the row bytes.
   struct Level {
     uint32_t threshold = 0;
-    uint32_t* d_long = nullptr;  // long rows, heaviest first
+    std::vector<uint32_t> long_rows;  // host copy, heaviest first
+    std::vector<uint32_t> long_deg;
+    uint32_t* d_long = nullptr;       // device copy (edge softmax hub rows)
     uint32_t num_long = 0;
-    uint32_t num_xl = 0;         // leading long rows above kXlEdges (narrow slices)
-    uint64_t long_edges = 0;     // edges in long rows (sizes the long-row grid)
-    uint2* d_segs = nullptr;     // segments of consecutive non-long rows
+    uint2* d_segs = nullptr;          // segments of consecutive non-long rows
     uint32_t num_segs = 0;
   };
   Level level[5];
   int n_levels = 0;
-  uint32_t* d_counter = nullptr;  // [0] segment units, [1] long-row units
-  uint32_t* d_rowof = nullptr;     // owner row of each CSR position (edge dots), lazy
-  cudaStream_t side = nullptr;     // long-row kernel runs here concurrently
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // long-row column units per (level, width), built on first use
+  struct Units {
+    int level = 0, width = 0;
+    uint2* d = nullptr;
+    uint32_t n = 0;
+  };
+  std::vector<Units> units;
+  uint32_t* d_rowof = nullptr;  // owner row of each CSR position (edge dots), lazy
   int num_sms = 148;
-  std::mutex mu;  // guards the host-call workspace
-  void* ws = nullptr;
-  size_t ws_bytes = 0;
-  void* dws = nullptr;  // device workspace of the prescaled gathers
-  size_t dws_bytes = 0;
+  std::recursive_mutex mu;      // held while a call is enqueued
+  std::vector<CallCtx*> ctxs;
+  uint64_t calls = 0;
   // source blocks (gspmm_graph_set_source_blocks): sub-graphs over neighbour
   // id ranges, built on first use for block_nb blocks
   int blocks_pref = 0;  // 0 auto, 1 never, >= 2 forced
   uint32_t block_nb = 0;
   std::vector<gspmm_graph_s*> blocks;
+  // plan options (gspmm_graph_set_plan)
+  uint32_t seg_cost = 0;        // 0 -> kSegEdges
+  uint32_t forced_long = 0;     // 0 -> the kLevelThresholds levels
+  uint32_t unit_cols = 0;       // 0 -> automatic long-row unit widths
+  int rows_kernel_only = 0;     // 1 -> every call on the register kernel (rows.cu)
 };
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no
-// libcuda link dependency).
-bool gspmm_b200::encode_rows_tmap(CUtensorMap* map, const OperandDesc& d, int width, int box) {
-  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static Encode enc = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      f = nullptr;
-    return reinterpret_cast<Encode>(f);
-  }();
-  if (!enc || box < 8 || box > 256 || box % 8 || d.ld % 4 || d.rows < 1) return false;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(width), static_cast<cuuint64_t>(d.rows)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(d.ld) * 4u};
-  const cuuint32_t boxd[2] = {static_cast<cuuint32_t>(box), 1u};
-  const cuuint32_t es[2] = {1u, 1u};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(d.base), dims, strides,
-             boxd, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+namespace {
+
+// The context of caller stream s (graph mutex held).
+int context_for(gspmm_graph_s* g, cudaStream_t s, CallCtx** out) {
+  ++g->calls;
+  for (CallCtx* c : g->ctxs)
+    if (c->key == s) {
+      c->last_use = g->calls;
+      *out = c;
+      return GSPMM_OK;
+    }
+  CallCtx* c = nullptr;
+  if (g->ctxs.size() < kMaxContexts) {
+    c = new CallCtx;
+    cudaError_t e = cudaMalloc(&c->d_counter, 4 * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      cudaFree(c->d_counter);
+      delete c;
+      return cuda_fail(e, "call context");
+    }
+    g->ctxs.push_back(c);
+  } else {
+    c = g->ctxs[0];
+    for (CallCtx* x : g->ctxs)
+      if (x->last_use < c->last_use) c = x;
+  }
+  c->key = s;
+  c->last_use = g->calls;
+  *out = c;
+  return GSPMM_OK;
 }
+
+int begin_call(CallCtx* c, cudaStream_t s) {
+  if (c->used) CUDA_TRY(cudaStreamWaitEvent(s, c->done, 0), "context order");
+  return GSPMM_OK;
+}
+
+int end_call(CallCtx* c, cudaStream_t s) {
+  CUDA_TRY(cudaEventRecord(c->done, s), "context order");
+  c->used = true;
+  return GSPMM_OK;
+}
+
+void free_contexts(gspmm_graph_s* g) {
+  for (CallCtx* c : g->ctxs) {
+    cudaFree(c->d_counter);
+    cudaFree(c->dws);
+    if (c->done) cudaEventDestroy(c->done);
+    if (c->side) {
+      cudaStreamDestroy(c->side);
+      cudaEventDestroy(c->fork);
+      cudaEventDestroy(c->join);
+    }
+    delete c;
+  }
+  g->ctxs.clear();
+}
+
+}  // namespace
 
 namespace {
 
@@ -298,6 +363,8 @@ int bind(const gspmm_graph_s* g, const gspmm_config* cfg, const gspmm_mat* u,
   L.gather_dim = static_cast<int32_t>(gather);
   L.heads = heads;
   L.other_scale = opt->other_scale;
+  if (opt->source_blocks < 0) return fail(GSPMM_ERR_ARG, "source_blocks must be >= 0");
+  L.src_blocks = opt->source_blocks;
   L.arg_other = opt->arg_other;
   L.arg_edge = opt->arg_edge;
   L.arg_ld = opt->arg_ld ? opt->arg_ld : w;
@@ -339,66 +406,57 @@ int bind(const gspmm_graph_s* g, const gspmm_config* cfg, const gspmm_mat* u,
 // Which planned kernel runs this binding?  Both planned kernels take the
 // gathered full-width operand as lhs and at most a small (scalar /
 // per-head) edge or neighbour operand as rhs; everything else goes to the
-// simple register kernel (rows.cu).  0 = rows.cu, 1 = gather.cu (default),
-// 2 = stream.cu (TMA-staged, GSPMM_KERNEL=tma).
-int plan_kernel(const RowLaunch& L, int* rhs_width) {
-  static const char* kname = std::getenv("GSPMM_KERNEL");
-  static const int forced = !kname ? -1
-                            : std::strcmp(kname, "rows") == 0 ? 0
-                            : std::strcmp(kname, "tma") == 0 ? 2 : 1;
-  if (forced == 0 || std::getenv("GSPMM_DISABLE_STREAM") != nullptr) return 0;
-  if (L.binop == GSPMM_DOT || L.out_edge || !L.out) return 0;
-  if (L.reduce == R_PROD || L.reduce == R_LAST) return 0;  // rare: rows.cu
-  if (L.other_scale && L.rhs.base) return 0;                // scale on top of an rhs: rows.cu
-  if (L.lhs.mode != MODE_FULL || L.lhs.role == ROLE_ROW) return 0;
-  if (L.lhs.ld % 4 || !aligned(L.lhs.base, 16)) return 0;
-  if (L.out_ld % 4 || !aligned(L.out, 16)) return 0;
+// register kernel (rows.cu).  Returns false for rows.cu.
+bool planned(const gspmm_graph_s* g, const RowLaunch& L, int* rhs_width) {
+  if (g->rows_kernel_only) return false;
+  if (L.binop == GSPMM_DOT || L.out_edge || !L.out) return false;
+  if (L.reduce == R_PROD || L.reduce == R_LAST) return false;  // rare: rows.cu
+  if (L.other_scale && L.rhs.base) return false;                // scale on top of an rhs
+  if (L.lhs.mode != MODE_FULL || L.lhs.role == ROLE_ROW) return false;
+  if (L.lhs.ld % 4 || !aligned(L.lhs.base, 16)) return false;
+  if (L.out_ld % 4 || !aligned(L.out, 16)) return false;
   *rhs_width = 0;
-  const int k = forced == 2 ? 2 : 1;
   if (L.rhs.base) {
-    if (L.rhs.role == ROLE_ROW || L.rhs.mode == MODE_FULL) return 0;
+    if (L.rhs.role == ROLE_ROW || L.rhs.mode == MODE_FULL) return false;
     // lanes fold float4 column groups: a head must cover whole groups
-    if (L.rhs.mode == MODE_HEAD && L.rhs.group % 4) return 0;
-    const int h = L.rhs.mode == MODE_SCALAR ? 1 : L.width / L.rhs.group;
-    if (k == 2) {  // TMA variant stages the small operand with cp.async
-      if (L.other_scale) return 0;
-      if (h != 1 && h != 2 && h != 4 && h != 8 && h != 16) return 0;
-      if (h >= 2 && (L.rhs.ld % h || !aligned(L.rhs.base, h >= 4 ? 16 : 8))) return 0;
-      if (h >= 4 && L.rhs.ld % 4) return 0;
-    }
-    *rhs_width = h;
+    if (L.rhs.mode == MODE_HEAD && L.rhs.group % 4) return false;
+    *rhs_width = L.rhs.mode == MODE_SCALAR ? 1 : L.width / L.rhs.group;
   }
-  return k;
+  return true;
 }
 
-int launch(gspmm_graph_s* g, Bound& b, void* stream);
+int run_call(gspmm_graph_s* g, Bound& b, cudaStream_t s);
+int launch(gspmm_graph_s* g, CallCtx* ctx, Bound& b, cudaStream_t s);
 void destroy_graph(gspmm_graph_s* g);
 
 // Number of source blocks for this call: 1 = a single pass.
 uint32_t source_blocks_for(const gspmm_graph_s* g, const RowLaunch& L) {
-  if (g->blocks_pref == 1 || L.acc_in || L.epi) return 1;
+  const int pref = L.src_blocks ? L.src_blocks : g->blocks_pref;
+  if (pref == 1 || L.acc_in || L.epi) return 1;
   int rw = 0;
-  if (plan_kernel(L, &rw) == 0) return 1;
+  if (!planned(g, L, &rw)) return 1;
   if (L.lhs.role != ROLE_OTHER || L.arg_other || L.arg_edge) return 1;
   if (L.reduce != R_SUM && L.reduce != R_MAX && L.reduce != R_MIN) return 1;
   if (L.rhs.base && L.rhs.role == ROLE_POS) return 1;
-  if (g->blocks_pref >= 2) return std::min<uint32_t>(g->blocks_pref, 64);
-  // automatic: blocks of <= GSPMM_SRC_BLOCK_MB of gathered rows (default
-  // 48 MB, a share of the 126 MB L2) when the gathered operand exceeds 1.5x
-  // the L2 and each row has >= 8 edges per block (the partial-row read +
-  // write per pass is then small against the row's gathers).  Measured on
-  // cfg5 (232,965 x 602 fp32 = 561 MB, 495 edges per row): 12 blocks,
-  // 35.4 -> 18.2 ms; 32 / 64 / 96 / 160 MB blocks: 19.2 / 18.9 / 22.7 / 32.8 ms
+  if (pref >= 2) return std::min<uint32_t>(pref, 64);
+  // automatic: blocks of <= 48 MB of gathered rows when the gathered operand
+  // exceeds 1.5x the L2 and each row has >= 8 edges per block (the
+  // partial-row read + write per pass is then small against the row's
+  // gathers).  Measured on cfg5 (232,965 x 602 fp32 = 561 MB, 495 edges per
+  // row): 12 blocks, 35.4 -> 18.2 ms; 32 / 64 / 96 / 160 MB blocks: 19.2 /
+  // 18.9 / 22.7 / 32.8 ms
   const double bytes = static_cast<double>(g->num_cols) * L.width * 4.0;
-  static const double target = env_u32("GSPMM_SRC_BLOCK_MB", 48) * 1048576.0;
   if (bytes < 1.5 * 126.0 * 1048576.0) return 1;
-  const uint32_t nb = static_cast<uint32_t>(std::ceil(bytes / target));
+  const uint32_t nb = static_cast<uint32_t>(std::ceil(bytes / kSrcBlockBytes));
   const double avg = g->num_rows ? static_cast<double>(g->m) / g->num_rows : 0.0;
   if (nb < 2 || avg < 8.0 * nb) return 1;
   return std::min<uint32_t>(nb, 64);
 }
 
-int build_source_blocks(gspmm_graph_s* g, uint32_t nb) {
+// Source-block sub-graphs (graph mutex held).  Built on the caller's stream
+// and completed before they are published: a concurrent call on another
+// stream only ever sees finished blocks.
+int build_source_blocks(gspmm_graph_s* g, uint32_t nb, cudaStream_t s) {
   if (g->block_nb == nb) return GSPMM_OK;
   for (auto* sg : g->blocks) destroy_graph(sg);
   g->blocks.clear();
@@ -414,22 +472,26 @@ int build_source_blocks(gspmm_graph_s* g, uint32_t nb) {
     return st;
   };
   CUDA_TRY(cudaMalloc(&bpos, sizeof(uint32_t) * (nb + 1ull) * rows), "block bounds");
-  CUDA_TRY(launch_block_bounds(g->d_indptr, g->d_indices, rows, nb, bs, bpos, nullptr),
+  CUDA_TRY(launch_block_bounds(g->d_indptr, g->d_indices, rows, nb, bs, bpos, s),
            "block bounds");
   if (cudaMalloc(&ip, sizeof(uint32_t) * (rows + 1ull)) != cudaSuccess ||
       cudaMalloc(&ix, sizeof(uint32_t) * std::max<uint64_t>(g->m, 1)) != cudaSuccess ||
       cudaMalloc(&ie, sizeof(uint32_t) * std::max<uint64_t>(g->m, 1)) != cudaSuccess)
     return done(cuda_fail(cudaErrorMemoryAllocation, "block CSR"));
   for (uint32_t b = 0; b < nb; ++b) {
-    const cudaError_t e = launch_block_csr(bpos + static_cast<uint64_t>(b) * rows,
-                                           bpos + static_cast<uint64_t>(b + 1) * rows, rows,
-                                           g->d_indices, g->d_eids, ip, ix, ie, nullptr);
+    cudaError_t e = launch_block_csr(bpos + static_cast<uint64_t>(b) * rows,
+                                     bpos + static_cast<uint64_t>(b + 1) * rows, rows,
+                                     g->d_indices, g->d_eids, ip, ix, ie, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return done(cuda_fail(e, "block CSR"));
     gspmm_graph sg = nullptr;
     const int st = gspmm_graph_create_device(g->device, g->orientation, rows, g->num_cols, ip,
                                              ix, ie, &sg);
     if (st) return done(st);
     sg->blocks_pref = 1;
+    sg->seg_cost = g->seg_cost;
+    sg->forced_long = g->forced_long;
+    sg->unit_cols = g->unit_cols;
     g->blocks.push_back(sg);
   }
   g->block_nb = nb;
@@ -438,8 +500,8 @@ int build_source_blocks(gspmm_graph_s* g, uint32_t nb) {
 
 // Source-blocked passes: pass b folds block b's neighbours into the partial
 // rows of passes < b (bit-identical: the canonical rows are neighbour-sorted).
-int launch_blocked(gspmm_graph_s* g, Bound& b, void* stream, uint32_t nb) {
-  int st = build_source_blocks(g, nb);
+int launch_blocked(gspmm_graph_s* g, Bound& b, cudaStream_t s, uint32_t nb) {
+  int st = build_source_blocks(g, nb, s);
   if (st) return st;
   for (uint32_t k = 0; k < nb; ++k) {
     gspmm_graph_s* sg = g->blocks[k];
@@ -450,83 +512,153 @@ int launch_blocked(gspmm_graph_s* g, Bound& b, void* stream, uint32_t nb) {
     bb.L.acc_in = k ? b.L.out : nullptr;
     bb.L.epi = k + 1 == nb ? 2 : 1;
     bb.L.deg_indptr = k + 1 == nb ? g->d_indptr : nullptr;
-    st = launch(sg, bb, stream);
+    st = run_call(sg, bb, s);
     if (st) return st;
   }
   return GSPMM_OK;
 }
 
-int launch(gspmm_graph_s* g, Bound& b, void* stream) {
+// Long-row column units of plan level li for output width W (graph mutex
+// held), built on first use: every long row is cut into column slices of a
+// width chosen so that no unit's time -- the larger of its bytes at one CTA's
+// stream rate and its edge count at the fp32 add-chain rate -- exceeds half
+// the long rows' balanced share of the GPU; 8 columns at least (a 32-byte
+// sector), 512 at most (the consumer warps' reach).  Heaviest units first.
+int long_units_for(gspmm_graph_s* g, int li, int W, const gspmm_graph_s::Units** out) {
+  for (const auto& u : g->units)
+    if (u.level == li && u.width == W) {
+      *out = &u;
+      return GSPMM_OK;
+    }
+  const auto& lv = g->level[li];
+  const int Wp = (W + 3) & ~3;
+  double total = 0.0;
+  for (uint32_t d : lv.long_deg) total += static_cast<double>(d) * Wp * 4.0;
+  const double cap = std::max(0.5 * total / (g->num_sms * kUnitBytesPerS), 20e-6);
+  struct U {
+    uint32_t r, c0, cw;
+    double t;
+  };
+  std::vector<U> us;
+  for (size_t i = 0; i < lv.long_rows.size(); ++i) {
+    const double n = lv.long_deg[i];
+    int sw;
+    if (g->unit_cols) {
+      sw = static_cast<int>(g->unit_cols);
+    } else {
+      sw = static_cast<int>(cap * kUnitBytesPerS / (n * 4.0)) & ~3;
+      sw = std::max(8, std::min(sw, 512));
+    }
+    sw = std::min(sw, Wp);
+    const int ns = (Wp + sw - 1) / sw;
+    sw = (((Wp + ns - 1) / ns) + 3) & ~3;  // balanced slices
+    for (int c0 = 0; c0 < W; c0 += sw) {
+      const int cw = std::min(sw, W - c0);
+      const double t = std::max(n * cw * 4.0 / kUnitBytesPerS, n / kChainEdgesPerS);
+      us.push_back({lv.long_rows[i], static_cast<uint32_t>(c0), static_cast<uint32_t>(cw), t});
+    }
+  }
+  std::stable_sort(us.begin(), us.end(), [](const U& a, const U& b) { return a.t > b.t; });
+  std::vector<uint2> h(us.size());
+  for (size_t i = 0; i < us.size(); ++i) h[i] = make_uint2(us[i].r, us[i].c0 | (us[i].cw << 16));
+  gspmm_graph_s::Units u;
+  u.level = li;
+  u.width = W;
+  u.n = static_cast<uint32_t>(h.size());
+  CUDA_TRY(cudaMalloc(&u.d, sizeof(uint2) * std::max<size_t>(h.size(), 1)), "long units");
+  if (!h.empty()) {
+    const cudaError_t e = cudaMemcpy(u.d, h.data(), sizeof(uint2) * h.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(u.d);
+      return cuda_fail(e, "long units");
+    }
+  }
+  g->units.push_back(u);
+  *out = &g->units.back();
+  return GSPMM_OK;
+}
+
+// One call on handle g: takes the graph mutex for the enqueue, runs in the
+// caller stream's context (see CallCtx).
+int run_call(gspmm_graph_s* g, Bound& b, cudaStream_t s) {
+  std::lock_guard<std::recursive_mutex> lock(g->mu);
+  CUDA_TRY(cudaSetDevice(g->device), "cudaSetDevice");
+  CallCtx* ctx = nullptr;
+  int st = context_for(g, s, &ctx);
+  if (st) return st;
+  if ((st = begin_call(ctx, s))) return st;
+  st = launch(g, ctx, b, s);
+  const int st2 = end_call(ctx, s);
+  return st ? st : st2;
+}
+
+int launch(gspmm_graph_s* g, CallCtx* ctx, Bound& b, cudaStream_t s) {
   cudaError_t err;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   int rw = 0;
-  int kind = 0;
   if (!b.L.out_edge && b.L.binop != GSPMM_DOT && b.L.other_scale && !b.L.rhs.base &&
       b.L.binop == GSPMM_COPY && b.L.lhs.role == ROLE_OTHER && b.L.lhs.mode == MODE_FULL &&
-      b.L.lhs.rows > 0 && plan_kernel(b.L, &rw) != 0 &&
+      b.L.lhs.rows > 0 && planned(g, b.L, &rw) &&
       static_cast<double>(g->m) >= 4.0 * static_cast<double>(b.L.lhs.rows)) {
     // The per-neighbour scale (the mean backward's 1/deg) on dense-enough
-    // graphs: scale every gathered row once into a workspace, then run the
-    // plain copy-sum.  Each product is the same single rounding as the
-    // kernels' per-edge scale, so the result is bit-identical (measured: cfg3
-    // mean backward 6.67 -> see DESIGN).
-    static const bool prescale_on = std::getenv("GSPMM_NO_PRESCALE") == nullptr;
-    if (prescale_on) {
-      const int64_t W = b.L.width;
-      const int64_t yld = (W + 3) & ~int64_t{3};
-      // the handle's device workspace (grown on demand; a handle runs one
-      // call at a time).  A stream-ordered allocation per call measured
-      // slower than the whole saving: the pool unmaps it at every sync.
-      const size_t need = sizeof(float) * static_cast<size_t>(b.L.lhs.rows * yld);
-      if (need > g->dws_bytes) {
-        cudaFree(g->dws);
-        g->dws = nullptr;
-        g->dws_bytes = 0;
-        CUDA_TRY(cudaMalloc(&g->dws, need), "prescale workspace");
-        g->dws_bytes = need;
-      }
-      float* y = static_cast<float*>(g->dws);
-      cudaError_t e0 = launch_scale_rows(b.L.lhs.base, b.L.lhs.rows, W, b.L.lhs.ld,
-                                         b.L.other_scale, y, yld, s);
-      int st = GSPMM_OK;
-      if (e0 == cudaSuccess) {
-        Bound bb = b;
-        bb.L.lhs.base = y;
-        bb.L.lhs.ld = yld;
-        bb.L.other_scale = nullptr;
-        st = launch(g, bb, stream);
-      }
-      if (e0 != cudaSuccess) return cuda_fail(e0, "prescale");
-      return st;
+    // graphs: scale every gathered row once into the context's workspace,
+    // then run the plain copy-sum.  Each product is the same single rounding
+    // as the kernels' per-edge scale, so the result is bit-identical
+    // (measured: cfg3 mean backward 6.67 -> 6.01 ms, cfg5 18.05 -> 16.56).
+    const int64_t W = b.L.width;
+    const int64_t yld = (W + 3) & ~int64_t{3};
+    const size_t need = sizeof(float) * static_cast<size_t>(b.L.lhs.rows * yld);
+    if (need > ctx->dws_bytes) {
+      // (cudaFree synchronizes the device: no call still reads the old one)
+      cudaFree(ctx->dws);
+      ctx->dws = nullptr;
+      ctx->dws_bytes = 0;
+      CUDA_TRY(cudaMalloc(&ctx->dws, need), "prescale workspace");
+      ctx->dws_bytes = need;
     }
+    float* y = static_cast<float*>(ctx->dws);
+    CUDA_TRY(launch_scale_rows(b.L.lhs.base, b.L.lhs.rows, W, b.L.lhs.ld, b.L.other_scale, y,
+                               yld, s),
+             "prescale");
+    Bound bb = b;
+    bb.L.lhs.base = y;
+    bb.L.lhs.ld = yld;
+    bb.L.other_scale = nullptr;
+    return launch(g, ctx, bb, s);
   }
   if (!b.L.out_edge && b.L.binop != GSPMM_DOT) {
     const uint32_t nb = source_blocks_for(g, b.L);
-    if (nb > 1) return launch_blocked(g, b, stream, nb);
+    if (nb > 1) return launch_blocked(g, b, s, nb);
   }
   if (b.L.binop == GSPMM_DOT && b.L.out_edge &&
       (b.L.lhs.mode != MODE_FULL || (b.L.lhs.ld % 2 == 0 && aligned(b.L.lhs.base, 8))) &&
       (b.L.rhs.mode != MODE_FULL || (b.L.rhs.ld % 2 == 0 && aligned(b.L.rhs.base, 8)))) {
     // edge-destined dots stream edge batches; needs the row of each edge
+    // (built once, completed before it is published to other streams)
     if (!g->d_rowof) {
-      CUDA_TRY(cudaMalloc(&g->d_rowof, sizeof(uint32_t) * std::max<uint64_t>(g->m, 1)),
+      uint32_t* rowof = nullptr;
+      CUDA_TRY(cudaMalloc(&rowof, sizeof(uint32_t) * std::max<uint64_t>(g->m, 1)),
                "row-of-edge array");
-      CUDA_TRY(launch_row_of_edge(g->d_indptr, g->num_rows, g->d_rowof, s), "row-of-edge");
+      cudaError_t e = launch_row_of_edge(g->d_indptr, g->num_rows, rowof, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) {
+        cudaFree(rowof);
+        return cuda_fail(e, "row-of-edge");
+      }
+      g->d_rowof = rowof;
     }
     err = launch_dot_edges(b.L, g->d_rowof, g->m, s);
   } else if (b.L.binop == GSPMM_DOT) {
     err = launch_dot(b.L, s);
-  } else if ((kind = plan_kernel(b.L, &rw)) != 0) {
+  } else if (planned(g, b.L, &rw)) {
     StreamLaunch p;
     p.row = b.L;
-    // plan level: rows gathering more than ~8 MB go to the long-row CTAs
-    // (measured: 4096 edges of 1 KB, 16384 of 400 B; heaviest segments run first)
+    // plan level: rows gathering more than ~8 MB run as long-row units
+    // (measured: 4096 edges of 1 KB, 16384 of 400 B); a row no heavier than
+    // half the average per-warp share of the segment work finishes inside
+    // the segment kernel's span and stays there
     const int slice_bytes = 4 * std::min(b.L.width, 256);
     uint32_t target = std::max<uint32_t>(1024, (8u << 20) / static_cast<uint32_t>(slice_bytes));
     {
-      // a row no heavier than half the average per-warp share of the
-      // segment work finishes inside the segment kernel's span: keep it there
-      // (measured: long-row CTAs stream a row slower per SM than warps do)
       const uint32_t slices = static_cast<uint32_t>((b.L.width + 255) / 256);
       const double warps = static_cast<double>(g->num_sms) * (b.L.width > 128 ? 32 : 24);
       const double half_share = 0.5 * static_cast<double>(g->m) * slices / warps;
@@ -538,161 +670,109 @@ int launch(gspmm_graph_s* g, Bound& b, void* stream) {
     const auto& lv = g->level[li];
     p.segs = lv.d_segs;
     p.n_segs = lv.num_segs;
-    p.long_rows = lv.d_long;
-    p.n_long = lv.num_long;
-    p.counter = g->d_counter;
     p.rhs_width = rw;
     const int W = b.L.width;
-    // one unit covers up to 640 columns for copy / scalar-weighted sums of
-    // gathered rows (gather_impl.cuh launch_wide), else <= 256-column slices
-    // (measured on cfg5, W = 602: 18.2 -> 16.0 ms)
-    // per-head weights on wide units: opt-in (GSPMM_WIDE_HEADS), measured
-    // slower on cfg4 (7.04 -> 7.51 ms: 128 registers, 20% idle quads at 512)
-    static const bool wide_heads = std::getenv("GSPMM_WIDE_HEADS") != nullptr;
-    static const bool wide_on = [] {
-      const char* v = std::getenv("GSPMM_WIDE_UNITS");
-      return !(v && std::strcmp(v, "0") == 0);
-    }();
-    // (W > 384: narrower rows would leave over 40% of the wide unit's
-    // lanes idle -- measured slower than two slices at W = 304)
-    const bool wide = wide_on && W > 384 && W <= 640 && b.L.reduce == R_SUM && !b.L.arg_other &&
+    // one segment unit covers up to 640 columns for copy / scalar-weighted
+    // sums of gathered rows (gather_impl.cuh launch_wide), else <= 256-column
+    // slices (measured on cfg5, W = 602: 18.2 -> 16.0 ms); W > 384 only:
+    // narrower rows would leave over 40% of the wide unit's lanes idle
+    // (measured slower than two slices at W = 304); per-head weights stay on
+    // 256-column slices (wide units measured slower on cfg4, 7.04 -> 7.51 ms)
+    const bool wide = W > 384 && W <= 640 && b.L.reduce == R_SUM && !b.L.arg_other &&
                       !b.L.arg_edge && b.L.lhs.role == ROLE_OTHER &&
-                      ((b.L.binop == B_COPY && !b.L.rhs.base) ||
-                       (b.L.binop == B_MUL && (rw == 1 || (wide_heads && rw > 1))));
+                      ((b.L.binop == B_COPY && !b.L.rhs.base) || (b.L.binop == B_MUL && rw == 1));
     p.seg_sw = wide ? W : W <= 256 ? W : 256;
     p.seg_slices = static_cast<uint32_t>((W + p.seg_sw - 1) / p.seg_sw);
-    static const uint32_t tma_min = env_u32("GSPMM_TMA_MIN_BYTES", 512);
-    p.tma_min_bytes = tma_min;
-    static const char* trace_path = std::getenv("GSPMM_UNIT_TRACE");
-    // development aid: per-unit timing of one launch, appended to a file
-    // (GSPMM_UNIT_TRACE_CONCURRENT=1: the launches of the call are not
-    // serialised; the buffers are read back after the join)
-    static const bool trace_conc = env_u32("GSPMM_UNIT_TRACE_CONCURRENT", 0) != 0;
-    struct Pending {
-      unsigned long long* d;
-      size_t bytes;
-      unsigned long long hdr[4];
-    };
-    std::vector<Pending> pending;
-    auto flush_trace = [&](cudaStream_t st) {
-      cudaStreamSynchronize(st);
-      for (auto& pd : pending) {
-        std::vector<unsigned long long> h(pd.bytes / sizeof(unsigned long long));
-        cudaMemcpy(h.data(), pd.d, pd.bytes, cudaMemcpyDeviceToHost);
-        if (FILE* f = std::fopen(trace_path, "ab")) {
-          std::fwrite(pd.hdr, sizeof(pd.hdr), 1, f);
-          std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
-          std::fclose(f);
-        }
-      }
-      pending.clear();
-    };
-    auto traced = [&](StreamLaunch q, cudaStream_t st, auto&& fn) -> cudaError_t {
-      if (!trace_path || !*trace_path) return fn(q, st);
-      const size_t bytes = sizeof(unsigned long long) * 4 * std::max<uint32_t>(q.n_units, 1);
-      // buffers cached per (mode, size): no allocation between the launches
-      static std::vector<std::pair<size_t, unsigned long long*>> cache[3];
-      unsigned long long* d = nullptr;
-      for (auto& c : cache[q.mode & 1]) if (c.first == bytes) d = c.second;
-      cudaError_t e2 = cudaSuccess;
-      if (!d) {
-        e2 = cudaMalloc(&d, bytes);
-        if (e2 != cudaSuccess) return e2;
-        cache[q.mode & 1].push_back({bytes, d});
-      }
-      cudaMemsetAsync(d, 0, bytes, st);
-      q.trace = d;
-      e2 = fn(q, st);
-      pending.push_back({d, bytes, {0xC0FFEEull, q.n_units, q.n_long_units,
-                                    static_cast<unsigned long long>(q.mode)}});
-      if (!trace_conc) flush_trace(st);
-      return e2;
-    };
-    if (kind == 2) {
-      // TMA variant: long rows as 32-column slices inside the same kernel
-      p.long_sw = W <= 32 ? W : 32;
-      p.long_slices = static_cast<uint32_t>((W + p.long_sw - 1) / p.long_sw);
-      p.n_long_units = p.n_long * p.long_slices;
-      p.n_units = p.n_long_units + p.n_segs * p.seg_slices;
-      err = traced(p, s, [](const StreamLaunch& q, cudaStream_t st) { return launch_stream(q, st); });
-    } else {
-      // Long rows (one per CTA, <= 256-column slices) run on the handle's
-      // side stream concurrently with the row segments: fork / join with
-      // events so the call stays ordered on the caller's stream.
+    err = cudaSuccess;
+    if (lv.num_long) {
+      // long rows first, alone on the GPU (every SM streams column units),
+      // then the segments: in the same stream, no side stream
+      const gspmm_graph_s::Units* units = nullptr;
+      const int st = long_units_for(g, li, W, &units);
+      if (st) return st;
       StreamLaunch pl = p;
       pl.mode = 1;
-      // long-row kernel: k_long_ws (default), k_long (GSPMM_LONG_KERNEL=ldg),
-      // k_long_tma (GSPMM_LONG_TMA=1)
-      static const char* lk = std::getenv("GSPMM_LONG_KERNEL");
-      static const bool long_tma = env_u32("GSPMM_LONG_TMA", 0) != 0;
-      static const bool long_ws = !long_tma && !(lk && std::strcmp(lk, "ldg") == 0);
-      // default: the LDGSTS CTAs; GSPMM_LONG_KERNEL=g4 selects the TMA
-      // gather4 CTAs, =ldg the register-staged ones (measured alternatives)
-      static const bool long_g4 = !long_tma && lk && std::strcmp(lk, "g4") == 0;
-      pl.long_ws = long_ws && !long_g4;
-      pl.long_g4 = long_g4;
-      static const int xl_sw = static_cast<int>(env_u32("GSPMM_XL_SW", long_g4 ? 128 : 64));
-      if (long_g4) {
-        // <= 256-column slices (the TMA box limit) of balanced width, boxes
-        // rounded up to 8 floats (four rows of a box are 128-byte aligned)
-        const int ns = (W + 255) / 256;
-        pl.long_sw = ((W + ns - 1) / ns + 7) & ~7;
-        pl.g4_box = pl.long_sw;
-        pl.g4_box_xl = (xl_sw + 7) & ~7;
-      } else if (long_ws) {
-        // <= 512-column slices of balanced width (16-byte multiples)
-        const int ns = (W + 511) / 512;
-        pl.long_sw = ((W + ns - 1) / ns + 3) & ~3;
-      } else {
-        pl.long_sw = W <= 256 ? W : 256;
-      }
-      pl.long_slices = static_cast<uint32_t>((W + pl.long_sw - 1) / pl.long_sw);
-      pl.long_tma = long_tma;
-      pl.xl_sw = long_g4 ? pl.g4_box_xl : xl_sw;
-      pl.n_xl = long_tma || W <= 32 || pl.xl_sw >= pl.long_sw ? 0 : lv.num_xl;
-      pl.xl_slices = static_cast<uint32_t>((W + pl.xl_sw - 1) / pl.xl_sw);
-      pl.n_xl_units = pl.n_xl * pl.xl_slices;
-      pl.n_long_units = pl.n_xl_units + (pl.n_long - pl.n_xl) * pl.long_slices;
-      pl.n_units = pl.n_long_units;
-      pl.counter = g->d_counter + 1;
-      {
-        // long-row CTAs ~3x the long rows' share of the edges (measured on the
-        // cfg2-4 shapes: a long-row CTA streams ~30 GB/s and holds a whole SM)
-        static const uint32_t forced = env_u32("GSPMM_LONG_CTAS", 0);
-        const double share = g->m ? static_cast<double>(lv.long_edges) / g->m : 0.0;
-        static const double factor = env_u32("GSPMM_LONG_FACTOR10", 30) / 10.0;
-        uint32_t c = forced ? forced : static_cast<uint32_t>(share * g->num_sms * factor + 1.0);
-        // the narrow slices of the heaviest rows must run side by side
-        c = std::max<uint32_t>(c, std::min<uint32_t>(pl.n_xl_units, g->num_sms / 2));
-        pl.long_ctas = std::min<uint32_t>(std::max<uint32_t>(c, 1), g->num_sms);
-      }
-      p.mode = 0;
-      p.n_long_units = 0;
-      p.n_units = p.n_segs * p.seg_slices;
-      auto run_gather = [](const StreamLaunch& q, cudaStream_t st) { return launch_gather(q, st); };
-      err = cudaSuccess;
-      if (pl.n_units) {
-        if (!g->side) {
-          CUDA_TRY(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking), "side stream");
-          CUDA_TRY(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming), "event");
-          CUDA_TRY(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming), "event");
-        }
-        CUDA_TRY(cudaEventRecord(g->ev_fork, s), "fork");
-        CUDA_TRY(cudaStreamWaitEvent(g->side, g->ev_fork, 0), "fork");
-        err = traced(pl, g->side, run_gather);
-        if (err == cudaSuccess) err = cudaEventRecord(g->ev_join, g->side);
-      }
-      if (err == cudaSuccess && p.n_units) err = traced(p, s, run_gather);
-      if (pl.n_units) {
-        cudaError_t ej = cudaStreamWaitEvent(s, g->ev_join, 0);
-        if (err == cudaSuccess) err = ej;
-      }
-      if (!pending.empty()) flush_trace(s);
+      pl.long_units = units->d;
+      pl.n_units = units->n;
+      pl.counter = ctx->d_counter + 1;
+      err = launch_gather(pl, s);
     }
+    p.mode = 0;
+    p.n_units = p.n_segs * p.seg_slices;
+    p.counter = ctx->d_counter;
+    if (err == cudaSuccess && p.n_units) err = launch_gather(p, s);
   } else {
     err = launch_rows(b.L, s);
   }
   if (err != cudaSuccess) return cuda_fail(err, "kernel launch");
+  return GSPMM_OK;
+}
+
+// Device plan levels (host indptr): long rows (heaviest first) and
+// edge-balanced segments of consecutive non-long rows, for each long-row
+// threshold.  Replaces the previous plan (gspmm_graph_set_plan).
+void free_plan(gspmm_graph_s* g) {
+  for (auto& lv : g->level) {
+    cudaFree(lv.d_long);
+    cudaFree(lv.d_segs);
+    lv = gspmm_graph_s::Level{};
+  }
+  for (auto& u : g->units) cudaFree(u.d);
+  g->units.clear();
+  g->n_levels = 0;
+}
+
+int build_plan(gspmm_graph_s* g, const uint32_t* indptr) {
+  free_plan(g);
+  const uint32_t seg_edges = g->seg_cost ? g->seg_cost : kSegEdges;
+  g->n_levels = g->forced_long ? 1 : 5;
+  for (int k = 0; k < g->n_levels; ++k) {
+    auto& lv = g->level[k];
+    lv.threshold = g->forced_long ? g->forced_long : kLevelThresholds[k];
+    std::vector<uint2> segs;
+    uint32_t begin = 0;
+    uint64_t acc = 0;
+    for (uint32_t r = 0; r < g->num_rows; ++r) {
+      const uint32_t deg = indptr[r + 1] - indptr[r];
+      if (deg > lv.threshold) {
+        lv.long_rows.push_back(r);
+        if (r > begin) segs.push_back(make_uint2(begin, r));
+        begin = r + 1;
+        acc = 0;
+        continue;
+      }
+      acc += deg + 2;  // cost: edges + per-row epilogue (empty rows are not free)
+      if (acc >= seg_edges) {
+        segs.push_back(make_uint2(begin, r + 1));
+        begin = r + 1;
+        acc = 0;
+      }
+    }
+    if (g->num_rows > begin) segs.push_back(make_uint2(begin, g->num_rows));
+    // heaviest segments first: a segment holding one near-threshold row is the
+    // longest unit, and it must not start last
+    std::stable_sort(segs.begin(), segs.end(), [&](const uint2& a, const uint2& b) {
+      return indptr[a.y] - indptr[a.x] > indptr[b.y] - indptr[b.x];
+    });
+    std::stable_sort(lv.long_rows.begin(), lv.long_rows.end(), [&](uint32_t a, uint32_t b) {
+      return indptr[a + 1] - indptr[a] > indptr[b + 1] - indptr[b];
+    });
+    for (uint32_t r : lv.long_rows) lv.long_deg.push_back(indptr[r + 1] - indptr[r]);
+    lv.num_long = static_cast<uint32_t>(lv.long_rows.size());
+    lv.num_segs = static_cast<uint32_t>(segs.size());
+    CUDA_TRY(cudaMalloc(&lv.d_long, sizeof(uint32_t) * std::max<size_t>(lv.num_long, 1)),
+             "cudaMalloc plan");
+    CUDA_TRY(cudaMalloc(&lv.d_segs, sizeof(uint2) * std::max<size_t>(segs.size(), 1)),
+             "cudaMalloc segments");
+    if (lv.num_long)
+      CUDA_TRY(cudaMemcpy(lv.d_long, lv.long_rows.data(), sizeof(uint32_t) * lv.num_long,
+                          cudaMemcpyHostToDevice),
+               "upload plan");
+    if (!segs.empty())
+      CUDA_TRY(cudaMemcpy(lv.d_segs, segs.data(), sizeof(uint2) * segs.size(),
+                          cudaMemcpyHostToDevice),
+               "upload segments");
+  }
   return GSPMM_OK;
 }
 
@@ -825,62 +905,8 @@ int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
   g->m = m;
   cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
 
-  // Device plan levels: long rows (heaviest first) and edge-balanced
-  // segments of consecutive non-long rows, for each long-row threshold.
-  const uint32_t seg_edges = env_u32("GSPMM_SEG_EDGES", kSegEdges);
-  const uint32_t forced_long = env_u32("GSPMM_LONG_EDGES", 0);
-  const uint32_t thresholds[5] = {1024, kLongEdges, 16384, 32768, 65536};
-  g->n_levels = forced_long ? 1 : 5;
-  std::vector<uint32_t> long_rows[5];
-  std::vector<uint2> segs[5];
-  for (int k = 0; k < g->n_levels; ++k) {
-    auto& lv = g->level[k];
-    lv.threshold = forced_long ? forced_long : thresholds[k];
-    uint32_t begin = 0;
-    uint64_t acc = 0;
-    for (uint32_t r = 0; r < num_rows; ++r) {
-      const uint32_t deg = indptr[r + 1] - indptr[r];
-      if (deg > lv.threshold) {
-        long_rows[k].push_back(r);
-        lv.long_edges += deg;
-        if (r > begin) segs[k].push_back(make_uint2(begin, r));
-        begin = r + 1;
-        acc = 0;
-        continue;
-      }
-      acc += deg + 2;  // cost: edges + per-row epilogue (empty rows are not free)
-      if (acc >= seg_edges) {
-        segs[k].push_back(make_uint2(begin, r + 1));
-        begin = r + 1;
-        acc = 0;
-      }
-    }
-    if (num_rows > begin) segs[k].push_back(make_uint2(begin, num_rows));
-    // heaviest segments first: a segment holding one near-threshold row is the
-    // longest unit, and it must not start last
-    std::stable_sort(segs[k].begin(), segs[k].end(), [&](const uint2& a, const uint2& b) {
-      return indptr[a.y] - indptr[a.x] > indptr[b.y] - indptr[b.x];
-    });
-    std::stable_sort(long_rows[k].begin(), long_rows[k].end(), [&](uint32_t a, uint32_t b) {
-      return indptr[a + 1] - indptr[a] > indptr[b + 1] - indptr[b];
-    });
-    lv.num_long = static_cast<uint32_t>(long_rows[k].size());
-    const uint32_t xl_edges = env_u32("GSPMM_XL_EDGES", kXlEdges);
-    for (uint32_t r : long_rows[k])
-      if (indptr[r + 1] - indptr[r] > xl_edges) ++lv.num_xl;
-    lv.num_segs = static_cast<uint32_t>(segs[k].size());
-  }
-
   auto cleanup = [&](cudaError_t e, const char* where) {
-    cudaFree(g->d_indptr);
-    cudaFree(g->d_indices);
-    cudaFree(g->d_eids);
-    for (auto& lv : g->level) {
-      cudaFree(lv.d_long);
-      cudaFree(lv.d_segs);
-    }
-    cudaFree(g->d_counter);
-    delete g;
+    destroy_graph(g);
     return cuda_fail(e, where);
   };
   cudaError_t e;
@@ -902,25 +928,11 @@ int gspmm_graph_create(int device, int orientation, uint32_t num_rows,
         cudaSuccess)
       return cleanup(e, "upload edge_ids");
   }
-  for (int k = 0; k < g->n_levels; ++k) {
-    auto& lv = g->level[k];
-    if ((e = cudaMalloc(&lv.d_long, sizeof(uint32_t) * std::max<size_t>(long_rows[k].size(), 1))) !=
-        cudaSuccess)
-      return cleanup(e, "cudaMalloc plan");
-    if ((e = cudaMalloc(&lv.d_segs, sizeof(uint2) * std::max<size_t>(segs[k].size(), 1))) !=
-        cudaSuccess)
-      return cleanup(e, "cudaMalloc segments");
-    if (!long_rows[k].empty() &&
-        (e = cudaMemcpy(lv.d_long, long_rows[k].data(), sizeof(uint32_t) * long_rows[k].size(),
-                        cudaMemcpyHostToDevice)) != cudaSuccess)
-      return cleanup(e, "upload plan");
-    if (!segs[k].empty() &&
-        (e = cudaMemcpy(lv.d_segs, segs[k].data(), sizeof(uint2) * segs[k].size(),
-                        cudaMemcpyHostToDevice)) != cudaSuccess)
-      return cleanup(e, "upload segments");
+  const int st = build_plan(g, indptr);
+  if (st) {
+    destroy_graph(g);
+    return st;
   }
-  if ((e = cudaMalloc(&g->d_counter, 2 * sizeof(uint32_t))) != cudaSuccess)
-    return cleanup(e, "cudaMalloc counter");
   *out = g;
   return GSPMM_OK;
 }
@@ -947,6 +959,18 @@ int gspmm_build_csr_device(uint32_t n, int64_t m, const uint32_t* d_src, const u
   if (orientation != GSPMM_SRC_MAJOR && orientation != GSPMM_DST_MAJOR)
     return fail(GSPMM_ERR_ARG, "orientation must be 0 (src-major) or 1 (dst-major)");
   if (static_cast<uint64_t>(m) > 0xffffffffull) return fail(GSPMM_ERR_ARG, "more than 2^32 - 1 edges");
+  // build_csr's id check (csr.cpp:79-86): the lowest offending edge
+  uint64_t bad = ~0ull;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(check_edge_ids(n, static_cast<uint64_t>(m), d_src, d_dst, cs, &bad), "build_csr_device");
+  if (bad != ~0ull) {
+    uint32_t ids[2] = {0, 0};
+    CUDA_TRY(cudaMemcpy(&ids[0], d_src + bad, 4, cudaMemcpyDeviceToHost), "build_csr_device");
+    CUDA_TRY(cudaMemcpy(&ids[1], d_dst + bad, 4, cudaMemcpyDeviceToHost), "build_csr_device");
+    return fail(GSPMM_ERR_STRUCTURE, "edge " + std::to_string(bad) + " references node id " +
+                                         std::to_string(std::max(ids[0], ids[1])) +
+                                         " >= num_nodes " + std::to_string(n));
+  }
   const cudaError_t e = launch_build_csr(n, static_cast<uint64_t>(m), d_src, d_dst,
                                          orientation == GSPMM_DST_MAJOR, d_indptr, d_indices,
                                          d_edge_ids, static_cast<cudaStream_t>(stream));
@@ -977,8 +1001,32 @@ int gspmm_graph_destroy(gspmm_graph g) {
 int gspmm_graph_set_source_blocks(gspmm_graph g, int nblocks) {
   if (!g) return fail(GSPMM_ERR_ARG, "null graph handle");
   if (nblocks < 0) return fail(GSPMM_ERR_ARG, "nblocks must be >= 0");
+  std::lock_guard<std::recursive_mutex> lock(g->mu);
   g->blocks_pref = nblocks;
   return GSPMM_OK;
+}
+
+int gspmm_graph_set_plan(gspmm_graph g, const gspmm_plan* plan) {
+  if (!g) return fail(GSPMM_ERR_ARG, "null graph handle");
+  const gspmm_plan dflt{};
+  if (!plan) plan = &dflt;
+  if (plan->unit_cols % 4 || plan->unit_cols > 512 || plan->kernel < 0 || plan->kernel > 1)
+    return fail(GSPMM_ERR_ARG, "plan: unit_cols must be a multiple of 4 up to 512, kernel 0 or 1");
+  std::lock_guard<std::recursive_mutex> lock(g->mu);
+  CUDA_TRY(cudaSetDevice(g->device), "cudaSetDevice");
+  // in-flight calls may still read the old plan
+  CUDA_TRY(cudaDeviceSynchronize(), "set_plan");
+  g->seg_cost = plan->seg_cost;
+  g->forced_long = plan->long_threshold;
+  g->unit_cols = plan->unit_cols;
+  g->rows_kernel_only = plan->kernel;
+  for (auto* sg : g->blocks) destroy_graph(sg);
+  g->blocks.clear();
+  g->block_nb = 0;
+  std::vector<uint32_t> h(static_cast<size_t>(g->num_rows) + 1);
+  CUDA_TRY(cudaMemcpy(h.data(), g->d_indptr, sizeof(uint32_t) * h.size(), cudaMemcpyDeviceToHost),
+           "download indptr");
+  return build_plan(g, h.data());
 }
 
 }  // extern "C"
@@ -987,22 +1035,12 @@ namespace {
 void destroy_graph(gspmm_graph_s* g) {
   cudaSetDevice(g->device);
   for (auto* sg : g->blocks) destroy_graph(sg);
+  free_plan(g);
+  free_contexts(g);
   cudaFree(g->d_indptr);
   cudaFree(g->d_indices);
   cudaFree(g->d_eids);
-  for (auto& lv : g->level) {
-    cudaFree(lv.d_long);
-    cudaFree(lv.d_segs);
-  }
-  cudaFree(g->d_counter);
   cudaFree(g->d_rowof);
-  if (g->side) {
-    cudaStreamDestroy(g->side);
-    cudaEventDestroy(g->ev_fork);
-    cudaEventDestroy(g->ev_join);
-  }
-  cudaFree(g->ws);
-  cudaFree(g->dws);
   delete g;
 }
 }  // namespace
@@ -1061,8 +1099,7 @@ int gspmm_binary_reduce_ex(gspmm_graph g, const gspmm_config* cfg,
   int st = bind(g, cfg, u, v, e, out, opt, &b);
   if (st) return st;
   if (!out) return fail(GSPMM_ERR_SHAPE, "missing output matrix");
-  CUDA_TRY(cudaSetDevice(g->device), "cudaSetDevice");
-  return launch(g, b, stream);
+  return run_call(g, b, static_cast<cudaStream_t>(stream));
 }
 
 int gspmm_binary_reduce(gspmm_graph g, const gspmm_config* cfg,
@@ -1112,25 +1149,30 @@ static int softmax_common(gspmm_graph g, bool backward, const gspmm_mat* l, cons
     return fail(GSPMM_ERR_ARG, "edge_softmax: a and grad_a must share one edge order");
   if (m && (!l->data || !out->data || (backward && !ga->data)))
     return fail(GSPMM_ERR_ARG, "null data");
+  std::lock_guard<std::recursive_mutex> lock(g->mu);
   CUDA_TRY(cudaSetDevice(g->device), "cudaSetDevice");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CallCtx* ctx = nullptr;
+  if ((st = context_for(g, s, &ctx))) return st;
   const auto& lv = g->level[0];
-  if (lv.num_long && !g->side) {
-    CUDA_TRY(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking), "side stream");
-    CUDA_TRY(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming), "event");
-    CUDA_TRY(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming), "event");
+  if (lv.num_long && !ctx->side) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "side stream");
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming), "event");
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming), "event");
   }
+  if ((st = begin_call(ctx, s))) return st;
   SideStream side;
-  side.stream = g->side;
-  side.fork = g->ev_fork;
-  side.join = g->ev_join;
+  side.stream = ctx->side;
+  side.fork = ctx->fork;
+  side.join = ctx->join;
   const cudaError_t e = launch_edge_softmax(
       backward, g->d_indptr, g->d_eids, g->num_rows, static_cast<int>(heads),
       l->edge_order == GSPMM_EDGE_BY_POS, l->data, l->ld ? l->ld : heads,
       backward ? ga->data : nullptr, backward ? (ga->ld ? ga->ld : heads) : 0, out->data,
-      out->ld ? out->ld : heads, lv.d_long, lv.num_long, lv.threshold, g->num_sms,
-      static_cast<cudaStream_t>(stream), side);
+      out->ld ? out->ld : heads, lv.d_long, lv.num_long, lv.threshold, g->num_sms, s, side);
+  st = end_call(ctx, s);
   if (e != cudaSuccess) return cuda_fail(e, "edge_softmax");
-  return GSPMM_OK;
+  return st;
 }
 
 int gspmm_edge_softmax(gspmm_graph g, const gspmm_mat* logits, const gspmm_out* out,
@@ -1143,22 +1185,32 @@ int gspmm_edge_softmax_backward(gspmm_graph g, const gspmm_mat* a, const gspmm_m
   return softmax_common(g, true, a, grad_a, grad_logits, stream);
 }
 
+int gspmm_argmax_backward_range(const int32_t* arg, int64_t rows, int64_t dim,
+                                int64_t arg_ld, const float* grad_out, int64_t grad_ld,
+                                float* grad_src, int64_t src_lo, int64_t src_rows,
+                                int64_t src_ld, void* stream) {
+  if (rows < 0 || dim < 0 || src_lo < 0 || src_rows < 0)
+    return fail(GSPMM_ERR_ARG, "argmax_backward: negative size");
+  if ((rows && dim && (!arg || !grad_out)) || (src_rows && dim && !grad_src))
+    return fail(GSPMM_ERR_ARG, "null argument");
+  if ((arg_ld && arg_ld < dim) || (grad_ld && grad_ld < dim) || (src_ld && src_ld < dim))
+    return fail(GSPMM_ERR_SHAPE, "argmax_backward: a row stride is below the width");
+  if (!src_rows || !dim) return GSPMM_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  retain_pool_memory();
+  cudaError_t e = launch_argmax_backward(arg, rows, dim, arg_ld ? arg_ld : dim, grad_out,
+                                         grad_ld ? grad_ld : dim, grad_src, src_lo, src_rows,
+                                         src_ld ? src_ld : dim, s);
+  if (e != cudaSuccess) return cuda_fail(e, "argmax_backward");
+  return GSPMM_OK;
+}
+
 int gspmm_argmax_backward(const int32_t* arg, int64_t rows, int64_t dim,
                           int64_t arg_ld, const float* grad_out, int64_t grad_ld,
                           float* grad_src, int64_t src_rows, int64_t src_ld,
                           void* stream) {
-  if (!arg || !grad_out || !grad_src) return fail(GSPMM_ERR_ARG, "null argument");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  retain_pool_memory();
-  double* acc = nullptr;
-  const size_t bytes = sizeof(double) * std::max<int64_t>(src_rows * dim, 1);
-  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&acc), bytes, s), "argmax workspace");
-  cudaError_t e = launch_argmax_backward(arg, rows, dim, arg_ld ? arg_ld : dim, grad_out,
-                                         grad_ld ? grad_ld : dim, grad_src, src_rows,
-                                         src_ld ? src_ld : dim, acc, s);
-  cudaFreeAsync(acc, s);
-  if (e != cudaSuccess) return cuda_fail(e, "argmax_backward");
-  return GSPMM_OK;
+  return gspmm_argmax_backward_range(arg, rows, dim, arg_ld, grad_out, grad_ld, grad_src, 0,
+                                     src_rows, src_ld, stream);
 }
 
 static int host_call(gspmm_graph g, const gspmm_config* cfg, const gspmm_mat* u,
@@ -1181,6 +1233,10 @@ int gspmm_binary_reduce_host_async(gspmm_graph g, const gspmm_config* cfg,
   return host_call(g, cfg, u, v, e, out, opt, stream, false, wait_event, upload_event);
 }
 
+// The host-buffer entries stage through a stream-ordered allocation of the
+// caller's stream (the device pool keeps freed memory mapped, so a steady
+// stream of calls re-uses one block): concurrent calls on other streams or
+// threads never share a staging buffer.
 static int host_call(gspmm_graph g, const gspmm_config* cfg, const gspmm_mat* u,
                      const gspmm_mat* v, const gspmm_mat* e, const gspmm_out* out,
                      const gspmm_options* opt, void* stream, bool sync, void* wait_event,
@@ -1190,10 +1246,8 @@ static int host_call(gspmm_graph g, const gspmm_config* cfg, const gspmm_mat* u,
   Bound probe;
   int st = bind(g, cfg, u, v, e, out, opt, &probe);
   if (st) return st;
-  if (opt && opt->other_scale)
-    return fail(GSPMM_ERR_ARG, "other_scale is a device-side option");
-  std::lock_guard<std::mutex> lock(g->mu);
   CUDA_TRY(cudaSetDevice(g->device), "cudaSetDevice");
+  retain_pool_memory();
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const gspmm_mat* in[3] = {u, v, e};
   size_t sz[3], total = 0;
@@ -1207,33 +1261,46 @@ static int host_call(gspmm_graph g, const gspmm_config* cfg, const gspmm_mat* u,
       out->rows ? static_cast<size_t>((out->rows - 1) * arg_ld + out->dim) * sizeof(int32_t) : 0;
   const bool ao = opt && opt->arg_other, ae = opt && opt->arg_edge;
   total += (ao ? round_up(arg_bytes) : 0) + (ae ? round_up(arg_bytes) : 0);
-  if (total > g->ws_bytes) {
-    cudaFree(g->ws);
-    g->ws = nullptr;
-    g->ws_bytes = 0;
-    CUDA_TRY(cudaMalloc(&g->ws, total), "workspace");
-    g->ws_bytes = total;
-  }
-  char* p = static_cast<char*>(g->ws);
+  // other_scale: a HOST array over the gathered (other) endpoint's nodes
+  const size_t scale_bytes =
+      opt && opt->other_scale ? sizeof(float) * static_cast<size_t>(g->num_cols) : 0;
+  total += round_up(scale_bytes);
   if (wait_event)
     CUDA_TRY(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(wait_event), 0), "wait event");
+  void* ws = nullptr;
+  CUDA_TRY(cudaMallocAsync(&ws, std::max<size_t>(total, 256), s), "host-call workspace");
+  char* p = static_cast<char*>(ws);
+  auto bail = [&](cudaError_t err, const char* where) {
+    cudaFreeAsync(ws, s);
+    return cuda_fail(err, where);
+  };
+  cudaError_t ce;
   gspmm_mat dev[3];
   const gspmm_mat* dptr[3] = {nullptr, nullptr, nullptr};
   for (int i = 0; i < 3; ++i) {
     if (!in[i] || !in[i]->data) continue;
     dev[i] = *in[i];
     dev[i].data = reinterpret_cast<const float*>(p);
-    CUDA_TRY(cudaMemcpyAsync(p, in[i]->data, sz[i], cudaMemcpyHostToDevice, s), "H2D operand");
+    if ((ce = cudaMemcpyAsync(p, in[i]->data, sz[i], cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return bail(ce, "H2D operand");
     dptr[i] = &dev[i];
     p += round_up(sz[i]);
   }
-  if (upload_event)
-    CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(upload_event), s), "upload event");
+  gspmm_options dopt{};
+  if (opt) dopt = *opt;
+  if (scale_bytes) {
+    if ((ce = cudaMemcpyAsync(p, opt->other_scale, scale_bytes, cudaMemcpyHostToDevice, s)) !=
+        cudaSuccess)
+      return bail(ce, "H2D scale");
+    dopt.other_scale = reinterpret_cast<const float*>(p);
+    p += round_up(scale_bytes);
+  }
+  if (upload_event && (ce = cudaEventRecord(static_cast<cudaEvent_t>(upload_event), s)) !=
+                          cudaSuccess)
+    return bail(ce, "upload event");
   gspmm_out dout = *out;
   dout.data = reinterpret_cast<float*>(p);
   p += round_up(out_bytes);
-  gspmm_options dopt{};
-  if (opt) dopt = *opt;
   if (ao) {
     dopt.arg_other = reinterpret_cast<int32_t*>(p);
     p += round_up(arg_bytes);
@@ -1243,16 +1310,76 @@ static int host_call(gspmm_graph g, const gspmm_config* cfg, const gspmm_mat* u,
     p += round_up(arg_bytes);
   }
   st = gspmm_binary_reduce_ex(g, cfg, dptr[0], dptr[1], dptr[2], &dout, &dopt, stream);
-  if (st) return st;
-  CUDA_TRY(cudaMemcpyAsync(out->data, dout.data, out_bytes, cudaMemcpyDeviceToHost, s), "D2H out");
-  if (ao)
-    CUDA_TRY(cudaMemcpyAsync(opt->arg_other, dopt.arg_other, arg_bytes, cudaMemcpyDeviceToHost, s),
-             "D2H arg");
-  if (ae)
-    CUDA_TRY(cudaMemcpyAsync(opt->arg_edge, dopt.arg_edge, arg_bytes, cudaMemcpyDeviceToHost, s),
-             "D2H arg");
+  if (st) {
+    cudaFreeAsync(ws, s);
+    return st;
+  }
+  if ((ce = cudaMemcpyAsync(out->data, dout.data, out_bytes, cudaMemcpyDeviceToHost, s)) !=
+      cudaSuccess)
+    return bail(ce, "D2H out");
+  if (ao && (ce = cudaMemcpyAsync(opt->arg_other, dopt.arg_other, arg_bytes,
+                                  cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return bail(ce, "D2H arg");
+  if (ae && (ce = cudaMemcpyAsync(opt->arg_edge, dopt.arg_edge, arg_bytes,
+                                  cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return bail(ce, "D2H arg");
+  CUDA_TRY(cudaFreeAsync(ws, s), "host-call workspace");
   if (sync) CUDA_TRY(cudaStreamSynchronize(s), "synchronize");
   return GSPMM_OK;
+}
+
+// Host-buffer argmax backward: arg and grad_out uploaded, grad_src read back
+// (the same stream-ordered staging as host_call).
+static int argmax_host(const int32_t* arg, int64_t rows, int64_t dim, const float* grad_out,
+                       float* grad_src, int64_t src_rows, int device, void* stream, bool sync,
+                       void* wait_event, void* upload_event) {
+  if (rows < 0 || dim < 0 || src_rows < 0) return fail(GSPMM_ERR_ARG, "negative size");
+  if ((rows && dim && (!arg || !grad_out)) || (src_rows && dim && !grad_src))
+    return fail(GSPMM_ERR_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(device), "cudaSetDevice");
+  retain_pool_memory();
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t ab = sizeof(int32_t) * static_cast<size_t>(rows * dim);
+  const size_t gb = sizeof(float) * static_cast<size_t>(rows * dim);
+  const size_t ob = sizeof(float) * static_cast<size_t>(src_rows * dim);
+  if (wait_event)
+    CUDA_TRY(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(wait_event), 0), "wait event");
+  void* ws = nullptr;
+  CUDA_TRY(cudaMallocAsync(&ws, std::max<size_t>(round_up(ab) + round_up(gb) + round_up(ob), 256), s),
+           "host-call workspace");
+  char* p = static_cast<char*>(ws);
+  int32_t* da = reinterpret_cast<int32_t*>(p);
+  float* dg = reinterpret_cast<float*>(p + round_up(ab));
+  float* dout = reinterpret_cast<float*>(p + round_up(ab) + round_up(gb));
+  cudaError_t ce = cudaMemcpyAsync(da, arg, ab, cudaMemcpyHostToDevice, s);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(dg, grad_out, gb, cudaMemcpyHostToDevice, s);
+  if (ce == cudaSuccess && upload_event)
+    ce = cudaEventRecord(static_cast<cudaEvent_t>(upload_event), s);
+  int st = GSPMM_OK;
+  if (ce == cudaSuccess)
+    st = gspmm_argmax_backward(da, rows, dim, 0, dg, 0, dout, src_rows, 0, stream);
+  if (ce == cudaSuccess && st == GSPMM_OK)
+    ce = cudaMemcpyAsync(grad_src, dout, ob, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(ws, s);
+  if (ce != cudaSuccess) return cuda_fail(ce, "argmax_backward_host");
+  if (st) return st;
+  if (sync) CUDA_TRY(cudaStreamSynchronize(s), "synchronize");
+  return GSPMM_OK;
+}
+
+int gspmm_argmax_backward_host(const int32_t* arg, int64_t rows, int64_t dim,
+                               const float* grad_out, float* grad_src, int64_t src_rows,
+                               int device, void* stream) {
+  return argmax_host(arg, rows, dim, grad_out, grad_src, src_rows, device, stream, true, nullptr,
+                     nullptr);
+}
+
+int gspmm_argmax_backward_host_async(const int32_t* arg, int64_t rows, int64_t dim,
+                                     const float* grad_out, float* grad_src, int64_t src_rows,
+                                     int device, void* stream, void* wait_event,
+                                     void* upload_event) {
+  return argmax_host(arg, rows, dim, grad_out, grad_src, src_rows, device, stream, false,
+                     wait_event, upload_event);
 }
 
 }  // extern "C"

@@ -118,16 +118,10 @@ __global__ void __launch_bounds__(kDotWarps * 32) k_dot(const RowLaunch p) {
 template <int V, int ROP>
 cudaError_t launch_dv(const RowLaunch& p, cudaStream_t s) {
   const size_t smem = sizeof(float) * kDotWarps * 32 * (32 * V + 1);
-  // the attribute is per device: set it again whenever the calling device
-  // differs from the last one configured (as the gather launchers do)
-  static int configured_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (configured_dev != dev) {
-    const cudaError_t e = cudaFuncSetAttribute(
-        k_dot<V, ROP>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  {
+    const cudaError_t e = set_max_dynamic_smem(reinterpret_cast<const void*>(k_dot<V, ROP>),
+                                               static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    configured_dev = dev;
   }
   const int64_t blocks = (static_cast<int64_t>(p.num_rows) + kDotWarps - 1) / kDotWarps;
   if (blocks == 0) return cudaSuccess;
@@ -390,14 +384,10 @@ cudaError_t launch_dot_edges(const RowLaunch& p, const uint32_t* rowof, uint64_t
   if (p.lhs.mode == MODE_FULL && p.rhs.mode == MODE_FULL && p.gather_dim % 4 == 0 &&
       p.lhs.ld % 4 == 0 && p.rhs.ld % 4 == 0 && al16(p.lhs.base) && al16(p.rhs.base)) {
     const size_t smem = sizeof(float) * kEd4Warps * 32 * kEd4Stride;
-    static int configured_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (configured_dev != dev) {
-      const cudaError_t e = cudaFuncSetAttribute(
-          k_dot_edges4, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    {
+      const cudaError_t e = set_max_dynamic_smem(reinterpret_cast<const void*>(k_dot_edges4),
+                                                 static_cast<int>(smem));
       if (e != cudaSuccess) return e;
-      configured_dev = dev;
     }
     const uint64_t batches = (m + 31) / 32;
     uint64_t blocks = (batches + kEd4Warps - 1) / kEd4Warps;

@@ -1,30 +1,26 @@
 // gather_impl.cuh -- the production owner-computes row kernel (sm_100a),
 // instantiated per binary operator in gather_{copy,mul,arith}.cu.
 //
-// Same semantics as rows.cu / stream.cu (the reference's RowParallelSpmm
-// left fold, kernels.cpp:162-195, bit for bit), built from measurements on
-// B200 (scripts/mb_gather.cu, profiles/):
+// Same semantics as rows.cu (the reference's RowParallelSpmm left fold,
+// kernels.cpp:162-195, bit for bit), built from measurements on B200
+// (scripts/mb_gather.cu, profiles/):
 //
 //   * random source-row gathers run fastest as 128-bit LDGs into registers
 //     (7.2 TB/s for 1 KB rows, 5.0 TB/s for 400 B rows) -- faster than one
 //     TMA bulk copy per row (5.9 / 1.8 TB/s), whose per-SM request rate caps
-//     small rows; so rows are gathered with LDG.128 into a register
-//     ping-pong: the next batch's loads are in flight while the current
-//     batch is folded;
-//   * persistent CTAs pull WORK UNITS (the device plan: edge-balanced
-//     segments of consecutive rows, and column slices of long rows) from a
-//     global counter, first units interleaved across SMs;
-//   * WIDE units: lanes own 4 (or 8) output columns, one edge per warp load
-//     instruction (512 B or 1 KB);  NARROW units (32-column slices of long
-//     rows): lane = (edge group g, column quad i), four edges per warp load
-//     instruction; the four edges are then folded in order by the column
-//     owners through warp shuffles -- the fold stays sequential per column;
-//   * neighbour ids / scalar edge operands arrive as coalesced 32-edge
-//     windows prefetched one window (NARROW: two) ahead and broadcast with
-//     shuffles; row ends likewise;
-//   * fused epilogue: zero-degree fixup, mean, argmax; each output row is
-//     written exactly once.
+//     small rows, and than LDGSTS (3.6 / 1.4 TB/s); so rows are gathered with
+//     LDG.128 into registers, in both kernels;
+//   * k_gather: persistent warps pull SEGMENT UNITS (edge-balanced runs of
+//     consecutive short rows, one column slice each) from a global counter;
+//     lanes own 4 (or 8, or 20) output columns, one edge per warp load
+//     instruction; neighbour ids / scalar edge operands arrive as coalesced
+//     32-edge windows prefetched one window ahead and broadcast with
+//     shuffles; a batch of U edges is loaded, then folded in edge order;
+//   * k_long_rg: one CTA per COLUMN UNIT of a long row (see below);
+//   * fused epilogue: zero-degree fixup, mean, argmax; each output element
+//     is written exactly once.
 #pragma once
+#include <atomic>
 #include <type_traits>
 #include "device_ops.cuh"
 #include "stream.h"
@@ -64,12 +60,6 @@ constexpr int kThreads = 256;
 #endif
 #ifndef GATHER_STREAM_IN
 #define GATHER_STREAM_IN 1
-#endif
-// L2 prefetch distance of the segment kernel, in batches (0 = off).
-// Measured slower at every distance (cfg2 1.82 -> 1.89 / 1.91 / 2.01 ms at
-// 2 / 4 / 8 batches; uniform er256 2.41 -> 3.96 ms at 8): kept for study.
-#ifndef GATHER_PF
-#define GATHER_PF 0
 #endif
 #ifndef GATHER_MINB5
 #define GATHER_MINB5 2
@@ -304,22 +294,6 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
     }
     const uint32_t jb = u.e0 + b * U;
     const uint32_t n = min(static_cast<uint32_t>(U), u.e1 - jb);
-    if constexpr (GATHER_PF > 0 && LO) {
-      // L2 prefetch of the rows GATHER_PF batches ahead: memory-level
-      // parallelism beyond the registers' ping-pong, at one instruction per
-      // lane (lane = (edge, 128-byte line of its slice))
-      constexpr int kLines = VPL * 4;  // 128-byte lines per <= VPL*128-column slice
-      constexpr int kEdges = 32 / kLines < U ? 32 / kLines : U;
-      const uint32_t q = (b + GATHER_PF) * U + static_cast<uint32_t>(lane / kLines);  // unit edge
-      const int line = lane % kLines;
-      const uint32_t src_lane = q & 31u;
-      const uint32_t o_cur = __shfl_sync(kFull, win_o, src_lane);
-      const uint32_t o_nxt = __shfl_sync(kFull, nxt_o, src_lane);
-      const uint32_t wq = q / 32u, wb = b / static_cast<uint32_t>(kPerWin);
-      if (lane / kLines < kEdges && u.e0 + q < u.e1 && line * 32 < u.cw && (wq == wb || wq == wb + 1))
-        prefetch_l2(reinterpret_cast<const char*>(L.lhs.base + u.c0 + line * 32) +
-                    static_cast<uint64_t>(wq == wb ? o_cur : o_nxt) * ldb);
-    }
     float4 x[U][VPL];
     float r[U][SK == SK_HEAD ? VPL : 1];
     uint32_t okey[ARG == 2 ? U : 1];  // ARG 2: the neighbour id of each edge
@@ -396,299 +370,78 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
 }
 
 // -------------------------------------------------------------- LONG ROWS
-// One column slice (32 / 64 / 128 / 256 floats) of one long row per CTA: the
-// 16 warps gather a round of R edges with LDG.128 into registers while the
-// previous round, staged in shared memory, is folded by the column owners
-// (thread t owns column t) in canonical edge order.  A lone warp cannot keep
-// enough bytes in flight for a 66k-329k-edge row (one owner must see every
-// edge in order); a CTA keeps ~128 KB in flight, and the heaviest rows are
-// cut into narrow slices so several CTAs on several SMs stream one row.
-// Narrow slices pack epi = 128 / slice edges into each warp load instruction
-// (lane = edge group g x column quad i).
-constexpr int kLongThreads = 512;
-
-// Shared memory is carved out of the same 228 KB as L1, and L1 tracks the
-// in-flight LDG misses: the round buffer is kept at 96 KB (measured: a 192 KB
-// carve-out halved the long-row stream rate).
-template <int VPL>
-struct LongGeom {
-  static constexpr int U = VPL == 1 ? 12 : 6;          // load instructions per warp per round
-  static constexpr int kWarps = kLongThreads / 32;
-  static constexpr int kMaxSmall = 16;                  // staged small floats per edge
-  // round: R = kWarps * U * epi edges of slot_f floats; slot_f * epi = 128
-  // for narrow slices, 128 * VPL otherwise -> the data buffer is constant
-  static constexpr size_t data_floats() { return static_cast<size_t>(kWarps) * U * 128 * VPL; }
-  static constexpr size_t max_edges() { return static_cast<size_t>(kWarps) * U * 4; }
-  static constexpr size_t smem_bytes(int rws) {
-    return sizeof(float) * (data_floats() + max_edges() * static_cast<size_t>(rws));
-  }
-};
-
-template <int VPL, int BOP, int ROP, bool ARG, bool SMALL>
-__global__ void __launch_bounds__(kLongThreads, 1) k_long(const StreamLaunch p) {
-  using G = LongGeom<VPL>;
-  constexpr int U = G::U;
-  extern __shared__ __align__(16) float sm[];
-  __shared__ uint32_t s_unit;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const RowLaunch& L = p.row;
-  const int rw = SMALL ? p.rhs_width : 0;
-  const bool scale_on = SMALL && L.other_scale != nullptr;
-  const int rws = SMALL ? (rw > 0 ? rw : 1) : 0;  // staged small floats per edge
-  const bool need_eid = L.lhs.role == ROLE_EID || (rw && L.rhs.role == ROLE_EID);
-  float* buf = sm;
-  float* sbuf = sm + G::data_floats();
-
-  for (;;) {
-    if (tid == 0) s_unit = atomicAdd(p.counter, 1u);
-    __syncthreads();
-    const uint32_t unit = s_unit;
-    __syncthreads();
-    if (unit >= p.n_units) break;
-    const unsigned long long t0 = p.trace ? globaltimer_ns() : 0ull;
-    // units: first the narrow slices of the heaviest rows, then wide slices
-    uint32_t li, slc;
-    int sw;
-    if (unit < p.n_xl_units) {
-      li = unit / p.xl_slices;
-      slc = unit - li * p.xl_slices;
-      sw = p.xl_sw;
-    } else {
-      const uint32_t v = unit - p.n_xl_units;
-      li = p.n_xl + v / p.long_slices;
-      slc = v - (li - p.n_xl) * p.long_slices;
-      sw = p.long_sw;
-    }
-    const uint32_t r = __ldg(p.long_rows + li);
-    const int c0 = static_cast<int>(slc) * sw;
-    const int cw = min(sw, L.width - c0);
-    const int slot_f = cw <= 32 ? 32 : cw <= 64 ? 64 : cw <= 128 ? 128 : 256;
-    const int epi = slot_f > 128 ? 1 : 128 / slot_f;  // edges per warp load instruction
-    const int lpe = 32 / epi;                          // lanes per edge
-    const int g = lane / lpe, i = lane - g * lpe;
-    const int epw = U * epi;                           // edges per warp per round
-    const uint32_t R = static_cast<uint32_t>(G::kWarps * epw);
-    const uint32_t e0 = __ldg(L.indptr + r), e1 = __ldg(L.indptr + r + 1);
-    const uint32_t n = e1 - e0;
-    const uint32_t rounds = (n + R - 1) / R;
-    const float* lbase = L.lhs.base + c0 + i * 4;
-    bool col_ok[VPL];
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) col_ok[v] = i * 4 + v * 128 < cw && (v == 0 || slot_f > 128);
-    int hv[VPL];
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) hv[v] = (SMALL && rw > 1) ? (c0 + i * 4 + v * 128) / L.rhs.group : 0;
-
-    // ids of this warp's epw (<= 64) edges of a round: two 32-id windows
-    auto load_ids = [&](uint32_t rd, uint32_t (&o)[2], uint32_t (&e)[2]) {
-      const uint32_t jb = e0 + rd * R + warp * epw;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t j = jb + 32u * h + lane;
-        if (32 * h < epw && static_cast<int>(32 * h + lane) < epw && j < e1) {
-          o[h] = __ldg(L.indices + j);
-          if (need_eid) e[h] = __ldg(L.eids + j);
-        }
-      }
-    };
-    float4 x[U][VPL];
-    float sv[U][VPL];
-    auto issue = [&](uint32_t rd, const uint32_t (&o_w)[2], const uint32_t (&e_w)[2]) {
-      const uint32_t jb = e0 + rd * R + warp * epw;
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int q = k * epi + g;  // edge of this lane within the warp's chunk
-        const uint32_t o0 = __shfl_sync(kFull, o_w[0], q & 31);
-        const uint32_t o1 = __shfl_sync(kFull, o_w[1], q & 31);
-        const uint32_t o = q < 32 ? o0 : o1;
-        uint32_t e = 0;
-        if (need_eid) {
-          const uint32_t a0 = __shfl_sync(kFull, e_w[0], q & 31);
-          const uint32_t a1 = __shfl_sync(kFull, e_w[1], q & 31);
-          e = q < 32 ? a0 : a1;
-        }
-        const uint32_t j = jb + q;
-        if (j < e1) {
-          const float* src = lbase + operand_row(L.lhs.role, 0, o, e, j) * L.lhs.ld;
-#pragma unroll
-          for (int v = 0; v < VPL; ++v)
-            if (col_ok[v]) x[k][v] = __ldg(reinterpret_cast<const float4*>(src + v * 128));
-          if constexpr (SMALL) {
-#pragma unroll
-            for (int v = 0; v < VPL; ++v) {
-              if (rw > 0) {
-                sv[k][v] = col_ok[v]
-                    ? __ldg(L.rhs.base + operand_row(L.rhs.role, 0, o, e, j) * L.rhs.ld + hv[v])
-                    : 0.0f;
-              } else if (scale_on) {
-                sv[k][v] = __ldg(L.other_scale + o);
-              }
-            }
-          }
-        }
-      }
-    };
-    auto stage = [&](uint32_t rd) {
-      const uint32_t jb = e0 + rd * R + warp * epw;
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int q = k * epi + g;
-        if (jb + q < e1) {
-          const int eidx = warp * epw + q;  // edge within the round
-          float* dst = buf + static_cast<size_t>(eidx) * slot_f + i * 4;
-#pragma unroll
-          for (int v = 0; v < VPL; ++v)
-            if (col_ok[v]) *reinterpret_cast<float4*>(dst + v * 128) = x[k][v];
-          if constexpr (SMALL) {
-#pragma unroll
-            for (int v = 0; v < VPL; ++v)
-              if (col_ok[v]) sbuf[eidx * rws + hv[v]] = sv[k][v];
-          }
-        }
-      }
-    };
-
-    // the fold: thread tid < cw owns column c0 + tid
-    float acc = red_identity<ROP>();
-    uint32_t arg = 0xffffffffu;
-    const int hcol = (SMALL && rw > 1) ? (c0 + tid) / L.rhs.group : 0;
-    uint32_t ida[2] = {0, 0}, idea[2] = {0, 0}, idb[2] = {0, 0}, ideb[2] = {0, 0};
-    load_ids(0, ida, idea);
-    load_ids(1, idb, ideb);
-    issue(0, ida, idea);
-    stage(0);
-    __syncthreads();
-    for (uint32_t k = 0; k < rounds; ++k) {
-      if (k + 1 < rounds) {
-        issue(k + 1, idb, ideb);  // loads in flight during the fold below
-        load_ids(k + 2, idb, ideb);
-      }
-      if (tid < cw) {
-        const uint32_t cnt = min(R, n - k * R);
-        const float* col = buf + tid;
-        const int soff = SMALL && rw > 0 ? hcol : 0;
-#pragma unroll 4
-        for (uint32_t e = 0; e < cnt; ++e) {
-          float m = col[static_cast<size_t>(e) * slot_f];
-          if constexpr (SMALL) {
-            if (rw > 0) m = bin_apply<BOP>(m, sbuf[e * rws + soff]);
-            else m = __fmul_rn(bin_apply<BOP>(m, 0.0f), sbuf[e]);
-          } else {
-            m = bin_apply<BOP>(m, 0.0f);
-          }
-          if constexpr (ARG) {
-            if (red_wins<ROP>(acc, m)) {
-              acc = m;
-              arg = e0 + k * R + e;
-            }
-          } else {
-            acc = red_combine<ROP>(acc, m);
-          }
-        }
-      }
-      __syncthreads();
-      if (k + 1 < rounds) stage(k + 1);
-      __syncthreads();
-    }
-    if (tid < cw) {
-      float a = acc;
-      if constexpr (ROP == R_MAX || ROP == R_MIN) {
-        if (n == 0) a = 0.0f;
-      }
-      if (L.mean) a = n ? __fdiv_rn(a, __uint2float_rn(n)) : 0.0f;
-      L.out[static_cast<int64_t>(r) * L.out_ld + c0 + tid] = a;
-      if constexpr (ARG) {
-        const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + tid;
-        const bool none = arg == 0xffffffffu;
-        if (L.arg_other)
-          L.arg_other[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.indices + arg));
-        if (L.arg_edge) L.arg_edge[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.eids + arg));
-      }
-    }
-    if (p.trace && tid == 0) {
-      unsigned long long* t = p.trace + 4ull * unit;
-      t[0] = t0;
-      t[1] = globaltimer_ns();
-      t[2] = (static_cast<unsigned long long>(smid()) << 32) | 0xffffu;
-      t[3] = n;
-    }
-    __syncthreads();
-  }
-}
-
-// ------------------------------------- LONG ROWS, warp-specialised LDGSTS
-// The production long-row CTA.  One column slice (<= 512 floats) of one long
-// row per unit, streamed through a shared-memory ring of NB stages of R edges
-// by cp.async (LDGSTS: global -> shared, no registers hold data in flight).
-// Producers and consumers are decoupled by per-stage mbarriers: 12 producer
-// warps issue the copies of stage s as soon as the consumers released its
-// slot (empty[s % NB]); 4 consumer warps -- the column owners, one column
-// (narrow slices) or four (wide) per thread -- fold stage s in canonical edge
-// order as soon as its copies landed (full[s % NB]).  A copy costs one id
-// (shared-memory broadcast) and one 64-bit address per lane per edge.  The
-// ids of stage s + NB ride in stage s's copy group into a 2*NB id ring, so
-// issuing never waits on a global load.
-// Measured on B200 (scripts/mb_long.cu, scripts/var_long.sh): per-SM stream
-// rate grows with producer warps up to ~12 and with 48 KB stages; a CTA
-// barrier per stage (fold delaying the next issue) cost ~25%, and feeding
-// addresses from ids loaded into registers one stage earlier capped a CTA at
-// one id-load latency per stage (~20 GB/s).
-#ifndef WS_NB
-#define WS_NB 3
+// Rows above the plan level's threshold run as COLUMN UNITS: one unit = one
+// column slice [c0, c0 + cw) of one long row, folded by one CTA in canonical
+// edge order (bit-exact: one owner per column sees every edge in order).
+// The host cuts each long row into slices so that no unit runs much longer
+// than half the long rows' balanced share of the machine (the heaviest row,
+// 329k edges at config 3, becomes 8-column units whose time is the fp32 add
+// chain itself, ~0.67 ms; 100k-edge rows become 32-column units), and hands
+// the units out heaviest first (LPT).
+//
+// The CTA is warp-specialised: 12 producer warps gather each stage of R
+// edges x cw columns with 128-bit LDGs into registers -- the (edge, column
+// quad) items of a stage are spread over all 384 producer lanes, so a
+// narrow slice still keeps every lane busy -- one stage ahead of the stage
+// they store into the shared-memory ring (NB stages, empty/full
+// mbarriers); 4 consumer warps (one or four columns per thread) fold each
+// landed stage.  Neighbour ids ride two stages ahead as cp.async copies into
+// a small id ring.
+// Measured (round 1, scripts/mb_gather.cu): random 400 B rows stream at
+// 34 GB/s per SM through LDG.128 into registers against 9.5 GB/s through
+// LDGSTS (the previous long-row CTA) and ~100 rows/us through TMA gather4
+// (row-rate bound: no help for the 329k-edge chains).
+#ifndef LG_NB
+#define LG_NB 3
 #endif
-#ifndef WS_DF
-#define WS_DF 12288
+#ifndef LG_DF
+#define LG_DF 8192
 #endif
-#ifndef WS_P
-#define WS_P 12
-#endif
-// LONG_WS_MINB=2 caps the CTA at 64 registers so that two segment blocks
-// (instead of one) fit beside it: measured no faster (cfg3 mean 5.46 ->
-// 5.71 ms, cfg4 7.1 -> 7.1 ms), so the default stays 1
-#ifndef LONG_WS_MINB
-#define LONG_WS_MINB 1
-#endif
-constexpr int kWsProducers = WS_P, kWsConsumers = 4;
-constexpr int kWsThreads = 32 * (kWsProducers + kWsConsumers);
-struct WsGeom {
-  static constexpr int NB = WS_NB;
-  static constexpr int DF = WS_DF;          // data floats per stage
-  static constexpr int SF = DF / 6;         // small-operand floats per stage
-  static constexpr int MR = 256;            // max edges per stage
-  static constexpr size_t smem_bytes(bool small) {
-    return sizeof(float) * (static_cast<size_t>(NB) * (DF + (small ? SF : 0)) + 4ull * NB * MR) +
+constexpr int kLgProducers = 12, kLgConsumers = 4;
+constexpr int kLgThreads = 32 * (kLgProducers + kLgConsumers);
+struct LgGeom {
+  static constexpr int NB = LG_NB;       // data stages in the ring
+  static constexpr int DF = LG_DF;       // data floats per stage
+  static constexpr int MR = 1024;        // max edges per stage
+  static constexpr int NI = 4;           // stage-id slots (stages s .. s + 2 live)
+  static constexpr int SF = 1024;        // small-operand floats per stage
+  static constexpr int PL = 32 * kLgProducers;   // producer lanes
+  static constexpr int KQ = (DF / 4 + PL - 1) / PL;  // quads per producer lane per stage
+  static constexpr size_t smem_bytes(bool small, bool eid) {
+    return sizeof(float) * static_cast<size_t>(NB) * DF +
+           sizeof(uint32_t) * static_cast<size_t>(NI) * MR * (eid ? 2 : 1) +
+           (small ? sizeof(float) * static_cast<size_t>(NB) * SF : 0) +
            2ull * NB * sizeof(uint64_t);
   }
 };
 
 template <int BOP, int ROP, bool ARG, int SK>
-__global__ void __launch_bounds__(kWsThreads, LONG_WS_MINB) k_long_ws(const StreamLaunch p) {
-  using G = WsGeom;
-  constexpr int NB = G::NB;
+__global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p) {
+  using G = LgGeom;
+  constexpr int NB = G::NB, NI = G::NI, KQ = G::KQ, PL = G::PL;
   constexpr bool SMALL = SK != SK_NONE;
   extern __shared__ __align__(16) float sm[];
   __shared__ uint32_t s_unit;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool producer = warp < kWsProducers;
+  const bool producer = warp < kLgProducers;
   const RowLaunch& L = p.row;
-  const int rw = SMALL ? p.rhs_width : 0;
-  const bool scale_on = SMALL && L.other_scale != nullptr;
-  const bool need_eid = L.lhs.role == ROLE_EID || (rw && L.rhs.role == ROLE_EID);
-  float* sdata = sm;                                                    // NB x DF
-  uint32_t* sid = reinterpret_cast<uint32_t*>(sm + static_cast<size_t>(NB) * G::DF);  // 2NB x MR
-  uint32_t* seid = sid + 2 * NB * G::MR;                                // 2NB x MR
-  float* ssmall = reinterpret_cast<float*>(seid + 2 * NB * G::MR);      // NB x SF
+  const int rw = SMALL ? p.rhs_width : 0;  // small floats per edge (1 = scalar)
+  const bool need_eid = L.lhs.role == ROLE_EID || (SK != SK_SCALE && SMALL && L.rhs.role == ROLE_EID);
+  float* sdata = sm;                                                          // NB x DF
+  uint32_t* sid = reinterpret_cast<uint32_t*>(sm + static_cast<size_t>(NB) * G::DF);  // NI x MR
+  uint32_t* seid = sid + NI * G::MR;                                          // NI x MR (eid)
+  float* ssmall = reinterpret_cast<float*>(seid + (need_eid ? NI * G::MR : 0));  // NB x SF
   uint64_t* full = reinterpret_cast<uint64_t*>(ssmall + (SMALL ? NB * G::SF : 0));
   uint64_t* empty = full + NB;
   if (tid == 0) {
     for (int b = 0; b < NB; ++b) {
-      mbar_init(&full[b], kWsProducers);
-      mbar_init(&empty[b], kWsConsumers);
+      mbar_init(&full[b], kLgProducers);
+      mbar_init(&empty[b], kLgConsumers);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  uint32_t gs0 = 0;  // stages this CTA ran before the current unit (ring position)
+  uint32_t gs0 = 0;  // stages this CTA ran before the current unit (ring phase)
 
   for (;;) {
     if (tid == 0) s_unit = atomicAdd(p.counter, 1u);
@@ -696,27 +449,14 @@ __global__ void __launch_bounds__(kWsThreads, LONG_WS_MINB) k_long_ws(const Stre
     const uint32_t unit = s_unit;
     __syncthreads();
     if (unit >= p.n_units) break;
-    const unsigned long long t0 = p.trace ? globaltimer_ns() : 0ull;
-    uint32_t li, slc;
-    int sw;
-    if (unit < p.n_xl_units) {
-      li = unit / p.xl_slices;
-      slc = unit - li * p.xl_slices;
-      sw = p.xl_sw;
-    } else {
-      const uint32_t v = unit - p.n_xl_units;
-      li = p.n_xl + v / p.long_slices;
-      slc = v - (li - p.n_xl) * p.long_slices;
-      sw = p.long_sw;
-    }
-    const uint32_t r = __ldg(p.long_rows + li);
-    const int c0 = static_cast<int>(slc) * sw;
-    const int cw = min(sw, L.width - c0);
+    const uint2 ud = __ldg(p.long_units + unit);
+    const uint32_t r = ud.x;
+    const int c0 = static_cast<int>(ud.y & 0xffffu);
+    const int cw = static_cast<int>(ud.y >> 16);
     const int slot_f = (cw + 3) & ~3;
     const int qpe = slot_f >> 2;
-    const int cq = (cw + 3) >> 2;
     const int h0 = (SMALL && rw > 1) ? c0 / L.rhs.group : 0;
-    const int nh = SMALL ? ((rw > 1) ? (c0 + cw - 1) / L.rhs.group - h0 + 1 : 1) : 1;
+    const int nh = (SMALL && rw > 1) ? (c0 + cw - 1) / L.rhs.group - h0 + 1 : 1;
     uint32_t R = static_cast<uint32_t>(G::DF / slot_f);
     if (R > static_cast<uint32_t>(G::MR)) R = G::MR;
     if (SMALL && R * nh > static_cast<uint32_t>(G::SF)) R = G::SF / nh;
@@ -725,89 +465,109 @@ __global__ void __launch_bounds__(kWsThreads, LONG_WS_MINB) k_long_ws(const Stre
     const uint32_t rounds = (n + R - 1) / R;
 
     if (producer) {
-      const int ptid = tid;  // 0 .. 32 * kWsProducers - 1
-      const int lpe = qpe >= 32 ? 32 : qpe > 8 ? (qpe > 16 ? 32 : 16) : qpe > 4 ? 8 : qpe > 2 ? 4 : qpe;
-      const int epi = 32 / lpe;
-      const int sub = lane / lpe, il = lane - sub * lpe;
-      const int tpe = (qpe + lpe - 1) / lpe;
-      const uint32_t ngroups = (R + epi - 1) / epi;
-      const float* lbase = L.lhs.base + c0 + il * 4;
+      const int ptid = tid;  // 0 .. PL - 1
+      auto fetch_ids = [&](uint32_t m) {  // ids of unit stage m -> slot (gs0 + m) % NI
+        if (m >= rounds) return;
+        const uint32_t slot = (gs0 + m) % NI;
+        const uint32_t cnt = min(R, n - m * R);
+        for (uint32_t t = static_cast<uint32_t>(ptid); t < cnt; t += PL) {
+          cp_async_4(sid + slot * G::MR + t, L.indices + e0 + m * R + t);
+          if (need_eid) cp_async_4(seid + slot * G::MR + t, L.eids + e0 + m * R + t);
+        }
+      };
+      // item i = ptid + k * PL of a stage is (edge q = i / qpe, quad t = i % qpe)
+      const uint32_t q0 = static_cast<uint32_t>(ptid) / static_cast<uint32_t>(qpe);
+      const int t0 = ptid - static_cast<int>(q0) * qpe;
+      const uint32_t dq = static_cast<uint32_t>(PL / qpe);
+      const int dt = PL - static_cast<int>(dq) * qpe;
+      const float* lbase = L.lhs.base + c0;
       const int64_t lld = L.lhs.ld;
       const int32_t lrole = L.lhs.role;
-      auto fetch_ids = [&](uint32_t m) {  // ids of unit stage m -> id slot (gs0 + m) % 2NB
-        if (m >= rounds) return;
-        const uint32_t slot = (gs0 + m) % (2 * NB);
-        for (uint32_t t = static_cast<uint32_t>(ptid); t < R; t += 32 * kWsProducers) {
-          const uint32_t j = e0 + m * R + t;
-          if (j < e1) {
-            cp_async_4(sid + slot * G::MR + t, L.indices + j);
-            if (need_eid) cp_async_4(seid + slot * G::MR + t, L.eids + j);
+      // gather stage m's items into registers (x) and remember their shared
+      // offsets (off, -1 = no item)
+      auto load_stage = [&](uint32_t m, float4 (&x)[KQ], int (&off)[KQ]) {
+        const uint32_t slot = (gs0 + m) % NI;
+        const uint32_t cnt = min(R, n - m * R);
+        const uint32_t* io = sid + slot * G::MR;
+        const uint32_t* ie = seid + slot * G::MR;
+        uint32_t q = q0;
+        int t = t0;
+#pragma unroll
+        for (int k = 0; k < KQ; ++k) {
+          off[k] = -1;
+          if (q < cnt) {
+            const uint32_t o = io[q];
+            const uint32_t e = need_eid ? ie[q] : 0u;
+            const uint32_t row = lrole == ROLE_OTHER
+                                     ? o
+                                     : static_cast<uint32_t>(operand_row(lrole, 0, o, e, e0 + m * R + q));
+            x[k] = __ldg(reinterpret_cast<const float4*>(lbase + static_cast<int64_t>(row) * lld + 4 * t));
+            off[k] = static_cast<int>(q) * slot_f + 4 * t;
+          }
+          q += dq;
+          t += dt;
+          if (t >= qpe) {
+            t -= qpe;
+            ++q;
           }
         }
       };
-      // prologue: ids of the first NB stages, visible to every producer
-      for (uint32_t m = 0; m < static_cast<uint32_t>(NB); ++m) fetch_ids(m);
-      cp_async_commit();
-      cp_async_wait_group<0>();
-      named_barrier_sync(1, 32 * kWsProducers);
-      // per-lane constants of the copy loop: which of the <= 4 quads of an
-      // edge this lane copies, source / shared byte offsets
-      uint32_t tmask = 0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-        if (t < tpe && il + t * lpe < cq) tmask |= 1u << t;
-      const char* lsrc = reinterpret_cast<const char*>(lbase);
-      const uint32_t ldb = static_cast<uint32_t>(lld) * 4u;
-      const uint32_t slot_b = static_cast<uint32_t>(slot_f) * 4u;
-      const uint32_t tstep = static_cast<uint32_t>(lpe) * 16u;
-      constexpr bool small1 = SK == SK_WIN || SK == SK_SCALE;
-      const float* s1base = rw == 1 ? L.rhs.base : L.other_scale;
-      const int64_t s1ld = rw == 1 ? L.rhs.ld : 1;
-      const int32_t s1role = rw == 1 ? L.rhs.role : static_cast<int32_t>(ROLE_OTHER);
-      for (uint32_t s = 0; s < rounds; ++s) {
+      auto store_stage = [&](uint32_t s, const float4 (&x)[KQ], const int (&off)[KQ]) {
         const uint32_t gsi = gs0 + s;
         const int b = static_cast<int>(gsi % NB);
         if (gsi >= static_cast<uint32_t>(NB)) mbar_wait(&empty[b], ((gsi / NB) - 1) & 1u);
-        const uint32_t islot = gsi % (2 * NB);
-        const uint32_t* io = sid + islot * G::MR;
-        const uint32_t* ie = seid + islot * G::MR;
-        const uint32_t sd = smem_u32(sdata + static_cast<size_t>(b) * G::DF) + static_cast<uint32_t>(il) * 16u;
-        float* bs = ssmall + static_cast<size_t>(b) * G::SF;
-        const uint32_t jr0 = s * R;
-        const uint32_t cnt = min(R, n - jr0);
-        const uint32_t gcount = (cnt + epi - 1) / epi;
-        for (uint32_t g = static_cast<uint32_t>(warp); g < gcount; g += kWsProducers) {
-          const uint32_t q = g * epi + sub;
-          if (q >= cnt) continue;
-          const uint32_t j = e0 + jr0 + q;
-          const uint32_t o = io[q];
-          const uint32_t e = need_eid ? ie[q] : 0u;
-          const uint32_t row = lrole == ROLE_OTHER ? o : static_cast<uint32_t>(operand_row(lrole, 0, o, e, j));
-          const char* src = lsrc + static_cast<uint64_t>(row) * ldb;
-          const uint32_t d = sd + q * slot_b;
+        float* sd = sdata + static_cast<size_t>(b) * G::DF;
 #pragma unroll
-          for (int t = 0; t < 4; ++t)
-            if ((tmask >> t) & 1u) cp_async_16_s(d + t * tstep, src + t * tstep);
-          if constexpr (SMALL) {
-            if (small1) {
-              if (il == 0) {
-                const uint32_t sr = s1role == ROLE_POS ? j : s1role == ROLE_EID ? e : o;
-                cp_async_4(bs + q, s1base + static_cast<int64_t>(sr) * s1ld);
-              }
-            } else {
-              const float* sp = L.rhs.base + operand_row(L.rhs.role, 0, o, e, j) * L.rhs.ld + h0;
-              for (int h = il; h < nh; h += lpe) cp_async_4(bs + q * nh + h, sp + h);
-            }
+        for (int k = 0; k < KQ; ++k)
+          if (off[k] >= 0) *reinterpret_cast<float4*>(sd + off[k]) = x[k];
+        if constexpr (SMALL) {
+          const uint32_t slot = gsi % NI;
+          const uint32_t cnt = min(R, n - s * R);
+          float* bs = ssmall + static_cast<size_t>(b) * G::SF;
+          const float* s1base = SK == SK_SCALE ? L.other_scale : L.rhs.base;
+          const int64_t s1ld = SK == SK_SCALE ? 1 : L.rhs.ld;
+          const int32_t s1role = SK == SK_SCALE ? static_cast<int32_t>(ROLE_OTHER) : L.rhs.role;
+          for (uint32_t i = static_cast<uint32_t>(ptid); i < cnt * nh; i += PL) {
+            const uint32_t q = i / static_cast<uint32_t>(nh);
+            const int h = static_cast<int>(i - q * nh);
+            const uint32_t o = sid[slot * G::MR + q];
+            const uint32_t e = need_eid ? seid[slot * G::MR + q] : 0u;
+            const int64_t sr = operand_row(s1role, 0, o, e, e0 + s * R + q);
+            cp_async_4(bs + i, s1base + sr * s1ld + h0 + h);
           }
         }
-        fetch_ids(s + NB);
-        cp_async_arrive(&full[b]);
+        cp_async_arrive(&full[b]);  // the full phase also waits for these copies
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[b]);
+      };
+      fetch_ids(0);
+      cp_async_commit();
+      fetch_ids(1);
+      cp_async_commit();
+      cp_async_wait_group<1>();
+      named_barrier_sync(1, PL);  // ids of stage 0 visible to every producer
+      float4 xa[KQ], xb[KQ];
+      int oa[KQ], ob[KQ];
+      load_stage(0, xa, oa);
+      // one step: ids two stages ahead, gather stage s + 1, store stage s
+      // (two register sets alternate, so no register with a pending load is
+      // ever moved)
+      auto step = [&](uint32_t s, float4 (&xc)[KQ], int (&oc)[KQ], float4 (&xn)[KQ],
+                      int (&on)[KQ]) {
+        fetch_ids(s + 2);
+        cp_async_commit();
+        cp_async_wait_group<1>();
+        named_barrier_sync(1, PL);  // ids of stage s + 1 visible
+        if (s + 1 < rounds) load_stage(s + 1, xn, on);
+        store_stage(s, xc, oc);
+      };
+      for (uint32_t s = 0; s < rounds; s += 2) {
+        step(s, xa, oa, xb, ob);
+        if (s + 1 < rounds) step(s + 1, xb, ob, xa, oa);
       }
       cp_async_wait_group<0>();
     } else {
-      const int ctid = tid - 32 * kWsProducers;  // 0 .. 127
+      const int ctid = tid - PL;  // 0 .. 127
       auto run = [&](auto fw_tag) {
         constexpr int FW = decltype(fw_tag)::value;
         const int cc = ctid * FW;
@@ -886,495 +646,9 @@ __global__ void __launch_bounds__(kWsThreads, LONG_WS_MINB) k_long_ws(const Stre
       };
       if (cw > 128) run(std::integral_constant<int, 4>{});
       else run(std::integral_constant<int, 1>{});
-      if (p.trace && ctid == 0) {
-        unsigned long long* t = p.trace + 4ull * unit;
-        t[0] = t0;
-        t[1] = globaltimer_ns();
-        t[2] = (static_cast<unsigned long long>(smid()) << 32) | 0xfffcu;
-        t[3] = n;
-      }
     }
     gs0 += rounds;
     __syncthreads();  // next unit: the id ring's first slots are rewritten
-  }
-}
-
-// ------------------------------------------ LONG ROWS, TMA tile::gather4
-// One column slice (<= 256 floats, the TMA box width) of one long row per
-// unit.  Warp 0 is the producer: each lane turns four staged neighbour ids
-// into one `cp.async.bulk.tensor.2d...tile::gather4` that lands four rows of
-// the slice in a shared-memory ring stage (completion by transaction bytes
-// on the stage's `full` mbarrier); warps 1-4 are the column owners that fold
-// each stage in canonical edge order and release it on `empty`.  No register
-// or L1 line holds a row in flight: the whole ~190 KB ring is the in-flight
-// window, and the load-store units stay free for the co-resident segment
-// warps.  Ids (and the small per-edge operand) arrive by cp.async NB stages
-// ahead, so issuing never waits on a global load.
-// Measured on B200 (scripts/mb_gather4.cu): one CTA streams ~73 rows/us of
-// 1 KB (74 GB/s, the per-SM share of the L2 limit) against ~41 for the
-// LDGSTS CTA above; the rate is bound by ~25 gather4 per us per SM, so the
-// slice should be as wide as the row allows.
-#ifndef G4_NB
-#define G4_NB 4
-#endif
-#ifndef G4_DF
-#define G4_DF 12288
-#endif
-constexpr int kG4Consumers = 4;
-constexpr int kG4Threads = 32 * (1 + kG4Consumers);
-struct G4Geom {
-  static constexpr int NB = G4_NB;
-  static constexpr int DF = G4_DF;  // data floats per stage
-  static constexpr int MR = 256;    // max edges per stage
-  static constexpr int SF = 512;    // small-operand floats per stage
-  static constexpr size_t smem_bytes() {
-    return sizeof(float) * (static_cast<size_t>(NB) * (DF + SF) + 4ull * NB * MR) +
-           2ull * NB * sizeof(uint64_t);
-  }
-};
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, int col, int r0,
-                                            int r1, int r2, int r3, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-      "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
-      : "memory");
-}
-
-template <int BOP, int ROP, bool ARG, int SK>
-__global__ void __launch_bounds__(kG4Threads, 1)
-    k_long_g4(const __grid_constant__ StreamLaunch p, const __grid_constant__ CUtensorMap tm_long,
-              const __grid_constant__ CUtensorMap tm_xl) {
-  using G = G4Geom;
-  constexpr int NB = G::NB;
-  constexpr bool SMALL = SK != SK_NONE;
-  extern __shared__ __align__(128) float sm[];
-  __shared__ uint32_t s_unit;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const RowLaunch& L = p.row;
-  const int rw = SMALL ? p.rhs_width : 0;
-  const bool need_eid = L.lhs.role == ROLE_EID || (rw && L.rhs.role == ROLE_EID);
-  float* sdata = sm;                                                              // NB x DF
-  float* ssmall = sm + static_cast<size_t>(NB) * G::DF;                           // NB x SF
-  uint32_t* sid = reinterpret_cast<uint32_t*>(ssmall + static_cast<size_t>(NB) * G::SF);  // 2NB x MR
-  uint32_t* seid = sid + 2 * NB * G::MR;                                          // 2NB x MR
-  uint64_t* full = reinterpret_cast<uint64_t*>(seid + 2 * NB * G::MR);
-  uint64_t* empty = full + NB;
-  if (tid == 0) {
-    for (int b = 0; b < NB; ++b) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], kG4Consumers);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  uint32_t gs0 = 0;  // stages run before the current unit (ring position)
-
-  for (;;) {
-    if (tid == 0) s_unit = atomicAdd(p.counter, 1u);
-    __syncthreads();
-    const uint32_t unit = s_unit;
-    __syncthreads();
-    if (unit >= p.n_units) break;
-    const unsigned long long t0 = p.trace ? globaltimer_ns() : 0ull;
-    uint32_t li, slc;
-    int sw, bw;
-    const bool xl = unit < p.n_xl_units;
-    if (xl) {
-      li = unit / p.xl_slices;
-      slc = unit - li * p.xl_slices;
-      sw = p.xl_sw;
-      bw = p.g4_box_xl;
-    } else {
-      const uint32_t v = unit - p.n_xl_units;
-      li = p.n_xl + v / p.long_slices;
-      slc = v - (li - p.n_xl) * p.long_slices;
-      sw = p.long_sw;
-      bw = p.g4_box;
-    }
-    const uint32_t r = __ldg(p.long_rows + li);
-    const int c0 = static_cast<int>(slc) * sw;
-    const int cw = min(sw, L.width - c0);
-    const int h0 = (SMALL && rw > 1) ? c0 / L.rhs.group : 0;
-    const int nh = SMALL ? ((rw > 1) ? (c0 + cw - 1) / L.rhs.group - h0 + 1 : 1) : 1;
-    uint32_t R = static_cast<uint32_t>(G::DF / bw);
-    if (R > static_cast<uint32_t>(G::MR)) R = G::MR;
-    if (SMALL && R * nh > static_cast<uint32_t>(G::SF)) R = G::SF / nh;
-    R &= ~3u;
-    const uint32_t e0 = __ldg(L.indptr + r), e1 = __ldg(L.indptr + r + 1);
-    const uint32_t n = e1 - e0;
-    const uint32_t rounds = (n + R - 1) / R;
-
-    if (warp == 0) {
-      const CUtensorMap* tm = xl ? &tm_xl : &tm_long;
-      const int32_t lrole = L.lhs.role;
-      auto fetch_ids = [&](uint32_t m) {  // ids of unit stage m -> id slot (gs0 + m) % 2NB
-        if (m < rounds) {
-          const uint32_t slot = (gs0 + m) % (2 * NB);
-          for (uint32_t t = static_cast<uint32_t>(lane); t < R; t += 32) {
-            const uint32_t j = e0 + m * R + t;
-            if (j < e1) {
-              cp_async_4(sid + slot * G::MR + t, L.indices + j);
-              if (need_eid) cp_async_4(seid + slot * G::MR + t, L.eids + j);
-            }
-          }
-        }
-        cp_async_commit();  // one group per stage, possibly empty
-      };
-      for (uint32_t m = 0; m < static_cast<uint32_t>(NB); ++m) fetch_ids(m);
-      constexpr bool small1 = SK == SK_WIN || SK == SK_SCALE;
-      const float* s1base = (SK == SK_SCALE) ? L.other_scale : L.rhs.base;
-      const int64_t s1ld = (SK == SK_SCALE) ? 1 : L.rhs.ld;
-      const int32_t s1role = (SK == SK_SCALE) ? static_cast<int32_t>(ROLE_OTHER) : L.rhs.role;
-      const uint32_t row_b = static_cast<uint32_t>(bw) * 4u;
-      for (uint32_t s = 0; s < rounds; ++s) {
-        const uint32_t gsi = gs0 + s;
-        const int b = static_cast<int>(gsi % NB);
-        if (gsi >= static_cast<uint32_t>(NB)) mbar_wait(&empty[b], ((gsi / NB) - 1) & 1u);
-        cp_async_wait_group<NB - 1>();  // ids of stage s landed (this lane's)
-        __syncwarp();                    // ... and every lane's
-        const uint32_t islot = gsi % (2 * NB);
-        const uint32_t* io = sid + islot * G::MR;
-        const uint32_t* ie = seid + islot * G::MR;
-        const uint32_t jr0 = s * R;
-        const uint32_t cnt = min(R, n - jr0);
-        const uint32_t ng = (cnt + 3) >> 2;
-        if (lane == 0) mbar_expect_tx(&full[b], ng * 4u * row_b);
-        __syncwarp();
-        const uint32_t sd = smem_u32(sdata + static_cast<size_t>(b) * G::DF);
-        for (uint32_t g = static_cast<uint32_t>(lane); g < ng; g += 32) {
-          int rr[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint32_t q = min(4 * g + k, cnt - 1);  // a tail group repeats its last row
-            const uint32_t o = io[q];
-            if (lrole == ROLE_OTHER) {
-              rr[k] = static_cast<int>(o);
-            } else {
-              const uint32_t e = need_eid ? ie[q] : 0u;
-              rr[k] = static_cast<int>(operand_row(lrole, 0, o, e, e0 + jr0 + q));
-            }
-          }
-          tma_gather4(sd + 4 * g * row_b, tm, c0, rr[0], rr[1], rr[2], rr[3], &full[b]);
-        }
-        if constexpr (SMALL) {
-          float* bs = ssmall + static_cast<size_t>(b) * G::SF;
-          for (uint32_t q = static_cast<uint32_t>(lane); q < cnt; q += 32) {
-            const uint32_t j = e0 + jr0 + q;
-            const uint32_t o = io[q];
-            const uint32_t e = need_eid ? ie[q] : 0u;
-            if (small1) {
-              const uint32_t sr = s1role == ROLE_POS ? j : s1role == ROLE_EID ? e : o;
-              cp_async_4(bs + q, s1base + static_cast<int64_t>(sr) * s1ld);
-            } else {
-              const float* sp = L.rhs.base + operand_row(L.rhs.role, 0, o, e, j) * L.rhs.ld + h0;
-              for (int h = 0; h < nh; ++h) cp_async_4(bs + q * nh + h, sp + h);
-            }
-          }
-        }
-        fetch_ids(s + NB);
-        if constexpr (SMALL) cp_async_arrive(&full[b]);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[b]);
-      }
-      cp_async_wait_group<0>();
-    } else {
-      const int ctid = tid - 32;  // 0 .. 127
-      auto run = [&](auto fw_tag) {
-        constexpr int FW = decltype(fw_tag)::value;
-        const int cc = ctid * FW;
-        const bool own = cc < cw;
-        const int hrel = (SMALL && rw > 1) ? (c0 + cc) / L.rhs.group - h0 : 0;
-        float acc[FW];
-        uint32_t arg[FW];
-#pragma unroll
-        for (int t = 0; t < FW; ++t) {
-          acc[t] = red_identity<ROP>();
-          arg[t] = 0xffffffffu;
-          if (L.acc_in && own && cc + t < cw)  // source-blocked pass: the partial
-            acc[t] = L.acc_in[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t];
-        }
-        for (uint32_t s = 0; s < rounds; ++s) {
-          const uint32_t gsi = gs0 + s;
-          const int b = static_cast<int>(gsi % NB);
-          mbar_wait(&full[b], (gsi / NB) & 1u);
-          if (own) {
-            const uint32_t cnt = min(R, n - s * R);
-            const float* col = sdata + static_cast<size_t>(b) * G::DF + cc;
-            const float* sv = ssmall + static_cast<size_t>(b) * G::SF + hrel;
-#pragma unroll 8
-            for (uint32_t e = 0; e < cnt; ++e) {
-              float x[FW];
-              if constexpr (FW == 2) {
-                const float2 v = *reinterpret_cast<const float2*>(col + static_cast<size_t>(e) * bw);
-                x[0] = v.x;
-                x[1] = v.y;
-              } else {
-                x[0] = col[static_cast<size_t>(e) * bw];
-              }
-              float sval = 0.0f;
-              if constexpr (SMALL) sval = sv[e * nh];
-#pragma unroll
-              for (int t = 0; t < FW; ++t) {
-                float m;
-                if constexpr (SK == SK_SCALE) m = __fmul_rn(bin_apply<BOP>(x[t], 0.0f), sval);
-                else if constexpr (SK == SK_NONE) m = bin_apply<BOP>(x[t], 0.0f);
-                else m = bin_apply<BOP>(x[t], sval);
-                if constexpr (ARG) {
-                  if (red_wins<ROP>(acc[t], m)) {
-                    acc[t] = m;
-                    arg[t] = e0 + s * R + e;
-                  }
-                } else {
-                  acc[t] = red_combine<ROP>(acc[t], m);
-                }
-              }
-            }
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[b]);
-        }
-        if (own) {
-          const uint32_t deg = L.deg_indptr ? __ldg(L.deg_indptr + r + 1) - __ldg(L.deg_indptr + r) : n;
-          const bool fix = L.epi != 1;  // a partial pass stores the raw fold
-#pragma unroll
-          for (int t = 0; t < FW; ++t) {
-            if (cc + t >= cw) break;
-            float a = acc[t];
-            if constexpr (ROP == R_MAX || ROP == R_MIN) {
-              if (fix && deg == 0) a = 0.0f;
-            }
-            if (fix && L.mean) a = deg ? __fdiv_rn(a, __uint2float_rn(deg)) : 0.0f;
-            L.out[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t] = a;
-            if constexpr (ARG) {
-              const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + cc + t;
-              const bool none = arg[t] == 0xffffffffu;
-              if (L.arg_other)
-                L.arg_other[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.indices + arg[t]));
-              if (L.arg_edge)
-                L.arg_edge[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.eids + arg[t]));
-            }
-          }
-        }
-      };
-      if (cw > 128) run(std::integral_constant<int, 2>{});
-      else run(std::integral_constant<int, 1>{});
-      if (p.trace && ctid == 0) {
-        unsigned long long* t = p.trace + 4ull * unit;
-        t[0] = t0;
-        t[1] = globaltimer_ns();
-        t[2] = (static_cast<unsigned long long>(smid()) << 32) | 0xfffbu;
-        t[3] = n;
-      }
-    }
-    gs0 += rounds;
-    __syncthreads();  // next unit: the id ring's first slots are rewritten
-  }
-}
-
-// ------------------------------------------------------ LONG ROWS via TMA
-// Warp-specialised variant for slices of >= 512 B: warp 8 is the producer
-// (lane 0 issues one cp.async.bulk per edge into a shared-memory ring of
-// 8-edge stages, ~200 KB deep; lanes 0-7 stage the small operand with
-// cp.async on the same full barrier), warps 0-7 are the 256 column owners
-// that fold each stage in edge order and release it on the empty barrier.
-// The SM's TMA engine is otherwise idle (segments gather with LDG), and a
-// full-row TMA request per edge keeps ~200 edges in flight for one row.
-constexpr int kLtConsumers = 8;                      // warps folding
-constexpr int kLtThreads = (kLtConsumers + 1) * 32;  // + producer warp
-constexpr int kLtMaxStages = 32;
-constexpr int kLtRingBytes = 200 * 1024;
-constexpr int kIdWin = 8;  // id windows in flight (producer)
-
-__host__ __device__ constexpr size_t lt_smem_bytes() {
-  return kLtRingBytes + 2 * kLtMaxStages * sizeof(uint64_t) + 2 * kIdWin * 32 * sizeof(uint32_t);
-}
-
-template <int BOP, int ROP, bool ARG, bool SMALL>
-__global__ void __launch_bounds__(kLtThreads, 1) k_long_tma(const StreamLaunch p) {
-  extern __shared__ __align__(128) unsigned char lt_smem[];
-  __shared__ uint32_t s_unit;
-  float* ring = reinterpret_cast<float*>(lt_smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(lt_smem + kLtRingBytes);
-  uint64_t* empty = full + kLtMaxStages;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool producer = warp == kLtConsumers;
-  const RowLaunch& L = p.row;
-  const int rw = SMALL ? p.rhs_width : 0;
-  const bool scale_on = SMALL && L.other_scale != nullptr;
-  const int rws = SMALL ? (rw > 0 ? rw : 1) : 0;
-  const bool need_eid = L.lhs.role == ROLE_EID || (rw && L.rhs.role == ROLE_EID);
-  if (tid == 0) {
-    for (int b = 0; b < kLtMaxStages; ++b) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], kLtConsumers);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  uint32_t full_phase = 0, empty_phase = 0;  // per-stage parity bits (per role)
-
-  for (;;) {
-    if (tid == 0) s_unit = atomicAdd(p.counter, 1u);
-    __syncthreads();
-    const uint32_t unit = s_unit;
-    __syncthreads();
-    if (unit >= p.n_units) break;
-    const unsigned long long t0 = p.trace ? globaltimer_ns() : 0ull;
-    const uint32_t li = unit / p.long_slices;
-    const uint32_t slc = unit - li * p.long_slices;
-    const uint32_t r = __ldg(p.long_rows + li);
-    const int c0 = static_cast<int>(slc) * p.long_sw;
-    const int cw = min(p.long_sw, L.width - c0);
-    const int slot_f = (cw + 3) & ~3;
-    const uint32_t slot_bytes = static_cast<uint32_t>(slot_f) * 4u;
-    int nst = kLtRingBytes / (8 * 4 * (slot_f + rws));
-    nst = nst > kLtMaxStages ? kLtMaxStages : nst;
-    float* tab = ring + static_cast<size_t>(nst) * 8 * slot_f;  // small operand per slot
-    const uint32_t e0 = __ldg(L.indptr + r), e1 = __ldg(L.indptr + r + 1);
-    const uint32_t n = e1 - e0;
-    const uint32_t n_stages = (n + 7) / 8;
-
-    if (producer) {
-      const float* lbase = L.lhs.base + c0;
-      // ids staged kIdWin windows (x32 edges) ahead through a shared ring with
-      // cp.async groups: the producer never waits on a fresh global load
-      uint32_t* id_o = reinterpret_cast<uint32_t*>(lt_smem + kLtRingBytes +
-                                                   2 * kLtMaxStages * sizeof(uint64_t));
-      uint32_t* id_e = id_o + kIdWin * 32;
-      auto load_win = [&](uint32_t w) {
-        const uint32_t j = e0 + 32u * w + lane;
-        const int sl = static_cast<int>(w % kIdWin) * 32 + lane;
-        if (j < e1) {
-          cp_async_4(id_o + sl, L.indices + j);
-          if (need_eid) cp_async_4(id_e + sl, L.eids + j);
-        }
-        cp_async_commit();
-      };
-      for (uint32_t w = 0; w < static_cast<uint32_t>(kIdWin); ++w) load_win(w);
-      for (uint32_t s = 0; s < n_stages; ++s) {
-        const int b = static_cast<int>(s % static_cast<uint32_t>(nst));
-        if (s >= static_cast<uint32_t>(nst)) {  // wait for the consumers to free it
-          mbar_wait(&empty[b], (empty_phase >> b) & 1u);
-          empty_phase ^= 1u << b;
-        }
-        if ((s & 3u) == 0) {  // entering id window s/4
-          if (s != 0) load_win((s >> 2) + kIdWin - 1);
-          cp_async_wait_group<kIdWin - 1>();
-          __syncwarp();
-        }
-        const uint32_t j0 = e0 + s * 8u;
-        const uint32_t cnt = min(8u, e1 - j0);
-        const int src = static_cast<int>(((s >> 2) % kIdWin) * 32 + (s & 3u) * 8u) + (lane & 7);
-        const uint32_t o = id_o[src];
-        const uint32_t e = need_eid ? id_e[src] : 0u;
-        // issuing lanes rotate over the warp (stage s uses lanes 8*(s%4) ..
-        // +7): bulk copies outstanding per issuing thread are limited
-        const uint32_t lbase8 = (s & 3u) * 8u;
-        const bool issuer = static_cast<uint32_t>(lane) >= lbase8 &&
-                            static_cast<uint32_t>(lane) < lbase8 + 8u;
-        const uint32_t l = static_cast<uint32_t>(lane) - lbase8;  // edge of this lane
-        const int slot = b * 8 + static_cast<int>(l);
-        if constexpr (SMALL) {
-          if (issuer && l < cnt) {
-            if (rw > 0) {
-              const float* sp = L.rhs.base + operand_row(L.rhs.role, 0, o, e, j0 + l) * L.rhs.ld;
-              for (int h = 0; h < rw; ++h) cp_async_4(tab + slot * rws + h, sp + h);
-            } else if (scale_on) {
-              cp_async_4(tab + slot, L.other_scale + o);
-            }
-          }
-          if (issuer) cp_async_arrive(&full[b]);
-          __syncwarp();
-        }
-        if (lane == 0) mbar_arrive_expect_tx(&full[b], cnt * slot_bytes);
-        __syncwarp();
-        if (issuer && l < cnt)
-          tma_load_1d(ring + slot * slot_f,
-                      lbase + operand_row(L.lhs.role, 0, o, e, j0 + l) * L.lhs.ld, slot_bytes,
-                      &full[b]);
-      }
-      // drain: the last min(nst, n_stages) stages' empties are consumed here
-      // so both roles enter the next unit with matching phases
-      const uint32_t tail = min(static_cast<uint32_t>(nst), n_stages);
-      for (uint32_t s = n_stages - tail; s < n_stages; ++s) {
-        const int b = static_cast<int>(s % static_cast<uint32_t>(nst));
-        mbar_wait(&empty[b], (empty_phase >> b) & 1u);
-        empty_phase ^= 1u << b;
-      }
-    } else {
-      // consumers: thread tid owns column c0 + tid
-      float acc = red_identity<ROP>();
-      uint32_t arg = 0xffffffffu;
-      const bool own = tid < cw;
-      const int hcol = (SMALL && rw > 1) ? (c0 + tid) / L.rhs.group : 0;
-      for (uint32_t s = 0; s < n_stages; ++s) {
-        const int b = static_cast<int>(s % static_cast<uint32_t>(nst));
-        mbar_wait(&full[b], (full_phase >> b) & 1u);
-        full_phase ^= 1u << b;
-        const uint32_t cnt = min(8u, n - s * 8u);
-        if (own) {
-          float mv[8], sv[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            mv[q] = ring[static_cast<size_t>(b * 8 + q) * slot_f + tid];
-            if constexpr (SMALL) sv[q] = tab[(b * 8 + q) * rws + hcol];
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            if (static_cast<uint32_t>(q) < cnt) {
-              float m;
-              if constexpr (SMALL) {
-                m = rw > 0 ? bin_apply<BOP>(mv[q], sv[q])
-                           : __fmul_rn(bin_apply<BOP>(mv[q], 0.0f), sv[q]);
-              } else {
-                m = bin_apply<BOP>(mv[q], 0.0f);
-              }
-              if constexpr (ARG) {
-                if (red_wins<ROP>(acc, m)) {
-                  acc = m;
-                  arg = e0 + s * 8u + q;
-                }
-              } else {
-                acc = red_combine<ROP>(acc, m);
-              }
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[b]);
-      }
-      if (own) {
-        float a = acc;
-        if constexpr (ROP == R_MAX || ROP == R_MIN) {
-          if (n == 0) a = 0.0f;
-        }
-        if (L.mean) a = n ? __fdiv_rn(a, __uint2float_rn(n)) : 0.0f;
-        L.out[static_cast<int64_t>(r) * L.out_ld + c0 + tid] = a;
-        if constexpr (ARG) {
-          const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + tid;
-          const bool none = arg == 0xffffffffu;
-          if (L.arg_other)
-            L.arg_other[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.indices + arg));
-          if (L.arg_edge) L.arg_edge[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.eids + arg));
-        }
-      }
-    }
-    if (p.trace && tid == 0) {
-      unsigned long long* t = p.trace + 4ull * unit;
-      t[0] = t0;
-      t[1] = globaltimer_ns();
-      t[2] = (static_cast<unsigned long long>(smid()) << 32) | 0xfffeu;
-      t[3] = n;
-    }
-    __syncthreads();
   }
 }
 
@@ -1382,7 +656,6 @@ __global__ void __launch_bounds__(kLtThreads, 1) k_long_tma(const StreamLaunch p
 template <int VPL, int U, int BOP, int ROP, int ARG, int SK, bool LO, bool PART>
 __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : VPL == 5 ? GATHER_MINB5 : GATHER_MINB2) k_gather(const StreamLaunch p) {
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
   const RowLaunch& L = p.row;
   const bool need_eid = L.lhs.role == ROLE_EID ||
                         ((SK == SK_WIN || SK == SK_HEAD) && L.rhs.role == ROLE_EID);
@@ -1407,7 +680,6 @@ __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : VPL == 5 ?
     if (unit >= p.n_units) break;
     if (lane == 0) next_unit = atomicAdd(p.counter, 1u);
     next_unit = __shfl_sync(kFull, next_unit, 0);
-    const unsigned long long t0 = p.trace ? globaltimer_ns() : 0ull;
 
     UnitCtx u;
     const uint32_t si = unit / p.seg_slices;
@@ -1420,101 +692,43 @@ __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : VPL == 5 ?
     u.e0 = __ldg(L.indptr + u.r0);
     u.e1 = __ldg(L.indptr + u.r1);
     wide_unit<VPL, U, BOP, ROP, ARG, SK, LO, PART>(L, u, need_eid, sbase, sld, srole, lane);
-    if (p.trace && lane == 0) {
-      unsigned long long* t = p.trace + 4ull * unit;
-      t[0] = t0;
-      t[1] = globaltimer_ns();
-      t[2] = (static_cast<unsigned long long>(smid()) << 32) | static_cast<unsigned>(warp);
-      t[3] = u.e1 - u.e0;
-    }
   }
 }
 
-// p.mode: 0 = row segments (k_gather), 1 = long rows (k_long)
+// p.mode: 0 = row segments (k_gather), 1 = long-row column units (k_long_rg)
 template <int VPL, int BOP, int ROP, int ARG, int SK, bool LO>
 cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
-  constexpr bool LARG = ARG != 0;  // the long-row kernels track positions
-  constexpr bool SMALL = SK != SK_NONE;
   cudaError_t e = cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const int sms = p.row.num_sms > 0 ? p.row.num_sms : 148;
-  if (p.mode == 1 && p.long_tma) {
-    // wide long-row slices: TMA-fed, warp-specialised CTAs
-    static int configured_t = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (configured_t != dev) {
-      e = cudaFuncSetAttribute(k_long_tma<BOP, ROP, LARG, SMALL>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(lt_smem_bytes()));
+  if (p.mode == 1) {
+    if constexpr (VPL == 1) {  // one instance per (BOP, ROP, ARG, SK)
+      constexpr bool SMALL = SK != SK_NONE;
+      const RowLaunch& L = p.row;
+      const bool eid = L.lhs.role == ROLE_EID || (SK != SK_SCALE && SMALL && L.rhs.role == ROLE_EID);
+      const size_t smem = LgGeom::smem_bytes(SMALL, eid);
+      auto* kern = k_long_rg<BOP, ROP, ARG != 0, SK>;
+      e = set_max_dynamic_smem(reinterpret_cast<const void*>(kern),
+                               static_cast<int>(LgGeom::smem_bytes(SMALL, true)));
       if (e != cudaSuccess) return e;
-      configured_t = dev;
-    }
-    unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
-    if (grid > p.n_units) grid = p.n_units;
-    k_long_tma<BOP, ROP, LARG, SMALL><<<grid, kLtThreads, lt_smem_bytes(), s>>>(p);
-  } else if (p.mode == 1 && p.long_g4) {
-    static int configured_g = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (configured_g != dev) {
-      e = cudaFuncSetAttribute(k_long_g4<BOP, ROP, LARG, SK>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(G4Geom::smem_bytes()));
-      if (e != cudaSuccess) return e;
-      configured_g = dev;
-    }
-    CUtensorMap tl, tx;
-    if (!encode_rows_tmap(&tl, p.row.lhs, p.row.width, p.g4_box) ||
-        !encode_rows_tmap(&tx, p.row.lhs, p.row.width, p.n_xl_units ? p.g4_box_xl : p.g4_box))
+      unsigned grid = static_cast<unsigned>(sms);
+      if (grid > p.n_units) grid = p.n_units;
+      kern<<<grid, kLgThreads, smem, s>>>(p);
+    } else {
       return cudaErrorInvalidValue;
-    unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
-    if (grid > p.n_units) grid = p.n_units;
-    k_long_g4<BOP, ROP, LARG, SK><<<grid, kG4Threads, G4Geom::smem_bytes(), s>>>(p, tl, tx);
-  } else if (p.mode == 1 && p.long_ws) {
-    const bool small = SMALL;
-    static int configured_w = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (configured_w != dev) {
-      e = cudaFuncSetAttribute(k_long_ws<BOP, ROP, LARG, SK>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(WsGeom::smem_bytes(small)));
-      if (e != cudaSuccess) return e;
-      configured_w = dev;
     }
-    unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
-    if (grid > p.n_units) grid = p.n_units;
-    k_long_ws<BOP, ROP, LARG, SK><<<grid, kWsThreads, WsGeom::smem_bytes(small), s>>>(p);
-  } else if (p.mode == 1) {
-    const int rws = SMALL ? (p.rhs_width > 0 ? p.rhs_width : 1) : 0;
-    const size_t smem = LongGeom<VPL>::smem_bytes(rws);
-    static int configured = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (configured != dev) {
-      e = cudaFuncSetAttribute(k_long<VPL, BOP, ROP, LARG, SMALL>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(LongGeom<VPL>::smem_bytes(LongGeom<VPL>::kMaxSmall)));
-      if (e != cudaSuccess) return e;
-      configured = dev;
-    }
-    // the host sizes the long-row grid by the long rows' share of the edges
-    // (p.long_ctas); the segment kernel's persistent blocks take the other
-    // SMs and absorb these ones when they finish
-    unsigned grid = p.long_ctas ? p.long_ctas : static_cast<unsigned>(sms);
-    if (grid > p.n_units) grid = p.n_units;
-    k_long<VPL, BOP, ROP, LARG, SMALL><<<grid, kLongThreads, smem, s>>>(p);
   } else {
     constexpr int U = VPL == 1 ? GATHER_U1 : VPL == 5 ? GATHER_U5 : GATHER_U2;
-    static int blocks_per_sm = 0;
-    if (!blocks_per_sm) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
+    static std::atomic<int> blocks_per_sm{0};
+    int bps = blocks_per_sm.load(std::memory_order_relaxed);
+    if (!bps) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps,
                                                     k_gather<VPL, U, BOP, ROP, ARG, SK, LO, false>,
                                                     kThreads, 0);
-      if (blocks_per_sm < 1) blocks_per_sm = 1;
+      if (bps < 1) bps = 1;
+      blocks_per_sm.store(bps, std::memory_order_relaxed);
     }
-    const unsigned grid = static_cast<unsigned>(sms * blocks_per_sm);
+    const unsigned grid = static_cast<unsigned>(sms * bps);
     if constexpr (!ARG) {  // argmax never runs source-blocked
       if (p.row.acc_in || p.row.epi) {
         k_gather<VPL, U, BOP, ROP, ARG, SK, LO, true><<<grid, kThreads, 0, s>>>(p);
@@ -1591,9 +805,9 @@ cudaError_t launch_wide(const StreamLaunch& p, cudaStream_t s) {
 
 template <int BOP>
 cudaError_t launch_bop(const StreamLaunch& p, cudaStream_t s) {
-  const int sw = p.mode == 1 ? p.long_sw : p.seg_sw;
-  if (p.mode == 0 && sw > 256) return launch_wide<BOP>(p, s);
-  return sw > 128 ? launch_red<2, BOP>(p, s) : launch_red<1, BOP>(p, s);
+  if (p.mode == 1) return launch_red<1, BOP>(p, s);  // long rows: one instance per width
+  if (p.seg_sw > 256) return launch_wide<BOP>(p, s);
+  return p.seg_sw > 128 ? launch_red<2, BOP>(p, s) : launch_red<1, BOP>(p, s);
 }
 
 }  // namespace gather_detail

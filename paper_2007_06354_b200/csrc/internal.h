@@ -70,6 +70,7 @@ struct RowLaunch {
   const float* acc_in = nullptr;
   const uint32_t* deg_indptr = nullptr;
   int32_t epi = 0;
+  int32_t src_blocks = 0;  // per-call source blocking (0 = the handle's setting)
 };
 
 // Kernel launchers (rows.cu, dot.cu, aux.cu).  Return cudaGetLastError().
@@ -83,12 +84,13 @@ cudaError_t launch_row_of_edge(const uint32_t* indptr, uint32_t rows, uint32_t* 
 cudaError_t launch_permute_edges(const uint32_t* eids, uint64_t m,
                                  const float* src, int64_t dim, int64_t src_ld,
                                  float* dst, int64_t dst_ld, cudaStream_t s);
-cudaError_t launch_argmax_backward(const int32_t* arg, int64_t rows,
-                                   int64_t dim, int64_t arg_ld,
-                                   const float* grad_out, int64_t grad_ld,
-                                   float* grad_src, int64_t src_rows,
-                                   int64_t src_ld, double* acc,
-                                   cudaStream_t s);
+// grad_src[arg[r,f] - src_lo, f] += grad_out[r,f] for targets inside
+// [src_lo, src_lo + src_rows) (f64 accumulation, rounded once); grad_src
+// overwritten.  Stream-ordered workspace.
+cudaError_t launch_argmax_backward(const int32_t* arg, int64_t rows, int64_t dim,
+                                   int64_t arg_ld, const float* grad_out, int64_t grad_ld,
+                                   float* grad_src, int64_t src_lo, int64_t src_rows,
+                                   int64_t src_ld, cudaStream_t s);
 
 // A handle's side stream and fork / join events (hub-row kernels run there,
 // concurrently with the warp-per-row kernels).  stream == nullptr: serial.
@@ -111,6 +113,10 @@ cudaError_t launch_edge_softmax(bool backward, const uint32_t* indptr, const uin
 cudaError_t launch_build_csr(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
                              bool dst_major, uint32_t* indptr, uint32_t* indices, uint32_t* eids,
                              cudaStream_t s);
+// Lowest edge id whose src or dst is >= n (~0 when all ids are in range);
+// synchronizes the stream.
+cudaError_t check_edge_ids(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
+                           cudaStream_t s, uint64_t* first_bad);
 cudaError_t launch_transpose_csr(uint32_t num_rows, uint32_t num_cols, uint64_t m,
                                  const uint32_t* indptr, const uint32_t* indices,
                                  const uint32_t* eids, uint32_t* t_indptr, uint32_t* t_indices,
@@ -131,6 +137,10 @@ cudaError_t launch_block_csr(const uint32_t* lo, const uint32_t* hi, uint32_t ro
 // gathered row.
 cudaError_t launch_scale_rows(const float* x, int64_t rows, int64_t dim, int64_t ld,
                               const float* scale, float* y, int64_t y_ld, cudaStream_t s);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device),
+// thread-safe (aux.cu).
+cudaError_t set_max_dynamic_smem(const void* func, int bytes);
 
 // Launch counter (evidence of native execution), bumped by each launcher.
 void note_launch(uint64_t n = 1);

@@ -1,12 +1,18 @@
 // shim.cpp -- the reference-signature C++ API (include/gspmm_b200.hpp) on
 // top of the C-ABI.  Synchronous host-buffer calls like the reference's;
-// device handles for a CsrGraph are cached (the reference declares a
-// CsrGraph immutable after construction, csr.hpp:33) so repeated calls on
-// one graph upload it once.
+// device handles are cached by graph CONTENT (orientation, sizes and a hash
+// of the three arrays), so repeated calls on one graph upload it once and a
+// new graph at recycled addresses never hits a stale device copy.  Handles
+// are reference-counted: evicting one never frees it under a running call.
+// Thread-safe, like the reference's calls (csr.hpp:35).
 #include "gspmm_b200.hpp"
 
+#include <algorithm>
 #include <memory>
 #include <mutex>
+#include <thread>
+#include <utility>
+#include <vector>
 
 namespace gspmm_b200 {
 
@@ -38,20 +44,84 @@ const char* op_name(Operand o) {
   }
 }
 
-struct CacheEntry {
-  const void* key[4] = {nullptr, nullptr, nullptr, nullptr};
-  std::uint64_t sizes[3] = {0, 0, 0};
-  gspmm_graph h = nullptr;
-  std::unique_ptr<CsrGraph> transposed;  // owner view for Push
+// Content fingerprint of a CsrGraph: orientation, sizes and a 64-bit hash of
+// indptr / indices / edge_ids (multithreaded: ~1 GB/s per thread).  The
+// cache is keyed on it, never on addresses: a graph destroyed and rebuilt at
+// recycled addresses with other contents gets its own device copy.
+struct Key {
+  int orientation = 0;
+  std::uint32_t rows = 0, cols = 0;
+  std::uint64_t m = 0, hash = 0;
+  bool transposed = false;  // the handle holds the transpose (Push)
+  bool operator==(const Key& o) const {
+    return orientation == o.orientation && rows == o.rows && cols == o.cols && m == o.m &&
+           hash == o.hash && transposed == o.transposed;
+  }
 };
+
+std::uint64_t mix(std::uint64_t h, std::uint64_t x) {
+  h ^= x + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  h *= 0xff51afd7ed558ccdull;
+  return h ^ (h >> 33);
+}
+
+std::uint64_t hash_words(const std::uint32_t* p, std::size_t n) {
+  constexpr std::size_t kChunk = std::size_t{1} << 22;
+  const std::size_t chunks = (n + kChunk - 1) / kChunk;
+  std::vector<std::uint64_t> part(chunks, 0);
+  auto work = [&](std::size_t c0, std::size_t c1) {
+    for (std::size_t c = c0; c < c1; ++c) {
+      std::uint64_t h = 0x243f6a8885a308d3ull ^ c;
+      const std::size_t b = c * kChunk, e = std::min(n, b + kChunk);
+      std::size_t i = b;
+      for (; i + 2 <= e; i += 2)
+        h = (h ^ (static_cast<std::uint64_t>(p[i]) | (static_cast<std::uint64_t>(p[i + 1]) << 32))) *
+            0x100000001b3ull * 0x9e3779b97f4a7c15ull;
+      if (i < e) h = (h ^ p[i]) * 0x9e3779b97f4a7c15ull;
+      part[c] = mix(h, e - b);
+    }
+  };
+  const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
+                                                      static_cast<unsigned>(chunks)));
+  if (nt <= 1) {
+    work(0, chunks);
+  } else {
+    std::vector<std::thread> ts;
+    for (unsigned t = 0; t < nt; ++t)
+      ts.emplace_back(work, chunks * t / nt, chunks * (t + 1) / nt);
+    for (auto& t : ts) t.join();
+  }
+  std::uint64_t h = n;
+  for (std::uint64_t x : part) h = mix(h, x);
+  return h;
+}
+
+Key key_of(const CsrGraph& g, bool transposed) {
+  Key k;
+  k.orientation = static_cast<int>(g.orientation);
+  k.rows = g.num_rows;
+  k.cols = g.num_cols;
+  k.m = g.indices.size();
+  k.transposed = transposed;
+  k.hash = mix(mix(hash_words(g.indptr.data(), g.indptr.size()),
+                   hash_words(g.indices.data(), g.indices.size())),
+               hash_words(g.edge_ids.data(), g.edge_ids.size()));
+  return k;
+}
+
+// A device handle shared by the cache and the calls using it: eviction only
+// drops the cache's reference, the handle is destroyed when the last call
+// using it returns.
+using Handle = std::shared_ptr<gspmm_graph_s>;
+
+Handle make_handle(gspmm_graph h) {
+  return Handle(h, [](gspmm_graph p) { gspmm_graph_destroy(p); });
+}
 
 struct Cache {
   std::mutex mu;
-  CacheEntry slot[4];
-  int next = 0;
-  ~Cache() {
-    for (auto& s : slot) gspmm_graph_destroy(s.h);
-  }
+  std::vector<std::pair<Key, Handle>> slot;  // most recent last
+  static constexpr std::size_t kSlots = 4;
 };
 
 Cache& cache() {
@@ -59,31 +129,42 @@ Cache& cache() {
   return c;
 }
 
-// Device handle for g (uploaded on first use).
-gspmm_graph handle_for(const CsrGraph& g) {
-  Cache& c = cache();
-  std::lock_guard<std::mutex> lock(c.mu);
-  const void* key[4] = {&g, g.indptr.data(), g.indices.data(), g.edge_ids.data()};
-  const std::uint64_t sizes[3] = {g.indptr.size(), g.indices.size(),
-                                  (static_cast<std::uint64_t>(g.num_rows) << 32) | g.num_cols};
-  for (auto& s : c.slot) {
-    if (s.h && s.key[0] == key[0] && s.key[1] == key[1] && s.key[2] == key[2] &&
-        s.key[3] == key[3] && s.sizes[0] == sizes[0] && s.sizes[1] == sizes[1] &&
-        s.sizes[2] == sizes[2])
-      return s.h;
-  }
+CsrGraph transpose_host(const CsrGraph& g);
+
+// Device handle for g (or for its transpose), uploaded on first use.  The
+// upload runs outside the cache lock; two threads racing on one new graph
+// both upload and the second keeps the first's handle.
+Handle handle_for(const CsrGraph& g, bool transposed) {
   if (g.indptr.size() != static_cast<std::size_t>(g.num_rows) + 1)
     throw StructureError("indptr length != num_rows+1");
-  gspmm_graph h = nullptr;
-  throw_status(gspmm_graph_create(0, static_cast<int>(g.orientation), g.num_rows, g.num_cols,
-                                  g.indptr.data(), g.indices.data(), g.edge_ids.data(),
-                                  /*validate=*/0, &h));
-  CacheEntry& s = c.slot[c.next];
-  c.next = (c.next + 1) % 4;
-  gspmm_graph_destroy(s.h);
-  for (int i = 0; i < 4; ++i) s.key[i] = key[i];
-  for (int i = 0; i < 3; ++i) s.sizes[i] = sizes[i];
-  s.h = h;
+  const Key k = key_of(g, transposed);
+  Cache& c = cache();
+  {
+    std::lock_guard<std::mutex> lock(c.mu);
+    for (auto it = c.slot.begin(); it != c.slot.end(); ++it)
+      if (it->first == k) {
+        Handle h = it->second;
+        std::rotate(it, it + 1, c.slot.end());  // most recent last
+        return h;
+      }
+  }
+  gspmm_graph raw = nullptr;
+  if (transposed) {
+    const CsrGraph t = transpose_host(g);
+    throw_status(gspmm_graph_create(0, static_cast<int>(t.orientation), t.num_rows, t.num_cols,
+                                    t.indptr.data(), t.indices.data(), t.edge_ids.data(),
+                                    /*validate=*/0, &raw));
+  } else {
+    throw_status(gspmm_graph_create(0, static_cast<int>(g.orientation), g.num_rows, g.num_cols,
+                                    g.indptr.data(), g.indices.data(), g.edge_ids.data(),
+                                    /*validate=*/0, &raw));
+  }
+  Handle h = make_handle(raw);
+  std::lock_guard<std::mutex> lock(c.mu);
+  for (auto& s : c.slot)
+    if (s.first == k) return s.second;
+  if (c.slot.size() >= Cache::kSlots) c.slot.erase(c.slot.begin());
+  c.slot.emplace_back(k, h);
   return h;
 }
 
@@ -156,8 +237,10 @@ BlockPlan build_block_plan(const CsrGraph& g, NodeId kb, std::int64_t nb) {
   BlockPlan p;
   p.kb = kb;
   p.nb = nb;
+  p.built_for = g.orientation;
   p.num_rows = g.num_rows;
   p.num_cols = g.num_cols;
+  p.num_edges = g.num_edges();
   p.num_blocks = g.num_cols ? (g.num_cols + kb - 1) / kb : 0;
   return p;
 }
@@ -178,43 +261,34 @@ FeatureMatrix binary_reduce(Strategy strategy, const CsrGraph& g, const BrConfig
   if (g.orientation != need)
     throw ShapeError(std::string("strategy with output ") + op_name(cfg.out) + " needs a " +
                      (need == Orientation::SrcMajor ? "src-major" : "dst-major") + " graph");
-  if (strategy == Strategy::BlockedPull && !plan)
-    throw ShapeError("BlockedPull requires a BlockPlan");
-  // Push scatters over the opposite orientation; the device runs owner rows.
-  std::unique_ptr<CsrGraph> owner;
-  const CsrGraph* view_g = &g;
-  if (strategy == Strategy::Push) {
-    owner = std::make_unique<CsrGraph>(transpose_host(g));
-    view_g = owner.get();
-  }
-  const gspmm_graph h = handle_for(*view_g);
-  // BlockedPull: the plan's neighbour-id blocks as source-blocked passes
-  // (bit-identical to Pull, like the reference's); otherwise automatic
-  const int blocks = strategy == Strategy::BlockedPull && plan->num_blocks >= 1
-                         ? static_cast<int>(plan->num_blocks)
-                         : 0;
-  throw_status(gspmm_graph_set_source_blocks(h, blocks));
+  // Push scatters over the opposite orientation; the device runs owner
+  // rows on the transposed view (cached like the graph itself)
+  const Handle h = handle_for(g, strategy == Strategy::Push);
   const gspmm_config c = to_c(cfg);
   gspmm_mat mu = view(u_feats), mv = view(v_feats), me = view(e_feats);
   int64_t rows = 0, dim = 0;
-  throw_status(gspmm_out_shape(h, &c, u_feats ? &mu : nullptr, v_feats ? &mv : nullptr,
+  throw_status(gspmm_out_shape(h.get(), &c, u_feats ? &mu : nullptr, v_feats ? &mv : nullptr,
                                e_feats ? &me : nullptr, nullptr, &rows, &dim));
+  // kernels.cpp:462-467, after the operand binding like the reference
+  if (strategy == Strategy::BlockedPull) {
+    if (!plan) throw ShapeError("BlockedPull requires a BlockPlan");
+    if (plan->built_for != g.orientation || plan->num_rows != g.num_rows ||
+        plan->num_cols != g.num_cols || plan->num_edges != g.num_edges())
+      throw ShapeError("BlockPlan was not built for this graph");
+  }
+  // BlockedPull: the plan's neighbour-id blocks as source-blocked passes
+  // (bit-identical to Pull, like the reference's), a per-call option;
+  // otherwise the automatic policy
+  gspmm_options opt{};
+  opt.source_blocks = strategy == Strategy::BlockedPull && plan->num_blocks >= 1
+                          ? static_cast<int32_t>(std::min<NodeId>(plan->num_blocks, 64))
+                          : 0;
   FeatureMatrix out(rows, dim);
   if (rows * dim > 0) {
     gspmm_out o{out.data.data(), rows, dim, dim};
-    throw_status(gspmm_binary_reduce_host(h, &c, u_feats ? &mu : nullptr,
+    throw_status(gspmm_binary_reduce_host(h.get(), &c, u_feats ? &mu : nullptr,
                                           v_feats ? &mv : nullptr, e_feats ? &me : nullptr, &o,
-                                          nullptr, nullptr));
-  }
-  if (owner) {
-    // Drop the temporary transposed view's handle from the cache key space.
-    Cache& cc = cache();
-    std::lock_guard<std::mutex> lock(cc.mu);
-    for (auto& s : cc.slot)
-      if (s.h == h) {
-        gspmm_graph_destroy(s.h);
-        s = CacheEntry{};
-      }
+                                          &opt, nullptr));
   }
   return out;
 }

@@ -3,9 +3,13 @@
 // side by side with the unmodified reference library (gspmm::, linked from
 // oracle/_ref) on identical inputs, in the style of the reference's own
 // proj/tests/test_kernels.cpp.  Exit code 0 = all checks passed.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "gspmm/bench.hpp"
 #include "gspmm/compare.hpp"
@@ -14,6 +18,7 @@
 #include "gspmm/kernels.hpp"
 #include "gspmm/oracle.hpp"
 #include "gspmm/rng.hpp"
+#include "gspmm_b200.h"
 #include "gspmm_b200.hpp"
 
 namespace R = gspmm;
@@ -106,6 +111,65 @@ static R::EdgeList random_small_graph(std::uint64_t seed) {  // test_util.hpp:30
   return R::generate(spec);
 }
 
+// The reference-side adapter of INTEGRATION.md section 2, written against
+// the REFERENCE's own types (R::CsrGraph, R::FeatureMatrix, R::BlockPlan)
+// and calling the C-ABI: Push runs on the transposed view, BlockedPull's plan
+// is checked like kernels.cpp:462-467 and becomes per-call source blocks,
+// every failure throws (no CPU fallback).
+[[noreturn]] static void throw_b200(int st) {
+  const std::string msg = std::string("B200: ") + gspmm_last_error();
+  if (st == GSPMM_ERR_SHAPE) throw R::ShapeError(msg);
+  if (st == GSPMM_ERR_CONFIG) throw R::ConfigError(msg);
+  if (st == GSPMM_ERR_STRUCTURE) throw R::StructureError(msg);
+  throw std::runtime_error(msg);
+}
+
+static gspmm_mat as_mat(const R::FeatureMatrix* f) {
+  gspmm_mat m{};
+  if (f) m = {f->data.data(), f->rows, f->dim, f->dim, GSPMM_EDGE_BY_ID};
+  return m;
+}
+
+static R::FeatureMatrix adapter_binary_reduce(R::Strategy strategy, const R::CsrGraph& g,
+                                              const R::BrConfig& cfg,
+                                              const R::FeatureMatrix* u_feats,
+                                              const R::FeatureMatrix* v_feats,
+                                              const R::FeatureMatrix* e_feats,
+                                              const R::BlockPlan* plan) {
+  R::validate_config(cfg);
+  if (g.orientation != R::required_orientation(strategy, cfg.out))
+    throw R::ShapeError("graph orientation does not match the strategy");
+  const R::CsrGraph owner_view = strategy == R::Strategy::Push ? R::transpose(g) : R::CsrGraph{};
+  const R::CsrGraph& dg = strategy == R::Strategy::Push ? owner_view : g;
+  if (strategy == R::Strategy::BlockedPull &&
+      (!plan || plan->built_for != g.orientation || plan->num_rows != g.num_rows ||
+       plan->num_cols != g.num_cols || plan->num_edges() != g.num_edges()))
+    throw R::ShapeError("BlockPlan was not built for this graph");
+  gspmm_graph h = nullptr;
+  int st = gspmm_graph_create(0, static_cast<int>(dg.orientation), dg.num_rows, dg.num_cols,
+                              dg.indptr.data(), dg.indices.data(), dg.edge_ids.data(), 0, &h);
+  if (st != GSPMM_OK) throw_b200(st);
+  const gspmm_config c{static_cast<int32_t>(cfg.lhs), static_cast<int32_t>(cfg.rhs),
+                       static_cast<int32_t>(cfg.binary), static_cast<int32_t>(cfg.reduce),
+                       static_cast<int32_t>(cfg.out)};
+  gspmm_mat mu = as_mat(u_feats), mv = as_mat(v_feats), me = as_mat(e_feats);
+  gspmm_options opt{};
+  if (strategy == R::Strategy::BlockedPull)
+    opt.source_blocks = static_cast<int32_t>(std::min<R::NodeId>(plan->num_blocks, 64));
+  int64_t rows = 0, dim = 0;
+  st = gspmm_out_shape(h, &c, u_feats ? &mu : nullptr, v_feats ? &mv : nullptr,
+                       e_feats ? &me : nullptr, &opt, &rows, &dim);
+  R::FeatureMatrix out(st == GSPMM_OK ? rows : 0, st == GSPMM_OK ? dim : 0);
+  if (st == GSPMM_OK && rows * dim > 0) {
+    gspmm_out o{out.data.data(), rows, dim, dim};
+    st = gspmm_binary_reduce_host(h, &c, u_feats ? &mu : nullptr, v_feats ? &mv : nullptr,
+                                  e_feats ? &me : nullptr, &o, &opt, nullptr);
+  }
+  gspmm_graph_destroy(h);
+  if (st != GSPMM_OK) throw_b200(st);
+  return out;
+}
+
 int main() {
   const R::Strategy kAll[] = {R::Strategy::Push, R::Strategy::Pull, R::Strategy::BlockedPull,
                               R::Strategy::RowParallelSpmm};
@@ -161,8 +225,85 @@ int main() {
           CHECK(R::bit_equal(t, oracle));
         else
           CHECK(R::max_rel_error(t, oracle) <= 1e-5);
+        // the reference-side adapter on the reference's
+        // own graph view and plan, Push and BlockedPull included
+        const R::CsrGraph& rg = views.oriented(R::required_orientation(s, cfg.out));
+        const R::BlockPlan rplan =
+            s == R::Strategy::BlockedPull
+                ? R::build_block_plan(rg, rg.num_cols > 3 ? (rg.num_cols + 2) / 3 : 1, 8)
+                : R::BlockPlan{};
+        const R::FeatureMatrix ad = adapter_binary_reduce(s, rg, cfg, &fu, &fv, &fe, &rplan);
+        CHECK(R::bit_equal(ad, want));
       }
     }
+  }
+  // a BlockPlan built for another graph is a ShapeError (kernels.cpp:462-467),
+  // in the shim and in the adapter
+  {
+    const R::EdgeList a = random_small_graph(7), b = random_small_graph(8);
+    const R::GraphViews va = R::make_views(a), vb = R::make_views(b);
+    const R::FeatureMatrix fa = R::random_features(a.num_nodes, 3, 1);
+    const B::BlockPlan wrong = B::build_block_plan(to_b(vb.dst_major), 4, 2);
+    const B::FeatureMatrix bfa = to_b(fa);
+    const B::CsrGraph bga = to_b(va.dst_major);
+    CHECK_THROWS_AS(B::binary_reduce(B::Strategy::BlockedPull, bga,
+                                     B::named_config("u_copy_add_v"), &bfa, nullptr, nullptr,
+                                     &wrong),
+                    B::ShapeError);
+    const R::BlockPlan rwrong = R::build_block_plan(vb.dst_major, 4, 2);
+    CHECK_THROWS_AS(adapter_binary_reduce(R::Strategy::BlockedPull, va.dst_major,
+                                          R::named_config("u_copy_add_v"), &fa, nullptr, nullptr,
+                                          &rwrong),
+                    R::ShapeError);
+  }
+  // graphs destroyed and rebuilt with the same sizes (recycled addresses):
+  // the content-keyed handle cache must never serve a stale device graph
+  for (std::uint64_t seed = 1; seed <= 24; ++seed) {
+    R::GeneratorSpec spec;
+    spec.kind = R::GeneratorKind::RMat;
+    spec.num_nodes = 150;
+    spec.num_edges = 1200;
+    spec.seed = seed;
+    const R::EdgeList el = R::generate(spec);
+    const R::GraphViews views = R::make_views(el);
+    const R::FeatureMatrix fu = R::random_features(el.num_nodes, 8, seed);
+    const R::FeatureMatrix want = R::binary_reduce(R::Strategy::RowParallelSpmm, views.dst_major,
+                                                   R::named_config("u_copy_add_v"), &fu, nullptr,
+                                                   nullptr);
+    B::CsrGraph* bg = new B::CsrGraph(to_b(views.dst_major));  // same sizes every seed
+    const B::FeatureMatrix bu = to_b(fu);
+    CHECK(same_bits(B::binary_reduce(B::Strategy::RowParallelSpmm, *bg,
+                                     B::named_config("u_copy_add_v"), &bu, nullptr, nullptr),
+                    want));
+    delete bg;
+  }
+  // one graph shared by several host threads at once (csr.hpp:35: a CsrGraph
+  // is safe to share), every strategy
+  {
+    const R::EdgeList el = random_small_graph(31);
+    const R::GraphViews views = R::make_views(el);
+    const R::FeatureMatrix fu = R::random_features(el.num_nodes, 16, 5);
+    const R::FeatureMatrix want = R::binary_reduce(R::Strategy::RowParallelSpmm, views.dst_major,
+                                                   R::named_config("u_copy_max_v"), &fu, nullptr,
+                                                   nullptr);
+    const B::CsrGraph bd = to_b(views.dst_major), bs = to_b(views.src_major);
+    const B::FeatureMatrix bu = to_b(fu);
+    std::vector<int> ok(8, 0);
+    std::vector<std::thread> ts;
+    for (int t = 0; t < 8; ++t)
+      ts.emplace_back([&, t] {
+        bool all = true;
+        for (int it = 0; it < 20; ++it) {
+          const B::Strategy s = (t % 2) ? B::Strategy::Push : B::Strategy::Pull;
+          const B::FeatureMatrix got = B::binary_reduce(
+              s, s == B::Strategy::Push ? bs : bd, B::named_config("u_copy_max_v"), &bu, nullptr,
+              nullptr);
+          all = all && same_bits(got, want);
+        }
+        ok[t] = all ? 1 : 0;
+      });
+    for (auto& t : ts) t.join();
+    for (int t = 0; t < 8; ++t) CHECK(ok[t] == 1);
   }
   // validation errors surface as the same exception types (:139-174)
   {

@@ -11,7 +11,6 @@ oracle_aggregate, compare.hpp:30-45) is checked as well.
 import numpy as np
 import pytest
 
-import os
 
 from gspmm_testutil import HAS_GPU, ROOT
 from oracle import oracle as O
@@ -27,11 +26,15 @@ SUM_TOL = 1e-5  # reference acceptance tolerance for sum-like reduces
 
 
 def dev_graph(g, orientation):
-    """Device handle for one orientation of an oracle Graph (cached)."""
+    """Device handle for one orientation of an oracle Graph (cached); a plan
+    set on the oracle Graph (g.plan = dict(...)) is applied to new handles."""
     cache = g.__dict__.setdefault("_dev", {})
     if orientation not in cache:
         ip, ix, ei = g.csr(orientation)
-        cache[orientation] = P.Graph(ip, ix, ei, g.n, g.n, orientation, validate=True)
+        h = P.Graph(ip, ix, ei, g.n, g.n, orientation, validate=True)
+        if getattr(g, "plan", None):
+            h.set_plan(**g.plan)
+        cache[orientation] = h
     return cache[orientation]
 
 
@@ -408,15 +411,14 @@ def test_long_rows_hub():
 
 
 @pytest.mark.parametrize("seg,long_", [(1, 2), (7, 16), (64, 100), (3, 100000)])
-def test_plan_granularity_does_not_change_results(seg, long_, monkeypatch):
+def test_plan_granularity_does_not_change_results(seg, long_):
     # tiny segments / long-row thresholds force every unit boundary case of
-    # the streaming kernel (rows split across units, empty rows at unit
-    # edges, long rows sliced into 32-column units) -- results stay bitwise
-    monkeypatch.setenv("GSPMM_SEG_EDGES", str(seg))
-    monkeypatch.setenv("GSPMM_LONG_EDGES", str(long_))
+    # the planned kernels (rows split across units, empty rows at unit
+    # edges, many long rows run as column units) -- results stay bitwise
     src, dst = O.gen_rmat(1500, 25000, seed=seg)
     src, dst = O.add_self_loops(1500, src, dst)
     g = O.Graph(1500, src, dst)
+    g.plan = dict(seg_cost=seg, long_threshold=long_)
     for dim in (4, 100, 256, 300):
         x = O.normal_features(1500, dim, dim)
         w = O.gcn_weights(1500, src, dst)
@@ -431,68 +433,73 @@ def test_plan_granularity_does_not_change_results(seg, long_, monkeypatch):
         g.__dict__.pop("_dev", None)  # rebuild handles with the next plan
 
 
-def test_register_path_matches_stream_path():
-    # the register-staged fallback (rows.cu) and the TMA-staged kernel
-    # (stream.cu) must agree bitwise; run the fallback in a subprocess
-    import subprocess
-    import sys
-    code = r"""
-import sys; sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
-import numpy as np, torch
-import paper_2007_06354_b200 as P
-from oracle import oracle as O
-src, dst = O.gen_rmat(3000, 60000, seed=9)
-g = O.Graph(3000, src, dst)
-x = O.normal_features(3000, 256, 1); w = O.gcn_weights(3000, src, dst)
-h = P.Graph(*g.dst_major, orientation=P.DST_MAJOR)
-out = P.binary_reduce(h, 'u_mul_e_add_v', u=torch.from_numpy(x).cuda(), e=torch.from_numpy(w).cuda())
-np.save(sys.argv[2], out.cpu().numpy())
-"""
-    import tempfile
-    outs = []
-    for disable in (False, True):
-        env = dict(os.environ)
-        env.pop("GSPMM_DISABLE_STREAM", None)
-        if disable:
-            env["GSPMM_DISABLE_STREAM"] = "1"
-        path = tempfile.mktemp(suffix=".npy")
-        r = subprocess.run([sys.executable, "-c", code, ROOT, path], env=env,
-                           capture_output=True, text=True, timeout=300)
-        assert r.returncode == 0, r.stderr[-2000:]
-        outs.append(np.load(path))
-    assert O.bit_equal(outs[0], outs[1])
+def test_register_path_matches_planned_path():
+    # the register kernel (rows.cu, plan kernel=1) and the planned kernels
+    # (k_gather + k_long_rg) must agree bitwise, long rows included
+    src, dst = O.gen_rmat(3000, 60000, seed=9)
+    g = O.Graph(3000, src, dst)
+    x = O.normal_features(3000, 256, 1)
+    w = O.gcn_weights(3000, src, dst)
+    h = P.Graph(*g.dst_major, orientation=P.DST_MAJOR)
+    h.set_plan(long_threshold=200)
+    assert h.num_long_rows > 0
+    planned = P.binary_reduce(h, "u_mul_e_add_v", u=cuda(x), e=cuda(w)).cpu().numpy()
+    h.set_plan(kernel=1)
+    before = P.launch_count()
+    reg = P.binary_reduce(h, "u_mul_e_add_v", u=cuda(x), e=cuda(w)).cpu().numpy()
+    assert P.launch_count() - before == 1  # one rows.cu launch
+    assert O.bit_equal(planned, reg)
+    assert O.bit_equal(reg, O.binary_reduce(g, O.named_config("u_mul_e_add_v"), u=x, e=w))
 
 
-@pytest.mark.parametrize("xl", [1, 50])
-def test_narrow_slices_of_heaviest_rows(xl, monkeypatch):
-    # rows above GSPMM_XL_EDGES are cut into 32-column slices streamed by
-    # several CTAs; results stay bitwise for every width
-    monkeypatch.setenv("GSPMM_XL_EDGES", str(xl))
-    rng = np.random.default_rng(7)
+@pytest.mark.parametrize("cols", [0, 4, 8, 12, 32, 64, 128, 132, 256, 512])
+def test_long_row_column_units(cols):
+    # long rows run as column units of `cols` columns (0: the automatic
+    # widths); every unit width, argmax and scalar / per-head / per-neighbour
+    # small operands included, stays bitwise for every feature width
+    rng = np.random.default_rng(cols + 7)
     n = 3000
-    src = np.concatenate([rng.integers(0, n, 40000), rng.integers(0, n, 30000)]).astype(np.uint32)
-    dst = np.concatenate([np.zeros(40000, np.int64) + 5, rng.integers(0, n, 30000)]).astype(np.uint32)
+    src = np.concatenate([rng.integers(0, n, 40000), rng.integers(0, n, 30000),
+                          rng.integers(0, n, 5000)]).astype(np.uint32)
+    dst = np.concatenate([np.zeros(40000, np.int64) + 5, rng.integers(0, n, 30000),
+                          np.zeros(5000, np.int64) + 17]).astype(np.uint32)
     g = O.Graph(n, src, dst)
+    g.plan = dict(long_threshold=1000, unit_cols=cols)
     w = O.gcn_weights(n, src, dst)
-    for dim in (20, 100, 128, 256, 300):
+    for dim in (4, 20, 100, 128, 256, 300, 512):
         x = O.normal_features(n, dim, dim)
         for cfg, kw in (((O.U, O.E, O.MUL, O.SUM, O.V), dict(u=x, e=w)),
+                        ((O.U, O.NONE, O.COPY, O.SUM, O.V), dict(u=x)),
                         ((O.U, O.NONE, O.COPY, O.MAX, O.V), dict(u=x))):
-            assert O.bit_equal(gpu_reduce(g, cfg, **kw), O.binary_reduce(g, cfg, **kw)), (xl, dim)
-        val, au, _ = gpu_reduce(g, (O.U, O.NONE, O.COPY, O.MAX, O.V), u=x, want_arg_other=True)
-        v2, au2, _ = O.copy_max_argmax(g, x)
-        assert O.bit_equal(val, v2) and (au == au2).all()
+            assert O.bit_equal(gpu_reduce(g, cfg, **kw), O.binary_reduce(g, cfg, **kw)), (cols, dim)
+        assert dev_graph(g, O.DST_MAJOR).num_long_rows == 2
+        val, au, ae = gpu_reduce(g, (O.U, O.NONE, O.COPY, O.MAX, O.V), u=x, want_arg_other=True,
+                                 want_arg_edge=True)
+        v2, au2, ae2 = O.copy_max_argmax(g, x)
+        assert O.bit_equal(val, v2) and (au == au2).all() and (ae == ae2).all()
+        if dim % 8 == 0 and dim >= 16:  # per-head weights (8 heads)
+            a = O.normal_features(len(src), 8, dim + 1)
+            want = O.multihead_u_mul_e_sum(g, x, a, 8)
+            got = gpu_reduce(g, (O.U, O.E, O.MUL, O.SUM, O.V), u=x, e=a, heads=8)
+            assert O.bit_equal(got, want), (cols, dim)
+        # mean backward on the src-major handle: per-neighbour scale
+        gy = O.normal_features(n, dim, dim + 2)
+        deg = O.in_degree(g)
+        inv = np.zeros(n, np.float32)
+        inv[deg > 0] = np.float32(1) / deg[deg > 0].astype(np.float32)
+        got = gpu_reduce(g, (O.V, O.NONE, O.COPY, O.SUM, O.U), v=gy,
+                         other_scale=torch.from_numpy(inv).cuda())
+        assert O.bit_equal(got, O.mean_backward(g, gy)), (cols, dim)
         g.__dict__.pop("_dev", None)
 
 
 @pytest.mark.parametrize("nb", [2, 3, 7])
-def test_source_blocks_bit_exact(nb, monkeypatch):
+def test_source_blocks_bit_exact(nb):
     # Source blocking (the paper's Alg. 3): nb passes, each folding one
     # neighbour-id block into the partial rows of the previous passes, must
     # give the single-pass result bit for bit -- sums, mean, max / min with
     # the zero-degree fixup, per-edge weights by edge id, the mean backward's
     # per-neighbour scale, and long rows (the hub) on both kernels.
-    monkeypatch.setenv("GSPMM_LONG_EDGES", "300")
     rng = np.random.default_rng(nb)
     n = 3000
     src = np.concatenate([rng.integers(0, n, 40000), rng.integers(0, n, 3000),
@@ -500,6 +507,7 @@ def test_source_blocks_bit_exact(nb, monkeypatch):
     dst = np.concatenate([rng.integers(0, n // 2, 40000), np.zeros(3000, np.int64),
                           rng.integers(0, n, 2000)]).astype(np.uint32)
     g = O.Graph(n, src, dst)  # rows >= n/2 get few in-edges: empty block ranges
+    g.plan = dict(long_threshold=300)
     x = O.normal_features(n, 200, nb)
     w = O.gcn_weights(n, src, dst)
     gy = O.normal_features(n, 200, nb + 3)
