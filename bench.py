@@ -779,15 +779,22 @@ C3_WORKLOAD = ("cfg3: copy_u+max with argmax and copy_u+mean, fwd+bwd; R-MAT(.57
                "2,449,029 nodes / 61,859,140 edges (seed 0) symmetrised to 123,718,280 directed; "
                "x fp32 [N x 100] U(-1,1) (seed 1); grad_out fp32 [N x 100] N(0,1) (seed 3)")
 C3_METRIC = ("aggregated edges/s (cfg3 step: max+argmax fwd, mean fwd, mean bwd, max bwd; "
-             "3 edge passes per step)")
+             "3 edge aggregations per step)")
+# the reference runs the two forward aggregations as two calls; the B200 arm
+# as one call with a second output (one gather of every source row)
 C3_PASSES = ("fwd copy_u+max+argmax", "fwd copy_u+mean", "bwd mean (grad_x)",
              "bwd max (argmax scatter)")
+C3_PASSES_B200 = ("fwd copy_u+max+argmax and copy_u+mean (one gather)", "bwd mean (grad_x)",
+                  "bwd max (argmax scatter)")
 
 
 def c3_config():
     # identical in both arms (the driver compares them)
-    return {"workload": C3_WORKLOAD, "nodes": C3_N, "edges": 2 * C3_M, "feat": C3_F,
-            "edge_passes_per_step": 3}
+    c = {"workload": C3_WORKLOAD, "nodes": C3_N, "edges": 2 * C3_M, "feat": C3_F,
+         "edge_passes_per_step": 3}
+    if C3_N != 2_449_029:
+        c["scaled_down"] = True  # --scale: a functional run, not the BASELINE size
+    return c
 
 
 def c3_graph(threads=0):
@@ -815,14 +822,14 @@ def c3_features(pinned):
 
 
 def c3_alg_bytes(rows_d, rows_s, E, src_rows):
-    """Algorithmic bytes per pass: features gathered once per
-    edge + CSR (indptr + indices) + output rows (+ the argmax rows); the max
-    backward reads the argmax and the gradient once and writes grad_x once."""
+    """Algorithmic bytes per pass of the B200 step: features
+    gathered once per edge + CSR (indptr + indices) + output rows (max,
+    argmax and mean for the fused forward); the max backward reads the argmax
+    and the gradient once and writes grad_x once."""
     F = C3_F
-    fwd = E * F * 4 + (rows_d + 1) * 4 + E * 4 + rows_d * F * 4
-    return {C3_PASSES[0]: fwd + rows_d * F * 4, C3_PASSES[1]: fwd,
-            C3_PASSES[2]: E * F * 4 + (rows_s + 1) * 4 + E * 4 + rows_s * F * 4,
-            C3_PASSES[3]: 2 * rows_d * F * 4 + src_rows * F * 4}
+    return {C3_PASSES_B200[0]: E * F * 4 + (rows_d + 1) * 4 + E * 4 + 3 * rows_d * F * 4,
+            C3_PASSES_B200[1]: E * F * 4 + (rows_s + 1) * 4 + E * 4 + rows_s * F * 4,
+            C3_PASSES_B200[2]: 2 * rows_d * F * 4 + src_rows * F * 4}
 
 
 class C3Reference:
@@ -935,7 +942,6 @@ def run_cfg3(args, rank, world, dist):
     gxm = torch.empty((rs, F), device=dev)
     gmax = torch.empty((rs, F), device=dev)
     cfg_max = (P.U, P.NONE, P.COPY, P.MAX, P.V)
-    cfg_mean = (P.U, P.NONE, P.COPY, P.MEAN, P.V)
     cfg_bwd = (P.V, P.NONE, P.COPY, P.SUM, P.U)
     gy_rows = gy[d_lo:d_hi]
     if world > 1:
@@ -961,8 +967,9 @@ def run_cfg3(args, rank, world, dist):
             P.argmax_backward(au, gy_rows, rs, out=gmax)
 
     passes = [
-        lambda: P.binary_reduce(gd, cfg_max, u=x, out=mx, arg_other_out=au),
-        lambda: P.binary_reduce(gd, cfg_mean, u=x, out=mean),
+        # max + argmax with the mean as a second output: one gather
+        lambda: P.binary_reduce(gd, cfg_max, u=x, out=mx, arg_other_out=au, out2=mean,
+                                reduce2=P.MEAN),
         lambda: P.binary_reduce(gs, cfg_bwd, v=gy, out=gxm, other_scale=inv_d),
         max_bwd,
     ]
@@ -1000,6 +1007,36 @@ def run_cfg3(args, rank, world, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
 
+    verify = None
+    if args.verify:
+        # whole outputs of the timed passes against the oracle (C restatement)
+        # on the full graph; shards gathered to rank 0 (gloo / NCCL objects)
+        torch.cuda.synchronize(dev)
+        mine = (d_lo, d_hi, s_lo, s_hi, mx.cpu().numpy(), au.cpu().numpy(), mean.cpu().numpy(),
+                gxm.cpu().numpy(), gmax.cpu().numpy())
+        parts = [mine]
+        if dist:
+            parts = [None] * world
+            dist.all_gather_object(parts, mine)
+        if rank == 0:
+            from oracle import oracle as O
+            full = {k: np.empty((C3_N, F), np.int32 if k == "au" else np.float32)
+                    for k in ("mx", "au", "mean", "gxm", "gmax")}
+            for (a, b, c, d, p_mx, p_au, p_mean, p_gxm, p_gmax) in parts:
+                full["mx"][a:b], full["au"][a:b], full["mean"][a:b] = p_mx, p_au, p_mean
+                full["gxm"][c:d], full["gmax"][c:d] = p_gxm, p_gmax
+            og = O.Graph(C3_N, src, dst)
+            xn, gyn = x_h.numpy(), gy_h.numpy()
+            w_max, w_au, _ = O.copy_max_argmax(og, xn)
+            w_gmax = O.argmax_backward(w_au, gyn, C3_N)
+            verify = {"max": bool(O.bit_equal(full["mx"], w_max)),
+                      "argmax": bool(np.array_equal(full["au"], w_au)),
+                      "mean": bool(O.bit_equal(full["mean"], O.mean(og, xn))),
+                      "mean_backward": bool(O.bit_equal(full["gxm"], O.mean_backward(og, gyn))),
+                      "max_backward_rel_err": float(O.max_rel_error(full["gmax"], w_gmax))}
+            verify["ok"] = all(v for k, v in verify.items() if k != "max_backward_rel_err") and \
+                verify["max_backward_rel_err"] <= 1e-6
+
     # --- e2e: the C-ABI host entries with pinned host buffers ----------------
     e2e = None
     if not args.skip_e2e:
@@ -1025,14 +1062,13 @@ def run_cfg3(args, rank, world, dist):
         def e2e_steps(k):
             for _ in range(k):
                 P.binary_reduce_host_async(gd, cfg_max, u=xn, out=mx_h, arg_other=au_h,
-                                           stream=s_a, wait_event=ev_b, upload_event=ev_a)
-                P.binary_reduce_host_async(gd, cfg_mean, u=xn, out=mean_h, stream=s_b,
-                                           wait_event=ev_a, upload_event=ev_b)
+                                           out2=mean_h, reduce2=P.MEAN, stream=s_a,
+                                           wait_event=ev_b, upload_event=ev_a)
+                P.binary_reduce_host_async(gs, cfg_bwd, v=gyn, out=gxm_h, other_scale=inv_h,
+                                           stream=s_b, wait_event=ev_a, upload_event=ev_b)
                 P.argmax_backward_host_async(au_h, gy_rows_h, gmax_h.shape[0], out=gmax_h,
                                              device=dev, stream=s_a, wait_event=ev_b,
                                              upload_event=ev_a)
-                P.binary_reduce_host_async(gs, cfg_bwd, v=gyn, out=gxm_h, other_scale=inv_h,
-                                           stream=s_b, wait_event=ev_a, upload_event=ev_b)
             s_a.synchronize()
             s_b.synchronize()
         e2e_steps(1)
@@ -1048,11 +1084,12 @@ def run_cfg3(args, rank, world, dist):
         if dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_s = float(te.item())
-        h2d = 2 * xn.nbytes + gyn.nbytes + gy_rows_h.nbytes + au_h.nbytes + inv_h.nbytes
+        h2d = xn.nbytes + gyn.nbytes + gy_rows_h.nbytes + au_h.nbytes + inv_h.nbytes
         d2h = mx_h.nbytes + au_h.nbytes + mean_h.nbytes + gxm_h.nbytes + gmax_h.nbytes
         e2e = {"value": 3 * E / e2e_s, "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
-               "path": "C-ABI host entries (gspmm_binary_reduce_host_async x3, "
+               "path": "C-ABI host entries (gspmm_binary_reduce_host_async: max + argmax with "
+                       "the mean as second output, mean backward; "
                        "gspmm_argmax_backward_host_async), pinned host buffers, two streams"}
 
     # --- CPU baseline (rank 0, N=1): the reference library, bounded sample ----
@@ -1084,7 +1121,7 @@ def run_cfg3(args, rank, world, dist):
     peak, peak_src = peaks()
     alg = c3_alg_bytes(rd, rs, gd.num_edges, rs)
     k_dom = max(range(len(passes)), key=lambda k: pass_ms[k])
-    name = C3_PASSES[k_dom]
+    name = C3_PASSES_B200[k_dom]
     achieved = alg[name] / (pass_ms[k_dom] * 1e-3) / 1e9
     traffic = c3_traffic()
     dram = traffic.get("passes", {}).get(name) if traffic and world == 1 else None
@@ -1107,12 +1144,13 @@ def run_cfg3(args, rank, world, dist):
         "notes": {"parallelism": f"dst/src-row shards x{world}" if world > 1 else "single GPU",
                   "l2": "inputs (980 MB feature matrices) larger than the 126 MB L2; no flush",
                   "mean_backward": "other_scale = 1/deg_in, prescaled rows"},
-        "passes_ms": {C3_PASSES[k]: round(pass_ms[k], 4) for k in range(len(passes))},
-        "passes_alg_gbs": {C3_PASSES[k]: alg[C3_PASSES[k]] / (pass_ms[k] * 1e-3) / 1e9
+        "passes_ms": {C3_PASSES_B200[k]: round(pass_ms[k], 4) for k in range(len(passes))},
+        "passes_alg_gbs": {C3_PASSES_B200[k]: alg[C3_PASSES_B200[k]] / (pass_ms[k] * 1e-3) / 1e9
                            for k in range(len(passes))},
         "roofline": roofline,
         "e2e": e2e, "cpu_baseline": cpu,
         "gpu_launches": int(launches), "clocks": clk.summary(), "impl": "b200",
+        **({"verify": verify} if verify is not None else {}),
     }
 
 
@@ -1220,6 +1258,12 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--verify", action="store_true",
+                    help="cfg3: check the timed passes' whole outputs against the oracle "
+                         "(small --scale only: the restated oracle is single-threaded)")
+    ap.add_argument("--scale", type=int, default=1,
+                    help="cfg3 / cfg5: divide the node and edge counts (functional tests "
+                         "only; the driver's bench runs the BASELINE sizes)")
     ap.add_argument("--cfg5-chunk", type=int, default=0,
                     help="cfg5: all-gather / aggregation column chunk (0: 640 on one GPU, "
                          "else 256)")
@@ -1232,6 +1276,10 @@ def main():
         log("[bench] warmup raised to 3 (timing rule)")
         args.warmup = 3
 
+    if args.scale > 1:
+        global C3_N, C3_M, C5_NODES
+        C3_N, C3_M = C3_N // args.scale, C3_M // args.scale
+        C5_NODES = C5_NODES // args.scale
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     dist = None

@@ -135,6 +135,16 @@ typedef struct {
   /* Source blocking for this call (see gspmm_graph_set_source_blocks):
    * 0 = the handle's setting, 1 = never, >= 2 = that many blocks. */
   int32_t source_blocks;
+  /* A second reduction of the same messages in the same call: out2 [out
+   * rows x width] (stride out2_ld, 0 -> width) receives
+   * binary_reduce(cfg with reduce = reduce2), reduce2 = GSPMM_SUM or
+   * GSPMM_MEAN -- bit-identical to a separate call.  With a Max/Min copy
+   * config (config 3's max + argmax and mean) both folds run over ONE
+   * gather of the source rows; other configs run it as a second pass.
+   * out2 == NULL: off.  Device pointer (host pointer in the *_host entries). */
+  float* out2;
+  int64_t out2_ld;
+  int32_t reduce2;
 } gspmm_options;
 
 typedef struct gspmm_graph_s* gspmm_graph;
@@ -150,6 +160,10 @@ typedef struct {
                               many columns per unit (multiple of 4, <= 512) */
   int32_t kernel;          /* 0 = planned kernels; 1 = the register kernel
                               (rows.cu) for every call (a reference path) */
+  uint32_t long_ctas;      /* 0 -> long-row units first, on every SM, then the
+                              segments (default); N -> the long-row units run
+                              concurrently with the segment kernel on N CTAs
+                              (one per SM; measured slower on config 3) */
 } gspmm_plan;
 
 /* ---- errors ---- */

@@ -71,12 +71,13 @@ class Out(C.Structure):
 
 class Plan(C.Structure):
     _fields_ = [("seg_cost", C.c_uint32), ("long_threshold", C.c_uint32),
-                ("unit_cols", C.c_uint32), ("kernel", C.c_int32)]
+                ("unit_cols", C.c_uint32), ("kernel", C.c_int32), ("long_ctas", C.c_uint32)]
 
 
 class Options(C.Structure):
     _fields_ = [("arg_other", C.c_void_p), ("arg_edge", C.c_void_p), ("arg_ld", C.c_int64),
-                ("heads", C.c_int32), ("other_scale", C.c_void_p), ("source_blocks", C.c_int32)]
+                ("heads", C.c_int32), ("other_scale", C.c_void_p), ("source_blocks", C.c_int32),
+                ("out2", C.c_void_p), ("out2_ld", C.c_int64), ("reduce2", C.c_int32)]
 
 
 # Every symbol include/gspmm_b200.h declares, with its prototype.

@@ -147,12 +147,13 @@ class Graph:
         check(A.LIB.gspmm_graph_set_source_blocks(self.handle, int(nblocks)), "set_source_blocks")
         return self
 
-    def set_plan(self, seg_cost=0, long_threshold=0, unit_cols=0, kernel=0):
+    def set_plan(self, seg_cost=0, long_threshold=0, unit_cols=0, kernel=0, long_ctas=0):
         """Rebuild the device plan (gspmm_graph_set_plan): segment-unit cost,
         a fixed long-row threshold, a fixed long-row unit width (multiple of
-        4, <= 512) and kernel=1 for the register kernel on every call.  0 =
-        the default of each.  Results never depend on the plan."""
-        p = A.Plan(seg_cost, long_threshold, unit_cols, kernel)
+        4, <= 512), kernel=1 for the register kernel on every call, long_ctas
+        = N to run the long-row units concurrently with the segments on N
+        CTAs.  0 = the default of each.  Results never depend on the plan."""
+        p = A.Plan(seg_cost, long_threshold, unit_cols, kernel, long_ctas)
         check(A.LIB.gspmm_graph_set_plan(self.handle, C.byref(p)), "set_plan")
         nl = C.c_uint32()
         check(A.LIB.gspmm_graph_info(self.handle, None, None, None, None, C.byref(nl)))
@@ -213,13 +214,17 @@ def _host_mat(a, edge_order=EDGE_BY_ID):
     return m
 
 
-def _opts(heads=1, arg_other=None, arg_edge=None, other_scale=None, arg_ld=0):
+def _opts(heads=1, arg_other=None, arg_edge=None, other_scale=None, arg_ld=0, out2=None,
+          out2_ld=0, reduce2=SUM):
     o = A.Options()
     o.heads = heads
     o.arg_other = arg_other
     o.arg_edge = arg_edge
     o.arg_ld = arg_ld
     o.other_scale = other_scale
+    o.out2 = out2
+    o.out2_ld = out2_ld
+    o.reduce2 = reduce2
     return o
 
 
@@ -252,12 +257,14 @@ def _check_out(t, rows, dim, dtype, dev, what):
 
 def binary_reduce(graph, cfg, u=None, v=None, e=None, *, out=None, e_order=EDGE_BY_ID,
                   want_arg_other=False, want_arg_edge=False, heads=1, other_scale=None,
-                  arg_other_out=None, arg_edge_out=None, stream=None):
+                  arg_other_out=None, arg_edge_out=None, out2=None, reduce2=SUM, stream=None):
     """binary_reduce (kernels.hpp:60-64) on device tensors.
 
     Returns ``out`` (allocated when not given) or ``(out, arg_other,
     arg_edge)`` when an argmax output is requested (``arg_*_out``: caller
-    buffers for them)."""
+    buffers for them).  ``out2``: a second output receiving the same config
+    with reducer ``reduce2`` (SUM or MEAN), fused into the same gather for
+    copy + max/min (config 3's max and mean forward)."""
     import torch
     cfg = as_config(cfg)
     mu, mv, me = _dev_mat(u), _dev_mat(v), _dev_mat(e, e_order)
@@ -285,9 +292,15 @@ def binary_reduce(graph, cfg, u=None, v=None, e=None, *, out=None, e_order=EDGE_
                 not other_scale.is_contiguous():
             raise A.ShapeError("other_scale must be a contiguous float32 tensor on the "
                                "operands' device")
+    o2 = None
+    if out2 is not None:
+        o2 = _check_out(out2, rows, dim, torch.float32, dev, "out2")
     opts = _opts(heads, ao.data_ptr() if ao is not None else None,
                  ae.data_ptr() if ae is not None else None,
-                 other_scale.data_ptr() if other_scale is not None else None)
+                 other_scale.data_ptr() if other_scale is not None else None,
+                 out2=o2.data_ptr() if o2 is not None else None,
+                 out2_ld=(o2.stride(0) if rows > 1 else dim) if o2 is not None else 0,
+                 reduce2=reduce2)
     check(A.LIB.gspmm_binary_reduce_ex(graph.handle, C.byref(cfg), _ref(mu), _ref(mv), _ref(me),
                                        C.byref(mo), C.byref(opts), _stream(stream, ref_t)),
           "binary_reduce")
@@ -412,7 +425,7 @@ def binary_reduce_host(graph, cfg, u=None, v=None, e=None, *, out=None, want_arg
 
 def binary_reduce_host_async(graph, cfg, u=None, v=None, e=None, *, out, heads=1, stream,
                              wait_event=None, upload_event=None, e_order=EDGE_BY_ID,
-                             arg_other=None, other_scale=None):
+                             arg_other=None, other_scale=None, out2=None, reduce2=SUM):
     """Enqueue-only form of binary_reduce_host (gspmm_binary_reduce_host_async):
     pinned host arrays in and out (``arg_other``: an int32 output array for
     the argmax; ``other_scale``: a host float32 array over the gathered
@@ -431,8 +444,12 @@ def binary_reduce_host_async(graph, cfg, u=None, v=None, e=None, *, out, heads=1
                                     other_scale.shape != (graph.num_cols,) or
                                     not other_scale.flags.c_contiguous):
         raise A.ShapeError(f"other_scale must be a float32 array of {graph.num_cols}")
+    if out2 is not None and (out2.shape != (rows, dim) or out2.dtype != np.float32 or
+                             not out2.flags.c_contiguous):
+        raise A.ShapeError(f"out2 must be a contiguous float32 {rows} x {dim} array")
     mo = A.Out(out.ctypes.data, rows, dim, dim)
-    opts = _opts(heads, _ptr(arg_other), None, _ptr(other_scale))
+    opts = _opts(heads, _ptr(arg_other), None, _ptr(other_scale), out2=_ptr(out2),
+                 reduce2=reduce2)
     ev = lambda x: None if x is None else (x if isinstance(x, int) else x.cuda_event)  # noqa: E731
     st = stream if isinstance(stream, int) else stream.cuda_stream
     check(A.LIB.gspmm_binary_reduce_host_async(graph.handle, C.byref(cfg), _ref(mu), _ref(mv),

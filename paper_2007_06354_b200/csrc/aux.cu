@@ -33,57 +33,65 @@ __global__ void k_permute_edges(const uint32_t* __restrict__ eids, uint64_t m,
   }
 }
 
-// Argmax backward in COLUMN CHUNKS: the f64 accumulator of one chunk of C
-// columns (src_rows x C x 8 B, ~80 MB at most, e.g. 4 columns of config 3's
-// 2.45M rows) stays resident in the 126 MB L2 while every row's C argmax ids
-// and gradients are scattered into it; a second kernel rounds the chunk to
-// fp32 once and zeroes it for the next chunk.  One 2 GB accumulator for all
-// columns (round 1) missed L2 on 65% of its reduction sectors and moved
-// 1.84x the algorithmic bytes.  Targets outside [lo, lo + src_rows) are
-// skipped (a rank's own source rows in the multi-GPU owner-computes form).
+// Argmax backward: a scatter with f64 reductions into a workspace, then one
+// rounding to fp32, so the result is the f64 sum rounded once whatever order
+// the reductions land in.  Targets outside [lo, lo + src_rows) are skipped
+// (a rank's own source rows in the multi-GPU owner-computes form).
+// Measured alternative (r02c/r02d, scripts/mb_argmax_bwd.py): column chunks
+// of 4 with an L2-resident 78 MB accumulator (evict_last reductions,
+// evict_first streams) ran 7.8 ms on config 3 against 2.6 ms for this
+// single pass: each chunk re-reads a 32-byte sector per row for 16 bytes and
+// pays a launch pair, and the chunk's reductions still missed L2.
+// VEC form: a thread owns four consecutive columns (one LDG.128 of the ids
+// and one of the gradients; consecutive threads read consecutive 16-byte
+// pieces of a row).  Measured alternative (r02h): lanes = 32 rows of one
+// column quad with the lanes that share a target combined first
+// (__match_any_sync) -- 3.41 ms on config 3 against 2.62 for this form.
 template <bool VEC>
-__global__ void k_argmax_chunk(const int32_t* __restrict__ arg, int64_t arg_ld,
-                               const float* __restrict__ grad, int64_t grad_ld, uint32_t rows,
-                               int c0, int cw, int64_t lo, uint32_t src_rows, int C,
-                               double* __restrict__ acc) {
+__global__ void k_argmax_scatter(const int32_t* __restrict__ arg, uint32_t rows, uint32_t dim,
+                                 int64_t arg_ld, const float* __restrict__ grad, int64_t grad_ld,
+                                 int64_t lo, uint32_t src_rows, double* __restrict__ acc) {
+  const uint32_t per_row = VEC ? dim / 4 : dim;
+  const uint32_t total = rows * per_row;
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride) {
-    const int32_t* ar = arg + static_cast<int64_t>(r) * arg_ld + c0;
-    const float* gr = grad + static_cast<int64_t>(r) * grad_ld + c0;
-    if constexpr (VEC) {  // cw == C, a multiple of 4, 16-byte aligned rows
-      for (int q = 0; q < cw; q += 4) {
-        const int4 a = __ldcs(reinterpret_cast<const int4*>(ar + q));
-        const float4 g = __ldcs(reinterpret_cast<const float4*>(gr + q));
-        const int32_t av[4] = {a.x, a.y, a.z, a.w};
-        const float gv[4] = {g.x, g.y, g.z, g.w};
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const uint32_t r = i / per_row, q = i - r * per_row;
+    if constexpr (VEC) {
+      const int4 a = __ldcs(reinterpret_cast<const int4*>(arg + r * arg_ld) + q);
+      const float4 g = __ldcs(reinterpret_cast<const float4*>(grad + r * grad_ld) + q);
+      const int32_t av[4] = {a.x, a.y, a.z, a.w};
+      const float gv[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int64_t u = static_cast<int64_t>(av[t]) - lo;
-          if (av[t] >= 0 && static_cast<uint64_t>(u) < src_rows)
-            atomicAdd(acc + u * C + q + t, static_cast<double>(gv[t]));
-        }
+      for (int t = 0; t < 4; ++t) {
+        const int64_t u = static_cast<int64_t>(av[t]) - lo;
+        if (av[t] >= 0 && static_cast<uint64_t>(u) < src_rows)
+          atomicAdd(acc + u * dim + q * 4 + t, static_cast<double>(gv[t]));
       }
     } else {
-      for (int t = 0; t < cw; ++t) {
-        const int32_t a = __ldg(ar + t);
-        const int64_t u = static_cast<int64_t>(a) - lo;
-        if (a >= 0 && static_cast<uint64_t>(u) < src_rows)
-          atomicAdd(acc + u * C + t, static_cast<double>(__ldg(gr + t)));
-      }
+      const int32_t a = __ldg(arg + r * arg_ld + q);
+      const int64_t u = static_cast<int64_t>(a) - lo;
+      if (a >= 0 && static_cast<uint64_t>(u) < src_rows)
+        atomicAdd(acc + u * dim + q, static_cast<double>(__ldg(grad + r * grad_ld + q)));
     }
   }
 }
 
-// out[u, c0 : c0 + cw] = (float) acc[u, :cw]; acc zeroed for the next chunk.
-__global__ void k_argmax_round(double* __restrict__ acc, uint32_t src_rows, int C, int cw,
-                               float* __restrict__ out, int64_t ld, int c0) {
+template <bool VEC>
+__global__ void k_round_f64(const double* __restrict__ acc, uint32_t rows, uint32_t dim,
+                            float* __restrict__ out, int64_t ld) {
+  const uint32_t per_row = VEC ? dim / 4 : dim;
+  const uint32_t total = rows * per_row;
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < src_rows; u += stride) {
-    double* a = acc + static_cast<int64_t>(u) * C;
-    float* o = out + static_cast<int64_t>(u) * ld + c0;
-    for (int t = 0; t < cw; ++t) {
-      o[t] = __double2float_rn(a[t]);
-      a[t] = 0.0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const uint32_t r = i / per_row, q = i - r * per_row;
+    if constexpr (VEC) {
+      const double2 a = __ldcs(reinterpret_cast<const double2*>(acc) + 2 * static_cast<uint64_t>(i));
+      const double2 b = __ldcs(reinterpret_cast<const double2*>(acc) + 2 * static_cast<uint64_t>(i) + 1);
+      reinterpret_cast<float4*>(out + r * ld)[q] =
+          make_float4(__double2float_rn(a.x), __double2float_rn(a.y), __double2float_rn(b.x),
+                      __double2float_rn(b.y));
+    } else {
+      out[r * ld + q] = __double2float_rn(acc[i]);
     }
   }
 }
@@ -151,37 +159,35 @@ cudaError_t launch_argmax_backward(const int32_t* arg, int64_t rows, int64_t dim
                                    float* grad_src, int64_t src_lo, int64_t src_rows,
                                    int64_t src_ld, cudaStream_t s) {
   if (src_rows <= 0 || dim <= 0) return cudaSuccess;
-  if (rows >= (int64_t{1} << 32) || src_rows >= (int64_t{1} << 32)) return cudaErrorInvalidValue;
+  if (rows * dim >= (int64_t{1} << 32) - (int64_t{1} << 24) ||
+      src_rows * dim >= (int64_t{1} << 32) - (int64_t{1} << 24))
+    return cudaErrorInvalidValue;
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
-  const bool vec_layout = dim % 4 == 0 && arg_ld % 4 == 0 && grad_ld % 4 == 0 && al16(arg) &&
-                          al16(grad_out);
-  // chunk width: the widest multiple of 4 whose accumulator fits ~80 MB
-  constexpr double kAccBytes = 80.0 * 1048576.0;
-  int C = static_cast<int>(kAccBytes / (8.0 * static_cast<double>(src_rows))) & ~3;
-  C = std::max(4, std::min<int>(C, static_cast<int>((dim + 3) & ~int64_t{3})));
+  const bool vec = dim % 4 == 0 && arg_ld % 4 == 0 && grad_ld % 4 == 0 && src_ld % 4 == 0 &&
+                   al16(arg) && al16(grad_out) && al16(grad_src);
+  const size_t bytes = sizeof(double) * static_cast<size_t>(src_rows * dim);
   double* acc = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&acc),
-                                  sizeof(double) * static_cast<size_t>(src_rows) * C, s);
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&acc), bytes, s);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(acc, 0, sizeof(double) * static_cast<size_t>(src_rows) * C, s);
-  const unsigned gs = grid_for(rows, 256), gr = grid_for(src_rows, 256);
-  for (int64_t c0 = 0; c0 < dim && e == cudaSuccess; c0 += C) {
-    const int cw = static_cast<int>(std::min<int64_t>(C, dim - c0));
-    if (rows > 0) {
-      if (vec_layout && cw % 4 == 0)
-        k_argmax_chunk<true><<<gs, 256, 0, s>>>(arg, arg_ld, grad_out, grad_ld,
-                                                static_cast<uint32_t>(rows), static_cast<int>(c0),
-                                                cw, src_lo, static_cast<uint32_t>(src_rows), C,
-                                                acc);
-      else
-        k_argmax_chunk<false><<<gs, 256, 0, s>>>(arg, arg_ld, grad_out, grad_ld,
-                                                 static_cast<uint32_t>(rows),
-                                                 static_cast<int>(c0), cw, src_lo,
-                                                 static_cast<uint32_t>(src_rows), C, acc);
-      note_launch();
-    }
-    k_argmax_round<<<gr, 256, 0, s>>>(acc, static_cast<uint32_t>(src_rows), C, cw, grad_src,
-                                      src_ld, static_cast<int>(c0));
+  e = cudaMemsetAsync(acc, 0, bytes, s);
+  const uint32_t R = static_cast<uint32_t>(rows), D = static_cast<uint32_t>(dim);
+  const uint32_t S = static_cast<uint32_t>(src_rows);
+  if (e == cudaSuccess && rows > 0) {
+    const int64_t work = vec ? rows * dim / 4 : rows * dim;
+    if (vec)
+      k_argmax_scatter<true><<<grid_for(work, 256), 256, 0, s>>>(arg, R, D, arg_ld, grad_out,
+                                                                 grad_ld, src_lo, S, acc);
+    else
+      k_argmax_scatter<false><<<grid_for(work, 256), 256, 0, s>>>(arg, R, D, arg_ld, grad_out,
+                                                                  grad_ld, src_lo, S, acc);
+    note_launch();
+  }
+  if (e == cudaSuccess) {
+    const int64_t work = vec ? src_rows * dim / 4 : src_rows * dim;
+    if (vec)
+      k_round_f64<true><<<grid_for(work, 256), 256, 0, s>>>(acc, S, D, grad_src, src_ld);
+    else
+      k_round_f64<false><<<grid_for(work, 256), 256, 0, s>>>(acc, S, D, grad_src, src_ld);
     note_launch();
     e = cudaGetLastError();
   }

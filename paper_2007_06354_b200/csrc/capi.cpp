@@ -160,6 +160,7 @@ struct gspmm_graph_s {
   uint32_t forced_long = 0;     // 0 -> the kLevelThresholds levels
   uint32_t unit_cols = 0;       // 0 -> automatic long-row unit widths
   int rows_kernel_only = 0;     // 1 -> every call on the register kernel (rows.cu)
+  uint32_t long_ctas = 0;       // 0 -> long rows before the segments; N -> concurrent
 };
 
 namespace {
@@ -386,6 +387,17 @@ int bind(const gspmm_graph_s* g, const gspmm_config* cfg, const gspmm_mat* u,
     L.out = out->data;
     L.out_ld = out->ld ? out->ld : w;
   }
+  if (opt->out2) {
+    if (opt->reduce2 != GSPMM_SUM && opt->reduce2 != GSPMM_MEAN)
+      return fail(GSPMM_ERR_CONFIG, "reduce2 must be sum or mean");
+    if (cfg->out == GSPMM_E || is_dot)
+      return fail(GSPMM_ERR_CONFIG, "a second reduction needs a node-destined, non-dot config");
+    if (opt->out2_ld != 0 && opt->out2_ld < w)
+      return fail(GSPMM_ERR_SHAPE, "out2 row stride is below the output width");
+    L.out2 = opt->out2;
+    L.out2_ld = opt->out2_ld ? opt->out2_ld : w;
+    L.mean2 = opt->reduce2 == GSPMM_MEAN;
+  }
 
   // Widest vector every operand layout admits.
   auto vec_ok = [&](int V) {
@@ -397,6 +409,7 @@ int bind(const gspmm_graph_s* g, const gspmm_config* cfg, const gspmm_mat* u,
     };
     if (!ok_op(L.lhs) || !ok_op(L.rhs)) return false;
     if (!is_dot && L.out && !(L.out_ld % V == 0 && aligned(L.out, 4 * V))) return false;
+    if (L.out2 && !(L.out2_ld % V == 0 && aligned(L.out2, 4 * V))) return false;
     return true;
   };
   L.vec = vec_ok(4) ? 4 : vec_ok(2) ? 2 : 1;
@@ -435,7 +448,7 @@ uint32_t source_blocks_for(const gspmm_graph_s* g, const RowLaunch& L) {
   if (pref == 1 || L.acc_in || L.epi) return 1;
   int rw = 0;
   if (!planned(g, L, &rw)) return 1;
-  if (L.lhs.role != ROLE_OTHER || L.arg_other || L.arg_edge) return 1;
+  if (L.lhs.role != ROLE_OTHER || L.arg_other || L.arg_edge || L.out2) return 1;
   if (L.reduce != R_SUM && L.reduce != R_MAX && L.reduce != R_MIN) return 1;
   if (L.rhs.base && L.rhs.role == ROLE_POS) return 1;
   if (pref >= 2) return std::min<uint32_t>(pref, 64);
@@ -492,6 +505,7 @@ int build_source_blocks(gspmm_graph_s* g, uint32_t nb, cudaStream_t s) {
     sg->seg_cost = g->seg_cost;
     sg->forced_long = g->forced_long;
     sg->unit_cols = g->unit_cols;
+    sg->long_ctas = g->long_ctas;
     g->blocks.push_back(sg);
   }
   g->block_nb = nb;
@@ -592,9 +606,31 @@ int run_call(gspmm_graph_s* g, Bound& b, cudaStream_t s) {
   return st ? st : st2;
 }
 
+// The fused second reduction runs in the planned kernels for copy + Max/Min
+// of gathered rows (a second accumulator per column); any other config gets
+// it as a second pass with the second reducer (same result bits).
+bool dual_fused(const gspmm_graph_s* g, const RowLaunch& L) {
+  int rw = 0;
+  return L.out2 && planned(g, L, &rw) && L.binop == B_COPY && !L.rhs.base && !L.other_scale &&
+         (L.reduce == R_MAX || L.reduce == R_MIN) && L.lhs.role == ROLE_OTHER &&
+         L.out2_ld % 4 == 0 && aligned(L.out2, 16);
+}
+
 int launch(gspmm_graph_s* g, CallCtx* ctx, Bound& b, cudaStream_t s) {
   cudaError_t err;
   int rw = 0;
+  if (b.L.out2 && !dual_fused(g, b.L)) {
+    Bound b1 = b, b2 = b;
+    b1.L.out2 = nullptr;
+    b2.L.out2 = nullptr;
+    b2.L.out = b.L.out2;
+    b2.L.out_ld = b.L.out2_ld;
+    b2.L.reduce = R_SUM;
+    b2.L.mean = b.L.mean2;
+    b2.L.arg_other = b2.L.arg_edge = nullptr;
+    const int st = launch(g, ctx, b1, s);
+    return st ? st : launch(g, ctx, b2, s);
+  }
   if (!b.L.out_edge && b.L.binop != GSPMM_DOT && b.L.other_scale && !b.L.rhs.base &&
       b.L.binop == GSPMM_COPY && b.L.lhs.role == ROLE_OTHER && b.L.lhs.mode == MODE_FULL &&
       b.L.lhs.rows > 0 && planned(g, b.L, &rw) &&
@@ -684,9 +720,10 @@ int launch(gspmm_graph_s* g, CallCtx* ctx, Bound& b, cudaStream_t s) {
     p.seg_sw = wide ? W : W <= 256 ? W : 256;
     p.seg_slices = static_cast<uint32_t>((W + p.seg_sw - 1) / p.seg_sw);
     err = cudaSuccess;
+    p.mode = 0;
+    p.n_units = p.n_segs * p.seg_slices;
+    p.counter = ctx->d_counter;
     if (lv.num_long) {
-      // long rows first, alone on the GPU (every SM streams column units),
-      // then the segments: in the same stream, no side stream
       const gspmm_graph_s::Units* units = nullptr;
       const int st = long_units_for(g, li, W, &units);
       if (st) return st;
@@ -695,11 +732,33 @@ int launch(gspmm_graph_s* g, CallCtx* ctx, Bound& b, cudaStream_t s) {
       pl.long_units = units->d;
       pl.n_units = units->n;
       pl.counter = ctx->d_counter + 1;
-      err = launch_gather(pl, s);
+      if (!g->long_ctas || !p.n_units) {
+        // long rows first, on every SM, then the segments (measured on
+        // config 3, r02h: the mean pass 5.48 ms against 9.0 ms with the
+        // long-row CTAs concurrent on an automatic budget, 5.78 on 74 SMs --
+        // a long-row CTA holds its SM's register file, and the segment
+        // kernel, bound by the L2's throughput, needs every SM)
+        err = launch_gather(pl, s);
+      } else {
+        // long-row units on a side stream on long_ctas CTAs, concurrently
+        // with the segment kernel
+        if (!ctx->side) {
+          CUDA_TRY(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "side stream");
+          CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming), "event");
+          CUDA_TRY(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming), "event");
+        }
+        pl.grid = g->long_ctas;
+        CUDA_TRY(cudaEventRecord(ctx->fork, s), "fork");
+        CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->fork, 0), "fork");
+        err = launch_gather(pl, ctx->side);
+        if (err == cudaSuccess) err = cudaEventRecord(ctx->join, ctx->side);
+        if (err == cudaSuccess) err = launch_gather(p, s);
+        const cudaError_t ej = cudaStreamWaitEvent(s, ctx->join, 0);
+        if (err == cudaSuccess) err = ej;
+        if (err != cudaSuccess) return cuda_fail(err, "kernel launch");
+        return GSPMM_OK;
+      }
     }
-    p.mode = 0;
-    p.n_units = p.n_segs * p.seg_slices;
-    p.counter = ctx->d_counter;
     if (err == cudaSuccess && p.n_units) err = launch_gather(p, s);
   } else {
     err = launch_rows(b.L, s);
@@ -1020,6 +1079,7 @@ int gspmm_graph_set_plan(gspmm_graph g, const gspmm_plan* plan) {
   g->forced_long = plan->long_threshold;
   g->unit_cols = plan->unit_cols;
   g->rows_kernel_only = plan->kernel;
+  g->long_ctas = plan->long_ctas;
   for (auto* sg : g->blocks) destroy_graph(sg);
   g->blocks.clear();
   g->block_nb = 0;
@@ -1261,6 +1321,12 @@ static int host_call(gspmm_graph g, const gspmm_config* cfg, const gspmm_mat* u,
       out->rows ? static_cast<size_t>((out->rows - 1) * arg_ld + out->dim) * sizeof(int32_t) : 0;
   const bool ao = opt && opt->arg_other, ae = opt && opt->arg_edge;
   total += (ao ? round_up(arg_bytes) : 0) + (ae ? round_up(arg_bytes) : 0);
+  const int64_t out2_ld = opt && opt->out2_ld ? opt->out2_ld : out->dim;
+  const size_t out2_bytes = opt && opt->out2 && out->rows
+                                ? static_cast<size_t>((out->rows - 1) * out2_ld + out->dim) *
+                                      sizeof(float)
+                                : 0;
+  total += round_up(out2_bytes);
   // other_scale: a HOST array over the gathered (other) endpoint's nodes
   const size_t scale_bytes =
       opt && opt->other_scale ? sizeof(float) * static_cast<size_t>(g->num_cols) : 0;
@@ -1309,6 +1375,10 @@ static int host_call(gspmm_graph g, const gspmm_config* cfg, const gspmm_mat* u,
     dopt.arg_edge = reinterpret_cast<int32_t*>(p);
     p += round_up(arg_bytes);
   }
+  if (out2_bytes) {
+    dopt.out2 = reinterpret_cast<float*>(p);
+    p += round_up(out2_bytes);
+  }
   st = gspmm_binary_reduce_ex(g, cfg, dptr[0], dptr[1], dptr[2], &dout, &dopt, stream);
   if (st) {
     cudaFreeAsync(ws, s);
@@ -1323,6 +1393,9 @@ static int host_call(gspmm_graph g, const gspmm_config* cfg, const gspmm_mat* u,
   if (ae && (ce = cudaMemcpyAsync(opt->arg_edge, dopt.arg_edge, arg_bytes,
                                   cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return bail(ce, "D2H arg");
+  if (out2_bytes && (ce = cudaMemcpyAsync(opt->out2, dopt.out2, out2_bytes,
+                                          cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return bail(ce, "D2H out2");
   CUDA_TRY(cudaFreeAsync(ws, s), "host-call workspace");
   if (sync) CUDA_TRY(cudaStreamSynchronize(s), "synchronize");
   return GSPMM_OK;

@@ -99,17 +99,23 @@ struct RowCursor {
   }
 };
 
-// PART: the kernel instance serves source-blocked passes (acc_in / epi /
-// deg_indptr honoured); the plain instances compile those paths out
-// (measured: the runtime checks cost up to 8% on cfg3 max + argmax).
+// MODE 1 (PART): the kernel instance serves source-blocked passes (acc_in /
+// epi / deg_indptr honoured); the plain instances (MODE 0) compile those
+// paths out (measured: the runtime checks cost up to 8% on cfg3 max +
+// argmax).  MODE 2 (DUAL): a second accumulator folds the same messages with
+// Sum into out2 (Mean when mean2): config 3's max + argmax and mean forward
+// from ONE gather of every source row instead of two passes.  Each output is
+// still its own sequential canonical fold, bit-identical to separate calls.
 // ARG: 0 = no argmax; 1 = track the CSR position of the winner (the ids are
 // looked up at the row's flush); 2 = track the winning neighbour id itself
 // (gathered-row kernels with only arg_other requested: no lookup latency at
 // the flush, measured 0.6 ms of cfg3's 7.7).
-template <int VPL, int ROP, int ARG, bool PART>
+template <int VPL, int ROP, int ARG, int MODE>
 struct Acc {
+  static constexpr bool PART = MODE == 1, DUAL = MODE == 2;
   float a[VPL][4];
   uint32_t arg[VPL][4];
+  float s2[DUAL ? VPL : 1][4];
   __device__ __forceinline__ void reset() {
 #pragma unroll
     for (int v = 0; v < VPL; ++v)
@@ -117,11 +123,13 @@ struct Acc {
       for (int t = 0; t < 4; ++t) {
         a[v][t] = red_identity<ROP>();
         arg[v][t] = 0xffffffffu;
+        if constexpr (DUAL) s2[v][t] = 0.0f;
       }
   }
   __device__ __forceinline__ void fold(int v, const float (&m)[4], uint32_t j) {
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
+      if constexpr (DUAL) s2[v][t] = __fadd_rn(s2[v][t], m[t]);
       if constexpr (ARG) {
         if (red_wins<ROP>(a[v][t], m[t])) {
           a[v][t] = m[t];
@@ -183,6 +191,20 @@ struct Acc {
       for (int t = 0; t < 4; ++t)
         if (c + t < cw) orow[c + t] = o[t];
     }
+    if constexpr (DUAL) {
+      float o2[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        o2[t] = L.mean2 ? (deg ? __fdiv_rn(s2[v][t], __uint2float_rn(deg)) : 0.0f) : s2[v][t];
+      float* orow2 = L.out2 + static_cast<int64_t>(r) * L.out2_ld + c0;
+      if (c + 4 <= cw) {
+        store_vec<4>(orow2 + c, o2);
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (c + t < cw) orow2[c + t] = o2[t];
+      }
+    }
     if constexpr (ARG) {
       const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + c;
 #pragma unroll
@@ -224,7 +246,7 @@ __device__ __forceinline__ float small_value(const RowLaunch& L, int rw, uint32_
 // kept the SMs ~70% issue-busy at 2.5 TB/s of DRAM traffic.
 enum SmallKind : int { SK_NONE = 0, SK_WIN = 1, SK_SCALE = 2, SK_HEAD = 3 };
 
-template <int VPL, int U, int BOP, int ROP, int ARG, int SK, bool LO, bool PART>
+template <int VPL, int U, int BOP, int ROP, int ARG, int SK, bool LO, int MODE>
 __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, bool need_eid,
                                           const float* sbase, int64_t sld, int32_t srole,
                                           int lane) {
@@ -249,7 +271,8 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
 
   RowCursor rc;
   rc.init(L.indptr, u.r0, u.r1, u.e0, lane);
-  Acc<VPL, ROP, ARG, PART> acc;
+  constexpr bool PART = MODE == 1;
+  Acc<VPL, ROP, ARG, MODE> acc;
   acc.begin(L, rc.r, u.c0, u.cw, lane);
 
   // id windows: lane k <-> edge e0 + 32w + k; the next window is in flight
@@ -385,7 +408,7 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
 // narrow slice still keeps every lane busy -- one stage ahead of the stage
 // they store into the shared-memory ring (NB stages, empty/full
 // mbarriers); 4 consumer warps (one or four columns per thread) fold each
-// landed stage.  Neighbour ids ride two stages ahead as cp.async copies into
+// landed stage.  Neighbour ids ride four stages ahead as cp.async copies into
 // a small id ring.
 // Measured (round 1, scripts/mb_gather.cu): random 400 B rows stream at
 // 34 GB/s per SM through LDG.128 into registers against 9.5 GB/s through
@@ -397,13 +420,23 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
 #ifndef LG_DF
 #define LG_DF 8192
 #endif
+#ifndef LG_MR
+#define LG_MR 1024
+#endif
+#ifndef LG_ID
+#define LG_ID 4
+#endif
+#ifndef LG_PIPE
+#define LG_PIPE 1
+#endif
 constexpr int kLgProducers = 12, kLgConsumers = 4;
 constexpr int kLgThreads = 32 * (kLgProducers + kLgConsumers);
 struct LgGeom {
   static constexpr int NB = LG_NB;       // data stages in the ring
   static constexpr int DF = LG_DF;       // data floats per stage
-  static constexpr int MR = 1024;        // max edges per stage
-  static constexpr int NI = 4;           // stage-id slots (stages s .. s + 2 live)
+  static constexpr int MR = LG_MR;       // max edges per stage
+  static constexpr int ID = LG_ID;       // stages the neighbour ids run ahead
+  static constexpr int NI = ID + 4;      // stage-id slots
   static constexpr int SF = 1024;        // small-operand floats per stage
   static constexpr int PL = 32 * kLgProducers;   // producer lanes
   static constexpr int KQ = (DF / 4 + PL - 1) / PL;  // quads per producer lane per stage
@@ -415,10 +448,10 @@ struct LgGeom {
   }
 };
 
-template <int BOP, int ROP, bool ARG, int SK>
+template <int BOP, int ROP, bool ARG, int SK, bool DUAL>
 __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p) {
   using G = LgGeom;
-  constexpr int NB = G::NB, NI = G::NI, KQ = G::KQ, PL = G::PL;
+  constexpr int NB = G::NB, NI = G::NI, KQ = G::KQ, PL = G::PL, ID = G::ID;
   constexpr bool SMALL = SK != SK_NONE;
   extern __shared__ __align__(16) float sm[];
   __shared__ uint32_t s_unit;
@@ -540,23 +573,25 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[b]);
       };
-      fetch_ids(0);
-      cp_async_commit();
-      fetch_ids(1);
-      cp_async_commit();
-      cp_async_wait_group<1>();
+#pragma unroll
+      for (int m = 0; m < ID; ++m) {
+        fetch_ids(static_cast<uint32_t>(m));
+        cp_async_commit();
+      }
+      cp_async_wait_group<ID - 1>();
       named_barrier_sync(1, PL);  // ids of stage 0 visible to every producer
       float4 xa[KQ], xb[KQ];
       int oa[KQ], ob[KQ];
       load_stage(0, xa, oa);
-      // one step: ids two stages ahead, gather stage s + 1, store stage s
+      // one step: ids ID stages ahead, gather stage s + 1, store stage s
       // (two register sets alternate, so no register with a pending load is
-      // ever moved)
+      // ever moved).  With the ids only two stages ahead every step waited
+      // for an id load issued one step earlier (r02d: 13 GB/s per CTA).
       auto step = [&](uint32_t s, float4 (&xc)[KQ], int (&oc)[KQ], float4 (&xn)[KQ],
                       int (&on)[KQ]) {
-        fetch_ids(s + 2);
+        fetch_ids(s + ID);
         cp_async_commit();
-        cp_async_wait_group<1>();
+        cp_async_wait_group<ID - 1>();
         named_barrier_sync(1, PL);  // ids of stage s + 1 visible
         if (s + 1 < rounds) load_stage(s + 1, xn, on);
         store_stage(s, xc, oc);
@@ -575,10 +610,12 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
         const int hrel = (SMALL && rw > 1) ? (c0 + cc) / L.rhs.group - h0 : 0;
         float acc[FW];
         uint32_t arg[FW];
+        float acc2[DUAL ? FW : 1];
 #pragma unroll
         for (int t = 0; t < FW; ++t) {
           acc[t] = red_identity<ROP>();
           arg[t] = 0xffffffffu;
+          if constexpr (DUAL) acc2[t] = 0.0f;
           if (L.acc_in && own && cc + t < cw)  // source-blocked pass: the partial
             acc[t] = L.acc_in[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t];
         }
@@ -590,33 +627,67 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
             const uint32_t cnt = min(R, n - s * R);
             const float* col = sdata + static_cast<size_t>(b) * G::DF + cc;
             const float* sv = ssmall + static_cast<size_t>(b) * G::SF + hrel;
-#pragma unroll 8
-            for (uint32_t e = 0; e < cnt; ++e) {
-              float x[FW];
-              if constexpr (FW == 4) {
-                const float4 v = *reinterpret_cast<const float4*>(col + static_cast<size_t>(e) * slot_f);
-                x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
-              } else {
-                x[0] = col[static_cast<size_t>(e) * slot_f];
-              }
-              float sval = 0.0f;
-              if constexpr (SMALL) sval = sv[e * nh];
+            // blocks of KB edges with the next block's shared-memory loads in
+            // flight while this block folds (two register sets alternate):
+            // the fold is then the add / compare chain itself, not chain +
+            // load latency per block (r02e: ~7.8 cycles per edge, 4 ideal)
+            constexpr int KB = FW == 4 ? 4 : 8;
+            float xa[KB][FW], xb[KB][FW], sa[KB], sb[KB];
+            auto ld = [&](uint32_t e, float (&x)[KB][FW], float (&sv8)[KB]) {
 #pragma unroll
-              for (int t = 0; t < FW; ++t) {
-                float m;
-                if constexpr (SK == SK_SCALE) m = __fmul_rn(bin_apply<BOP>(x[t], 0.0f), sval);
-                else if constexpr (SK == SK_NONE) m = bin_apply<BOP>(x[t], 0.0f);
-                else m = bin_apply<BOP>(x[t], sval);
-                if constexpr (ARG) {
-                  if (red_wins<ROP>(acc[t], m)) {
-                    acc[t] = m;
-                    arg[t] = e0 + s * R + e;
-                  }
+              for (int k = 0; k < KB; ++k) {
+                const uint32_t ek = min(e + k, cnt - 1);  // clamped: inside the stage
+                if constexpr (FW == 4) {
+                  const float4 v = *reinterpret_cast<const float4*>(col + static_cast<size_t>(ek) * slot_f);
+                  x[k][0] = v.x; x[k][1] = v.y; x[k][2] = v.z; x[k][3] = v.w;
                 } else {
-                  acc[t] = red_combine<ROP>(acc[t], m);
+                  x[k][0] = col[static_cast<size_t>(ek) * slot_f];
+                }
+                if constexpr (SMALL) sv8[k] = sv[ek * nh];
+              }
+            };
+            auto fold = [&](uint32_t e, const float (&x)[KB][FW], const float (&sv8)[KB]) {
+#pragma unroll
+              for (int k = 0; k < KB; ++k) {
+                // edges past the stage fold the reduce identity: exact (a
+                // sum from +0 is never -0, so + 0 changes nothing; -inf
+                // never wins a max), and the block stays straight-line code
+                const bool ok = e + k < cnt;
+#pragma unroll
+                for (int t = 0; t < FW; ++t) {
+                  float m;
+                  if constexpr (SK == SK_SCALE) m = __fmul_rn(bin_apply<BOP>(x[k][t], 0.0f), sv8[k]);
+                  else if constexpr (SK == SK_NONE) m = bin_apply<BOP>(x[k][t], 0.0f);
+                  else m = bin_apply<BOP>(x[k][t], sv8[k]);
+                  if constexpr (DUAL) acc2[t] = __fadd_rn(acc2[t], ok ? m : 0.0f);
+                  m = ok ? m : red_identity<ROP>();
+                  if constexpr (ARG) {
+                    if (red_wins<ROP>(acc[t], m)) {
+                      acc[t] = m;
+                      arg[t] = e0 + s * R + e + k;
+                    }
+                  } else {
+                    acc[t] = red_combine<ROP>(acc[t], m);
+                  }
                 }
               }
+            };
+#if LG_PIPE
+            ld(0, xa, sa);
+            for (uint32_t e = 0; e < cnt; e += 2 * KB) {
+              ld(e + KB, xb, sb);
+              fold(e, xa, sa);
+              ld(e + 2 * KB, xa, sa);
+              fold(e + KB, xb, sb);
             }
+#else
+            for (uint32_t e = 0; e < cnt; e += KB) {
+              ld(e, xa, sa);
+              fold(e, xa, sa);
+            }
+            (void)xb;
+            (void)sb;
+#endif
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[b]);
@@ -633,6 +704,9 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
             }
             if (fix && L.mean) a = deg ? __fdiv_rn(a, __uint2float_rn(deg)) : 0.0f;
             L.out[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t] = a;
+            if constexpr (DUAL)
+              L.out2[static_cast<int64_t>(r) * L.out2_ld + c0 + cc + t] =
+                  L.mean2 ? (deg ? __fdiv_rn(acc2[t], __uint2float_rn(deg)) : 0.0f) : acc2[t];
             if constexpr (ARG) {
               const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + cc + t;
               const bool none = arg[t] == 0xffffffffu;
@@ -653,7 +727,7 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
 }
 
 // -------------------------------------------------------------- segments
-template <int VPL, int U, int BOP, int ROP, int ARG, int SK, bool LO, bool PART>
+template <int VPL, int U, int BOP, int ROP, int ARG, int SK, bool LO, int MODE>
 __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : VPL == 5 ? GATHER_MINB5 : GATHER_MINB2) k_gather(const StreamLaunch p) {
   const int lane = threadIdx.x & 31;
   const RowLaunch& L = p.row;
@@ -691,12 +765,12 @@ __global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : VPL == 5 ?
     u.cw = min(p.seg_sw, L.width - u.c0);
     u.e0 = __ldg(L.indptr + u.r0);
     u.e1 = __ldg(L.indptr + u.r1);
-    wide_unit<VPL, U, BOP, ROP, ARG, SK, LO, PART>(L, u, need_eid, sbase, sld, srole, lane);
+    wide_unit<VPL, U, BOP, ROP, ARG, SK, LO, MODE>(L, u, need_eid, sbase, sld, srole, lane);
   }
 }
 
 // p.mode: 0 = row segments (k_gather), 1 = long-row column units (k_long_rg)
-template <int VPL, int BOP, int ROP, int ARG, int SK, bool LO>
+template <int VPL, int BOP, int ROP, int ARG, int SK, bool LO, bool DUAL = false>
 cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
@@ -707,11 +781,11 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
       const RowLaunch& L = p.row;
       const bool eid = L.lhs.role == ROLE_EID || (SK != SK_SCALE && SMALL && L.rhs.role == ROLE_EID);
       const size_t smem = LgGeom::smem_bytes(SMALL, eid);
-      auto* kern = k_long_rg<BOP, ROP, ARG != 0, SK>;
+      auto* kern = k_long_rg<BOP, ROP, ARG != 0, SK, DUAL>;
       e = set_max_dynamic_smem(reinterpret_cast<const void*>(kern),
                                static_cast<int>(LgGeom::smem_bytes(SMALL, true)));
       if (e != cudaSuccess) return e;
-      unsigned grid = static_cast<unsigned>(sms);
+      unsigned grid = p.grid ? p.grid : static_cast<unsigned>(sms);
       if (grid > p.n_units) grid = p.n_units;
       kern<<<grid, kLgThreads, smem, s>>>(p);
     } else {
@@ -719,24 +793,25 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
     }
   } else {
     constexpr int U = VPL == 1 ? GATHER_U1 : VPL == 5 ? GATHER_U5 : GATHER_U2;
+    constexpr int MODE = DUAL ? 2 : 0;
     static std::atomic<int> blocks_per_sm{0};
     int bps = blocks_per_sm.load(std::memory_order_relaxed);
     if (!bps) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps,
-                                                    k_gather<VPL, U, BOP, ROP, ARG, SK, LO, false>,
+                                                    k_gather<VPL, U, BOP, ROP, ARG, SK, LO, MODE>,
                                                     kThreads, 0);
       if (bps < 1) bps = 1;
       blocks_per_sm.store(bps, std::memory_order_relaxed);
     }
     const unsigned grid = static_cast<unsigned>(sms * bps);
-    if constexpr (!ARG) {  // argmax never runs source-blocked
+    if constexpr (!ARG && !DUAL) {  // argmax / dual never run source-blocked
       if (p.row.acc_in || p.row.epi) {
-        k_gather<VPL, U, BOP, ROP, ARG, SK, LO, true><<<grid, kThreads, 0, s>>>(p);
+        k_gather<VPL, U, BOP, ROP, ARG, SK, LO, 1><<<grid, kThreads, 0, s>>>(p);
         note_launch();
         return cudaGetLastError();
       }
     }
-    k_gather<VPL, U, BOP, ROP, ARG, SK, LO, false><<<grid, kThreads, 0, s>>>(p);
+    k_gather<VPL, U, BOP, ROP, ARG, SK, LO, MODE><<<grid, kThreads, 0, s>>>(p);
   }
   note_launch();
   return cudaGetLastError();
@@ -759,6 +834,14 @@ cudaError_t launch_red(const StreamLaunch& p, cudaStream_t s) {
     // instances (argmax of the neighbour id alone: tracked directly);
     // copy_e and other layouts: the generic-role instance
     if (lo) {
+      if constexpr (BOP == B_COPY && K == SK_NONE && (R == R_MAX || R == R_MIN)) {
+        if (L.out2) {  // the host routes only this combination here
+          if constexpr (A) {
+            if (!L.arg_edge) return launch_k<VPL, BOP, R, 2, K, true, true>(p, s);
+          }
+          return launch_k<VPL, BOP, R, A ? 1 : 0, K, true, true>(p, s);
+        }
+      }
       if constexpr (A) {
         if (!L.arg_edge) return launch_k<VPL, BOP, R, 2, K, true>(p, s);
       }

@@ -71,6 +71,11 @@ struct RowLaunch {
   const uint32_t* deg_indptr = nullptr;
   int32_t epi = 0;
   int32_t src_blocks = 0;  // per-call source blocking (0 = the handle's setting)
+  // second reduction of the same messages (Sum, or Mean when mean2) into
+  // out2, fused into the gather (planned kernels, copy + Max/Min only)
+  float* out2 = nullptr;
+  int64_t out2_ld = 0;
+  bool mean2 = false;
 };
 
 // Kernel launchers (rows.cu, dot.cu, aux.cu).  Return cudaGetLastError().

@@ -20,6 +20,7 @@ struct StreamLaunch {
   uint32_t n_units = 0;
   int rhs_width = 0;  // small-operand floats per edge (0 = none, 1 = scalar, H = heads)
   int mode = 0;       // 0 = row segments (k_gather), 1 = long-row units (k_long_rg)
+  uint32_t grid = 0;  // mode 1: CTAs (0 = one per SM)
 };
 
 // The planned row kernels (gather_copy.cu dispatches on the operator).

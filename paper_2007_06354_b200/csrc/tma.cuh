@@ -64,11 +64,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// MBAR_WAIT: 0 = try_wait with a suspend-time hint, 1 = try_wait (default
+// time limit), 2 = test_wait spin.
+#ifndef MBAR_WAIT
+#define MBAR_WAIT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  // try_wait with a suspend-time hint: the warp sleeps until the phase
-  // completes (or the hint elapses) instead of spinning on issue slots
   uint32_t ok = 0;
   while (!ok) {
+#if MBAR_WAIT == 0
+    // try_wait with a suspend-time hint: the warp sleeps until the phase
+    // completes (or the hint elapses) instead of spinning on issue slots
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
@@ -76,6 +82,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "=r"(ok)
         : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
         : "memory");
+#elif MBAR_WAIT == 1
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+#endif
   }
 }
 

@@ -266,3 +266,25 @@ def test_restatement_matches_reference_library(seed):
             assert O.bit_equal(mine, O.ref_binary_reduce(g, cfg, fu, fv, fe, strategy=strategy))
         assert O.bit_equal(O.oracle_aggregate(g, cfg, fu, fv, fe),
                            O.ref_oracle_aggregate(g, cfg, fu, fv, fe))
+
+
+@pytest.mark.parametrize("seed", (101, 107))
+def test_fault_injection_fails_the_checks(golden, seed):
+    # the checker must catch one corrupted element (the reference's
+    # --inject-fault, tools/main.cpp:201-204): a single ulp for the bitwise
+    # reducers, a 1e-3 relative change for the tolerance check
+    p = f"s{seed}_"
+    n = int(golden[p + "n"][0])
+    g = O.Graph(n, golden[p + "src"], golden[p + "dst"])
+    fu, fv, fe = golden[p + "fu"], golden[p + "fv"], golden[p + "fe"]
+    for cname in ("u_mul_e_add_v", "e_copy_max_v"):
+        cfg = O.named_config(cname)
+        got = O.binary_reduce(g, cfg, fu, fv, fe)
+        want = golden[p + "spmm_" + cname]
+        assert O.bit_equal(got, want)
+        i = int(np.argmax(np.abs(got).reshape(-1)))
+        bad = got.reshape(-1).copy()
+        bad[i] = np.nextafter(bad[i], np.float32(np.inf))
+        assert not O.bit_equal(bad.reshape(got.shape), want), cname
+        bad[i] = got.reshape(-1)[i] + np.float32(1e-3) * max(1.0, abs(float(got.reshape(-1)[i])))
+        assert O.max_rel_error(bad.reshape(got.shape), want) > 1e-5, cname

@@ -614,3 +614,43 @@ def test_argmax_backward_vector_and_scalar_paths(dim, pad):
     assert O.max_rel_error(got.cpu().numpy(), want) <= 1e-6
     if pad:
         assert (o_full[:, dim:] == 7.0).all()
+
+
+@pytest.mark.parametrize("long_", [0, 150])
+def test_second_reduction_fused_and_fallback(long_):
+    # out2 / reduce2: a second reduction of the same messages in the same
+    # call -- fused into one gather for copy + max/min (argmax included, long
+    # rows included), a second pass for any other config; always bitwise
+    # equal to the separate call
+    src, dst = O.gen_rmat(3000, 60000, seed=21)
+    g = O.Graph(3000, src, dst)
+    if long_:
+        g.plan = dict(long_threshold=long_)
+    w = O.gcn_weights(3000, src, dst)
+    for dim in (7, 100, 128, 256):
+        x = O.normal_features(3000, dim, dim)
+        xd = cuda(x)
+        h = dev_graph(g, O.DST_MAJOR)
+        mean_want, sum_want = O.mean(g, x), O.binary_reduce(g, O.named_config("u_copy_add_v"), u=x)
+        for red, arg in ((O.MAX, True), (O.MAX, False), (O.MIN, True)):
+            for red2, want2 in ((P.MEAN, mean_want), (P.SUM, sum_want)):
+                o2 = torch.empty((3000, dim), device="cuda")
+                res = P.binary_reduce(h, (O.U, O.NONE, O.COPY, red, O.V), u=xd, out2=o2,
+                                      reduce2=red2, want_arg_other=arg, want_arg_edge=arg)
+                v = res[0] if arg else res
+                want = O.binary_reduce(g, (O.U, O.NONE, O.COPY, red, O.V), u=x)
+                assert O.bit_equal(v.cpu().numpy(), want), (dim, red, red2)
+                assert O.bit_equal(o2.cpu().numpy(), want2), (dim, red, red2)
+                if arg and red == O.MAX:
+                    wv, wa, we = O.copy_max_argmax(g, x)
+                    assert np.array_equal(res[1].cpu().numpy(), wa)
+                    assert np.array_equal(res[2].cpu().numpy(), we)
+        # fallback (second pass): u_mul_e + sum with a mean second output
+        o2 = torch.empty((3000, dim), device="cuda")
+        got = P.binary_reduce(h, "u_mul_e_add_v", u=xd, e=cuda(w), out2=o2, reduce2=P.MEAN)
+        want = O.binary_reduce(g, O.named_config("u_mul_e_add_v"), u=x, e=w)
+        deg = O.in_degree(g).astype(np.float32)[:, None]
+        assert O.bit_equal(got.cpu().numpy(), want)
+        assert O.bit_equal(o2.cpu().numpy(), np.where(deg > 0, want / np.maximum(deg, 1), 0)
+                           .astype(np.float32))
+        g.__dict__.pop("_dev", None)
