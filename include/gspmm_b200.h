@@ -72,7 +72,9 @@ enum {
   GSPMM_ERR_SHAPE = 2,     /* ShapeError: operand/orientation mismatch     */
   GSPMM_ERR_STRUCTURE = 3, /* StructureError: malformed CSR                */
   GSPMM_ERR_CUDA = 4,      /* CUDA runtime failure (no device, OOM, ...)   */
-  GSPMM_ERR_ARG = 5        /* null handle / bad pointer argument           */
+  GSPMM_ERR_ARG = 5,       /* null handle / bad pointer argument           */
+  GSPMM_ERR_IO = 6,        /* IoError: unreadable / corrupt container      */
+  GSPMM_ERR_PARSE = 7      /* ParseError: text input that does not parse   */
 };
 
 /* ---- enums: numeric values of the reference ---- */
@@ -357,6 +359,56 @@ int64_t gspmm_synth_powerlaw(uint32_t n, uint32_t d_min, uint32_t d_max,
 /* GCN weight w[e] = 1/sqrt(deg_out(src[e]) * deg_in(dst[e])), edge-id order */
 void gspmm_synth_gcn_weights(uint32_t n, int64_t m, const uint32_t* src,
                              const uint32_t* dst, float* w, int threads);
+
+/* ---- file containers (io.hpp:25-41, io.cpp:80-207) ----
+ * FMAT1: "FMAT1", u64 rows, u64 dim, rows * dim float32 (little-endian).
+ * CSR1:  "CSR1", u8 orientation (0 src-major, else dst-major), u64 num_rows,
+ *        num_cols, num_edges, then indptr / indices / edge_ids as u64 arrays.
+ * Failures are GSPMM_ERR_IO with the reference's IoError messages ("cannot
+ * open ...", "... not a CSR1 file", "... truncated file", "... invalid CSR
+ * payload: <validate() message>"). */
+int gspmm_fmat1_info(const char* path, int64_t* rows, int64_t* dim);
+/* load_feature_matrix (io.cpp:149-166) into a HOST buffer of row stride ld
+ * (0 -> dim). */
+int gspmm_fmat1_read(const char* path, float* data, int64_t ld);
+/* The same into a DEVICE buffer on `device` (row stride ld, 0 -> dim; pad
+ * columns untouched): the file streams through a pinned ring, the read of
+ * one chunk overlapping the DMA of the previous.  Synchronizes `stream`. */
+int gspmm_fmat1_read_device(const char* path, int device, float* d_data,
+                            int64_t ld, void* stream);
+/* save_feature_matrix (io.cpp:137-147) from a host matrix. */
+int gspmm_fmat1_write(const char* path, const float* data, int64_t rows,
+                      int64_t dim, int64_t ld);
+int gspmm_csr1_info(const char* path, int* orientation, uint64_t* num_rows,
+                    uint64_t* num_cols, uint64_t* num_edges);
+/* load_csr (io.cpp:183-205) into HOST arrays sized from gspmm_csr1_info
+ * (indptr num_rows + 1, indices / edge_ids num_edges); validated. */
+int gspmm_csr1_read(const char* path, uint32_t* indptr, uint32_t* indices,
+                    uint32_t* edge_ids);
+/* save_csr (io.cpp:168-181). */
+int gspmm_csr1_write(const char* path, int orientation, uint32_t num_rows,
+                     uint32_t num_cols, const uint32_t* indptr,
+                     const uint32_t* indices, const uint32_t* edge_ids);
+/* load_csr straight to a device graph handle: the 64-bit payload streams
+ * through a pinned ring, is narrowed to 32-bit ids on the device (an id
+ * above 2^32 - 1 is an IoError, io.cpp:71-73) and checked on the device with
+ * validate()'s rules and messages (csr.cpp:111-156) before the plan is built. */
+int gspmm_graph_load_csr1(const char* path, int device, gspmm_graph* out);
+/* validate() (csr.cpp:111-156) of a DEVICE CSR, e.g. before
+ * gspmm_graph_create_device: GSPMM_ERR_STRUCTURE with the reference's
+ * message (the lowest offending nonzero, as its sequential scan reports). */
+int gspmm_validate_csr_device(int device, uint32_t num_rows, uint32_t num_cols,
+                              const uint32_t* d_indptr, const uint32_t* d_indices,
+                              const uint32_t* d_edge_ids, void* stream);
+/* load_edge_list / save_edge_list (io.cpp:80-135): "src dst" per line, '#'
+ * comments, optional "%nodes N".  src / dst are malloc'ed (gspmm_free); they
+ * feed gspmm_build_csr[_device].  Parse failures are GSPMM_ERR_PARSE with
+ * "<path>:<line>: <what>". */
+int gspmm_edge_list_read(const char* path, uint32_t* num_nodes,
+                         uint64_t* num_edges, uint32_t** src, uint32_t** dst);
+int gspmm_edge_list_write(const char* path, uint32_t num_nodes,
+                          uint64_t num_edges, const uint32_t* src,
+                          const uint32_t* dst);
 
 #ifdef __cplusplus
 }

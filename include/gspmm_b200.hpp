@@ -9,7 +9,10 @@
 //     named_config, config_name
 //   CsrGraph, FeatureMatrix            csr.hpp:37-54, feature_matrix.hpp:29-66
 //   StructureError/ShapeError/         error.hpp:22-45
-//     ConfigError
+//     ConfigError/ParseError/IoError
+//   load_csr / save_csr, load_ /       io.hpp:25-41
+//     save_feature_matrix, load_ /
+//     save_edge_list
 // It lives in namespace gspmm_b200 so a program can link it next to the
 // reference (the parity harness does).  A caller switches by changing the
 // namespace (or a `namespace gspmm = gspmm_b200;` alias).
@@ -46,6 +49,12 @@ struct ShapeError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ParseError : std::runtime_error {  // text input that does not parse
+  using std::runtime_error::runtime_error;
+};
+struct IoError : std::runtime_error {  // file failure or corrupt container
   using std::runtime_error::runtime_error;
 };
 // CUDA failures (no device, out of memory): the path has no CPU fallback.
@@ -122,6 +131,24 @@ FeatureMatrix binary_reduce(Strategy strategy, const CsrGraph& g,
 FeatureMatrix copy_reduce(Strategy strategy, const CsrGraph& g,
                           const FeatureMatrix& src_feats, ReduceOp reduce,
                           const BlockPlan* plan = nullptr, int threads = 0);
+
+// File containers (io.hpp:25-41): same signatures, formats and failures.
+struct Edge {
+  NodeId src;
+  NodeId dst;
+  friend bool operator==(const Edge&, const Edge&) = default;
+};
+struct EdgeList {  // edge_list.hpp:35-40: the edge id of edges[i] is i
+  NodeId num_nodes = 0;
+  std::vector<Edge> edges;
+  EdgeId num_edges() const { return static_cast<EdgeId>(edges.size()); }
+};
+EdgeList load_edge_list(const std::string& path);
+void save_edge_list(const std::string& path, const EdgeList& edges);
+void save_feature_matrix(const std::string& path, const FeatureMatrix& f);
+FeatureMatrix load_feature_matrix(const std::string& path);
+void save_csr(const std::string& path, const CsrGraph& g);
+CsrGraph load_csr(const std::string& path);
 
 // Throws the exception matching a C-ABI status (no-op for GSPMM_OK).
 void throw_status(int status);

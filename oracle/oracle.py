@@ -132,6 +132,18 @@ def _load_ref():
         "ref_run_graph": (dbl, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, i32, vp, i64]),
         "ref_bench_case": (dbl, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, i32, i32, i32,
                                  C.POINTER(dbl), C.POINTER(dbl)]),
+        "ref_io_error": (C.c_char_p, []),
+        "ref_save_csr": (i32, [C.c_char_p, vp]),
+        "ref_load_csr": (i32, [C.c_char_p, C.POINTER(vp), C.POINTER(i32), C.POINTER(u32),
+                               C.POINTER(u32), C.POINTER(u64)]),
+        "ref_graph_arrays": (None, [vp, vp, vp, vp]),
+        "ref_save_feature_matrix": (i32, [C.c_char_p, vp]),
+        "ref_load_feature_matrix": (i32, [C.c_char_p, C.POINTER(vp), C.POINTER(i64),
+                                          C.POINTER(i64)]),
+        "ref_feat_data": (None, [vp, vp]),
+        "ref_save_edge_list": (i32, [C.c_char_p, u32, i64, vp, vp]),
+        "ref_load_edge_list": (i32, [C.c_char_p, C.POINTER(u32), C.POINTER(i64),
+                                     C.POINTER(_u32p), C.POINTER(_u32p)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -667,3 +679,133 @@ class RefGraph:
             self.close()
         except Exception:
             pass
+
+
+# ------------------------------------------------ file containers
+# numpy restatement of the reference's binary containers (io.hpp:29-41,
+# io.cpp:137-205) and thin wrappers over the reference's own readers /
+# writers (oracle/_ref), for the loader round-trip tests.
+IO_ERROR, PARSE_ERROR = 6, 7
+
+
+def write_fmat1(path, a):
+    """save_feature_matrix (io.cpp:137-147)."""
+    a = np.ascontiguousarray(a, np.float32)
+    with open(path, "wb") as f:
+        f.write(b"FMAT1")
+        f.write(np.array(a.shape, "<u8").tobytes())
+        f.write(a.astype("<f4", copy=False).tobytes())
+
+
+def read_fmat1(path):
+    """load_feature_matrix (io.cpp:149-166); OracleError(IO_ERROR) on a bad file."""
+    try:
+        raw = open(path, "rb").read()
+    except OSError:
+        raise OracleError(IO_ERROR, "cannot open " + path)
+    if raw[:5] != b"FMAT1":
+        raise OracleError(IO_ERROR, path + ": not a FMAT1 file")
+    if len(raw) < 21:
+        raise OracleError(IO_ERROR, path + ": truncated file")
+    rows, dim = (int(v) for v in np.frombuffer(raw, "<u8", 2, 5))
+    if len(raw) - 21 < rows * dim * 4:
+        raise OracleError(IO_ERROR, path + ": truncated data section")
+    return np.frombuffer(raw, "<f4", rows * dim, 21).reshape(rows, dim).copy()
+
+
+def write_csr1(path, orientation, num_rows, num_cols, indptr, indices, eids):
+    """save_csr (io.cpp:168-181): every element as a 64-bit little-endian word."""
+    with open(path, "wb") as f:
+        f.write(b"CSR1")
+        f.write(bytes([1 if orientation == DST_MAJOR else 0]))
+        f.write(np.array([num_rows, num_cols, int(indptr[num_rows])], "<u8").tobytes())
+        for a in (indptr[:num_rows + 1], indices[:int(indptr[num_rows])],
+                  eids[:int(indptr[num_rows])]):
+            f.write(np.asarray(a).astype("<u8").tobytes())
+
+
+def read_csr1(path):
+    """load_csr (io.cpp:183-205) -> (orientation, num_rows, num_cols, indptr,
+    indices, eids) as uint32 arrays; the payload is validated (csr.cpp:111-156)."""
+    try:
+        raw = open(path, "rb").read()
+    except OSError:
+        raise OracleError(IO_ERROR, "cannot open " + path)
+    if raw[:4] != b"CSR1":
+        raise OracleError(IO_ERROR, path + ": not a CSR1 file")
+    if len(raw) < 29:
+        raise OracleError(IO_ERROR, path + ": truncated file")
+    orientation = DST_MAJOR if raw[4] else SRC_MAJOR
+    rows, cols, m = (int(v) for v in np.frombuffer(raw, "<u8", 3, 5))
+    if len(raw) - 29 < 8 * (rows + 1 + 2 * m):
+        raise OracleError(IO_ERROR, path + ": truncated file")
+    arrs, off = [], 29
+    for count in (rows + 1, m, m):
+        a = np.frombuffer(raw, "<u8", count, off)
+        off += 8 * count
+        if count and int(a.max()) > 0xffffffff:
+            raise OracleError(IO_ERROR, path + ": id does not fit the configured id width")
+        arrs.append(a.astype(np.uint32))
+    bad = validate(rows, cols, *arrs)
+    if bad:
+        raise OracleError(IO_ERROR, path + ": invalid CSR payload: " + bad)
+    return (orientation, rows, cols, *arrs)
+
+
+def _ref_io(st, what):
+    if st:
+        raise OracleError(st, what + ": " + REF.ref_io_error().decode(errors="replace"))
+
+
+def ref_save_csr(path, orientation, num_rows, num_cols, indptr, indices, eids):
+    g = RefGraph(orientation, num_rows, num_cols, indptr, indices, eids)
+    try:
+        _ref_io(REF.ref_save_csr(os.fsencode(path), g.h), "save_csr")
+    finally:
+        g.close()
+
+
+def ref_load_csr(path):
+    h, o, r, c, m = C.c_void_p(), C.c_int(), C.c_uint32(), C.c_uint32(), C.c_uint64()
+    _ref_io(REF.ref_load_csr(os.fsencode(path), C.byref(h), C.byref(o), C.byref(r), C.byref(c),
+                             C.byref(m)), "load_csr")
+    indptr = np.empty(r.value + 1, np.uint32)
+    indices = np.empty(max(m.value, 1), np.uint32)
+    eids = np.empty(max(m.value, 1), np.uint32)
+    REF.ref_graph_arrays(h, indptr.ctypes.data, indices.ctypes.data, eids.ctypes.data)
+    REF.ref_graph_free(h)
+    return o.value, r.value, c.value, indptr, indices[:m.value], eids[:m.value]
+
+
+def ref_save_feature_matrix(path, a):
+    a = np.ascontiguousarray(a, np.float32)
+    f = REF.ref_feat_create(a.shape[0], a.shape[1], a.ctypes.data)
+    try:
+        _ref_io(REF.ref_save_feature_matrix(os.fsencode(path), f), "save_feature_matrix")
+    finally:
+        REF.ref_feat_free(f)
+
+
+def ref_load_feature_matrix(path):
+    f, r, d = C.c_void_p(), C.c_int64(), C.c_int64()
+    _ref_io(REF.ref_load_feature_matrix(os.fsencode(path), C.byref(f), C.byref(r), C.byref(d)),
+            "load_feature_matrix")
+    out = np.empty((r.value, d.value), np.float32)
+    REF.ref_feat_data(f, out.ctypes.data)
+    REF.ref_feat_free(f)
+    return out
+
+
+def ref_save_edge_list(path, n, src, dst):
+    src = np.ascontiguousarray(src, np.uint32)
+    dst = np.ascontiguousarray(dst, np.uint32)
+    _ref_io(REF.ref_save_edge_list(os.fsencode(path), n, len(src), _ptr(src), _ptr(dst)),
+            "save_edge_list")
+
+
+def ref_load_edge_list(path):
+    n, m, ps, pd = C.c_uint32(), C.c_int64(), _u32p(), _u32p()
+    _ref_io(REF.ref_load_edge_list(os.fsencode(path), C.byref(n), C.byref(m), C.byref(ps),
+                                   C.byref(pd)), "load_edge_list")
+    src, dst = _take_edges(m.value, ps, pd, REF.ref_free)
+    return n.value, src, dst

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <string>
 #include <vector>
 
 #include "gspmm/bench.hpp"
@@ -18,6 +19,7 @@
 #include "gspmm/csr.hpp"
 #include "gspmm/error.hpp"
 #include "gspmm/generate.hpp"
+#include "gspmm/io.hpp"
 #include "gspmm/kernels.hpp"
 #include "gspmm/oracle.hpp"
 
@@ -34,6 +36,10 @@ int status_of(const std::exception_ptr& p) {
     return 2;
   } catch (const StructureError&) {
     return 3;
+  } catch (const IoError&) {
+    return 6;
+  } catch (const ParseError&) {
+    return 7;
   } catch (...) {
     return 9;
   }
@@ -366,6 +372,115 @@ double ref_run_graph(void* graph, int strategy, int lhs, int rhs, int binop, int
     return dt;
   } catch (...) {
     return -static_cast<double>(status_of(std::current_exception()));
+  }
+}
+
+// ---- file containers (io.hpp:25-41): the reference's own writers and
+// readers, for the CSR1 / FMAT1 / edge-list round-trip tests ------------------
+
+thread_local std::string g_io_msg;
+const char* ref_io_error(void) { return g_io_msg.c_str(); }
+
+namespace {
+int io_status(const std::exception_ptr& p) {
+  try {
+    std::rethrow_exception(p);
+  } catch (const std::exception& e) {
+    g_io_msg = e.what();
+  } catch (...) {
+    g_io_msg = "unknown";
+  }
+  return status_of(p);
+}
+}  // namespace
+
+int ref_save_csr(const char* path, void* graph) {
+  try {
+    save_csr(path, *static_cast<CsrGraph*>(graph));
+    return 0;
+  } catch (...) {
+    return io_status(std::current_exception());
+  }
+}
+
+// load_csr -> a graph handle (ref_graph_free) and its sizes
+int ref_load_csr(const char* path, void** graph, int* orientation, uint32_t* num_rows,
+                 uint32_t* num_cols, uint64_t* num_edges) {
+  try {
+    auto* g = new CsrGraph(load_csr(path));
+    *graph = g;
+    *orientation = g->orientation == Orientation::DstMajor ? 1 : 0;
+    *num_rows = g->num_rows;
+    *num_cols = g->num_cols;
+    *num_edges = g->num_edges();
+    return 0;
+  } catch (...) {
+    return io_status(std::current_exception());
+  }
+}
+
+void ref_graph_arrays(void* graph, uint32_t* indptr, uint32_t* indices, uint32_t* eids) {
+  const CsrGraph& g = *static_cast<CsrGraph*>(graph);
+  std::memcpy(indptr, g.indptr.data(), g.indptr.size() * sizeof(uint32_t));
+  std::memcpy(indices, g.indices.data(), g.indices.size() * sizeof(uint32_t));
+  std::memcpy(eids, g.edge_ids.data(), g.edge_ids.size() * sizeof(uint32_t));
+}
+
+int ref_save_feature_matrix(const char* path, void* feat) {
+  try {
+    save_feature_matrix(path, *static_cast<FeatureMatrix*>(feat));
+    return 0;
+  } catch (...) {
+    return io_status(std::current_exception());
+  }
+}
+
+int ref_load_feature_matrix(const char* path, void** feat, int64_t* rows, int64_t* dim) {
+  try {
+    auto* f = new FeatureMatrix(load_feature_matrix(path));
+    *feat = f;
+    *rows = f->rows;
+    *dim = f->dim;
+    return 0;
+  } catch (...) {
+    return io_status(std::current_exception());
+  }
+}
+
+void ref_feat_data(void* feat, float* out) {
+  const FeatureMatrix& f = *static_cast<FeatureMatrix*>(feat);
+  std::memcpy(out, f.data.data(), f.data.size() * sizeof(float));
+}
+
+int ref_save_edge_list(const char* path, uint32_t n, int64_t m, const uint32_t* src,
+                       const uint32_t* dst) {
+  try {
+    EdgeList el;
+    el.num_nodes = n;
+    el.edges.resize(m);
+    for (int64_t i = 0; i < m; ++i) el.edges[i] = Edge{src[i], dst[i]};
+    save_edge_list(path, el);
+    return 0;
+  } catch (...) {
+    return io_status(std::current_exception());
+  }
+}
+
+int ref_load_edge_list(const char* path, uint32_t* n, int64_t* m, uint32_t** src, uint32_t** dst) {
+  try {
+    const EdgeList el = load_edge_list(path);
+    const std::size_t k = el.edges.size();
+    *n = el.num_nodes;
+    *m = static_cast<int64_t>(k);
+    *src = static_cast<uint32_t*>(std::malloc((k ? k : 1) * sizeof(uint32_t)));
+    *dst = static_cast<uint32_t*>(std::malloc((k ? k : 1) * sizeof(uint32_t)));
+    for (std::size_t i = 0; i < k; ++i) {
+      (*src)[i] = el.edges[i].src;
+      (*dst)[i] = el.edges[i].dst;
+    }
+    return 0;
+  } catch (...) {
+    return io_status(std::current_exception());
   }
 }
 

@@ -8,8 +8,8 @@ See DESIGN.md.
 from . import _capi
 from ._capi import (ADD, COPY, COPY_LAST, DIV, DOT, DST_MAJOR, E, EDGE_BY_ID, EDGE_BY_POS, MAX,
                     MEAN, MIN, MUL, NONE, PROD, PULL, PUSH, BLOCKED, SPMM, SRC_MAJOR, SUB, SUM,
-                    U, V, ArgumentError, ConfigError, DeviceError, GspmmError, ShapeError,
-                    StructureError)
+                    U, V, ArgumentError, ConfigError, DeviceError, GspmmError, IoError, ParseError,
+                    ShapeError, StructureError)
 from .api import *  # noqa: F401,F403
 from .api import __all__ as _api_all
 

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libgspmm_b200.so")
 
 # status codes
-OK, ERR_CONFIG, ERR_SHAPE, ERR_STRUCTURE, ERR_CUDA, ERR_ARG = 0, 1, 2, 3, 4, 5
+OK, ERR_CONFIG, ERR_SHAPE, ERR_STRUCTURE, ERR_CUDA, ERR_ARG, ERR_IO, ERR_PARSE = 0, 1, 2, 3, 4, 5, 6, 7
 # enums (reference numeric values)
 U, V, E, NONE = 0, 1, 2, 3
 ADD, SUB, MUL, DIV, DOT, COPY = 0, 1, 2, 3, 4, 5
@@ -47,8 +47,16 @@ class ArgumentError(GspmmError):
     status = ERR_ARG
 
 
+class IoError(GspmmError):
+    status = ERR_IO
+
+
+class ParseError(GspmmError):
+    status = ERR_PARSE
+
+
 _ERRORS = {ERR_CONFIG: ConfigError, ERR_SHAPE: ShapeError, ERR_STRUCTURE: StructureError,
-           ERR_CUDA: DeviceError, ERR_ARG: ArgumentError}
+           ERR_CUDA: DeviceError, ERR_ARG: ArgumentError, ERR_IO: IoError, ERR_PARSE: ParseError}
 
 
 class Config(C.Structure):
@@ -127,6 +135,17 @@ SIGNATURES = {
     "gspmm_synth_normal": (None, [_i64, _u64, _vp, _i32]),
     "gspmm_synth_gcn_weights": (None, [_u32, _i64, _vp, _vp, _vp, _i32]),
     "gspmm_synth_powerlaw": (_i64, [_u32, _u32, _u32, _u64, _vp, _vp, _i32]),
+    "gspmm_fmat1_info": (_i32, [C.c_char_p, _P(_i64), _P(_i64)]),
+    "gspmm_fmat1_read": (_i32, [C.c_char_p, _vp, _i64]),
+    "gspmm_fmat1_read_device": (_i32, [C.c_char_p, _i32, _vp, _i64, _vp]),
+    "gspmm_fmat1_write": (_i32, [C.c_char_p, _vp, _i64, _i64, _i64]),
+    "gspmm_csr1_info": (_i32, [C.c_char_p, _P(_i32), _P(_u64), _P(_u64), _P(_u64)]),
+    "gspmm_csr1_read": (_i32, [C.c_char_p, _vp, _vp, _vp]),
+    "gspmm_csr1_write": (_i32, [C.c_char_p, _i32, _u32, _u32, _vp, _vp, _vp]),
+    "gspmm_graph_load_csr1": (_i32, [C.c_char_p, _i32, _P(_vp)]),
+    "gspmm_validate_csr_device": (_i32, [_i32, _u32, _u32, _vp, _vp, _vp, _vp]),
+    "gspmm_edge_list_read": (_i32, [C.c_char_p, _P(_u32), _P(_u64), _P(_vp), _P(_vp)]),
+    "gspmm_edge_list_write": (_i32, [C.c_char_p, _u32, _u64, _vp, _vp]),
 }
 
 

@@ -23,6 +23,8 @@ __all__ = [
     "synth_rmat", "synth_er", "build_csr", "transpose", "synth_uniform", "synth_normal",
     "synth_gcn_weights", "synth_powerlaw", "launch_count", "edge_softmax", "edge_softmax_backward",
     "build_csr_device", "transpose_device",
+    "load_feature_matrix", "save_feature_matrix", "load_csr", "save_csr", "load_graph",
+    "validate_csr_device", "load_edge_list", "save_edge_list",
 ]
 
 
@@ -112,6 +114,22 @@ class Graph:
         nl = C.c_uint32()
         check(A.LIB.gspmm_graph_info(h, None, None, None, None, C.byref(nl)))
         self.num_long_rows = nl.value
+        return self
+
+    @classmethod
+    def load(cls, path, device=0):
+        """load_csr (io.cpp:183-205) of a CSR1 container straight to a device
+        handle: the payload streams through a pinned ring, is narrowed to
+        32-bit ids and validated on the device (csr.cpp:111-156)."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        check(A.LIB.gspmm_graph_load_csr1(_path(path), device, C.byref(h)), "load_csr")
+        self._h = h
+        o, r, c_, m, nl = C.c_int(), C.c_uint32(), C.c_uint32(), C.c_uint64(), C.c_uint32()
+        check(A.LIB.gspmm_graph_info(h, C.byref(o), C.byref(r), C.byref(c_), C.byref(m),
+                                     C.byref(nl)))
+        self.orientation, self.num_rows, self.num_cols = o.value, r.value, c_.value
+        self.num_edges, self.num_long_rows, self.device = m.value, nl.value, device
         return self
 
     @property
@@ -562,3 +580,98 @@ def synth_gcn_weights(n, src, dst, threads=0):
     w = np.empty((len(src), 1), np.float32)
     A.LIB.gspmm_synth_gcn_weights(n, len(src), _ptr(src), _ptr(dst), w.ctypes.data, threads)
     return w
+
+
+# ------------------------------------------------- file containers (io.hpp)
+def _path(path):
+    import os
+    return os.fsencode(path)
+
+
+def load_feature_matrix(path, device=None, ld=0):
+    """load_feature_matrix (io.cpp:149-166) of a FMAT1 container.  device None:
+    a numpy array; else a CUDA tensor on that device, streamed through a
+    pinned ring (``ld`` > dim pads the device rows, e.g. 604 for 602 columns;
+    the view returned is [rows, dim])."""
+    rows, dim = C.c_int64(), C.c_int64()
+    check(A.LIB.gspmm_fmat1_info(_path(path), C.byref(rows), C.byref(dim)), "load_feature_matrix")
+    rows, dim = rows.value, dim.value
+    if device is None:
+        out = np.empty((rows, dim), np.float32)
+        check(A.LIB.gspmm_fmat1_read(_path(path), _ptr(out), 0), "load_feature_matrix")
+        return out
+    import torch
+    ld = ld or dim
+    dev = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+    buf = torch.empty((rows, ld), dtype=torch.float32, device=dev)
+    check(A.LIB.gspmm_fmat1_read_device(_path(path), dev.index or 0, buf.data_ptr(), ld,
+                                        _stream(None, buf)), "load_feature_matrix")
+    return buf[:, :dim]
+
+
+def save_feature_matrix(path, a):
+    """save_feature_matrix (io.cpp:137-147) from a 2-D float32 host array."""
+    a = np.asarray(a, np.float32)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    if a.ndim != 2:
+        raise A.ArgumentError("save_feature_matrix: a 2-D matrix is required")
+    if a.size and (a.strides[1] != 4 or a.strides[0] % 4 or a.strides[0] < 4 * a.shape[1]):
+        a = np.ascontiguousarray(a)
+    ld = a.strides[0] // 4 if a.shape[0] > 1 and a.size else a.shape[1]
+    check(A.LIB.gspmm_fmat1_write(_path(path), _ptr(a), a.shape[0], a.shape[1], ld),
+          "save_feature_matrix")
+
+
+def load_csr(path):
+    """load_csr (io.cpp:183-205) into host arrays: (orientation, num_rows,
+    num_cols, indptr, indices, edge_ids), validated."""
+    o, r, c_, m = C.c_int(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+    check(A.LIB.gspmm_csr1_info(_path(path), C.byref(o), C.byref(r), C.byref(c_), C.byref(m)),
+          "load_csr")
+    indptr = np.empty(r.value + 1, np.uint32)
+    indices = np.empty(max(m.value, 1), np.uint32)
+    eids = np.empty(max(m.value, 1), np.uint32)
+    check(A.LIB.gspmm_csr1_read(_path(path), _ptr(indptr), _ptr(indices), _ptr(eids)), "load_csr")
+    return o.value, r.value, c_.value, indptr, indices[:m.value], eids[:m.value]
+
+
+def save_csr(path, orientation, num_rows, num_cols, indptr, indices, edge_ids):
+    """save_csr (io.cpp:168-181)."""
+    indptr, indices, edge_ids = _u32(indptr), _u32(indices), _u32(edge_ids)
+    check(A.LIB.gspmm_csr1_write(_path(path), orientation, num_rows, num_cols, _ptr(indptr),
+                                 _ptr(indices), _ptr(edge_ids)), "save_csr")
+
+
+def load_graph(path, device=0):
+    """A CSR1 container as a device Graph (``Graph.load``)."""
+    return Graph.load(path, device)
+
+
+def validate_csr_device(num_rows, num_cols, indptr, indices, edge_ids, stream=None):
+    """validate() (csr.cpp:111-156) of a device CSR (int32 CUDA tensors);
+    raises StructureError with the reference's message."""
+    check(A.LIB.gspmm_validate_csr_device(indptr.device.index or 0, num_rows, num_cols,
+                                          indptr.data_ptr(), indices.data_ptr(),
+                                          edge_ids.data_ptr(), _stream(stream, indptr)),
+          "validate")
+
+
+def load_edge_list(path):
+    """load_edge_list (io.cpp:80-127): (num_nodes, src, dst)."""
+    n, m, ps, pd = C.c_uint32(), C.c_uint64(), C.c_void_p(), C.c_void_p()
+    check(A.LIB.gspmm_edge_list_read(_path(path), C.byref(n), C.byref(m), C.byref(ps),
+                                     C.byref(pd)), "load_edge_list")
+    cap = max(m.value, 1)
+    src = np.ctypeslib.as_array(C.cast(ps, C.POINTER(C.c_uint32)), shape=(cap,))[:m.value].copy()
+    dst = np.ctypeslib.as_array(C.cast(pd, C.POINTER(C.c_uint32)), shape=(cap,))[:m.value].copy()
+    A.LIB.gspmm_free(ps)
+    A.LIB.gspmm_free(pd)
+    return n.value, src, dst
+
+
+def save_edge_list(path, num_nodes, src, dst):
+    """save_edge_list (io.cpp:129-135)."""
+    src, dst = _u32(src), _u32(dst)
+    check(A.LIB.gspmm_edge_list_write(_path(path), num_nodes, len(src), _ptr(src), _ptr(dst)),
+          "save_edge_list")

@@ -874,6 +874,14 @@ size_t round_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 }  // namespace
 
+namespace gspmm_b200 {
+int set_last_error(int status, const std::string& msg) { return fail(status, msg); }
+int validate_csr_host(uint32_t num_rows, uint32_t num_cols, const uint32_t* indptr,
+                      const uint32_t* indices, const uint32_t* eids) {
+  return validate_host(num_rows, num_cols, indptr, indices, eids);
+}
+}  // namespace gspmm_b200
+
 extern "C" {
 
 const char* gspmm_last_error(void) { return g_err.c_str(); }

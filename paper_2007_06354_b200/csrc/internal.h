@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
+
 namespace gspmm_b200 {
 
 // Which endpoint of an edge an operand row is taken from, resolved by the
@@ -146,6 +148,13 @@ cudaError_t launch_scale_rows(const float* x, int64_t rows, int64_t dim, int64_t
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device),
 // thread-safe (aux.cu).
 cudaError_t set_max_dynamic_smem(const void* func, int bytes);
+
+// The thread-local message behind gspmm_last_error(); returns `status`.
+int set_last_error(int status, const std::string& msg);
+// validate() of host CSR arrays (csr.cpp:111-156); GSPMM_ERR_STRUCTURE with
+// the reference's message on failure.
+int validate_csr_host(uint32_t num_rows, uint32_t num_cols, const uint32_t* indptr,
+                      const uint32_t* indices, const uint32_t* eids);
 
 // Launch counter (evidence of native execution), bumped by each launcher.
 void note_launch(uint64_t n = 1);

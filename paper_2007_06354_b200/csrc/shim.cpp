@@ -23,6 +23,8 @@ void throw_status(int st) {
     case GSPMM_ERR_CONFIG: throw ConfigError(msg);
     case GSPMM_ERR_SHAPE: throw ShapeError(msg);
     case GSPMM_ERR_STRUCTURE: throw StructureError(msg);
+    case GSPMM_ERR_IO: throw IoError(msg);
+    case GSPMM_ERR_PARSE: throw ParseError(msg);
     default: throw DeviceError(msg);
   }
 }
@@ -311,6 +313,65 @@ FeatureMatrix copy_reduce(Strategy strategy, const CsrGraph& g, const FeatureMat
   }
   return binary_reduce(strategy, g, cfg, cfg.lhs == Operand::U ? &src_feats : nullptr, nullptr,
                        cfg.lhs == Operand::E ? &src_feats : nullptr, plan, threads);
+}
+
+// ---- file containers (io.hpp:25-41) over the C-ABI readers / writers ------
+
+EdgeList load_edge_list(const std::string& path) {
+  uint32_t n = 0;
+  uint64_t m = 0;
+  uint32_t *src = nullptr, *dst = nullptr;
+  throw_status(gspmm_edge_list_read(path.c_str(), &n, &m, &src, &dst));
+  EdgeList el;
+  el.num_nodes = n;
+  el.edges.resize(m);
+  for (uint64_t i = 0; i < m; ++i) el.edges[i] = Edge{src[i], dst[i]};
+  gspmm_free(src);
+  gspmm_free(dst);
+  return el;
+}
+
+void save_edge_list(const std::string& path, const EdgeList& el) {
+  std::vector<uint32_t> src(el.edges.size()), dst(el.edges.size());
+  for (std::size_t i = 0; i < el.edges.size(); ++i) {
+    src[i] = el.edges[i].src;
+    dst[i] = el.edges[i].dst;
+  }
+  throw_status(gspmm_edge_list_write(path.c_str(), el.num_nodes, el.edges.size(), src.data(),
+                                     dst.data()));
+}
+
+void save_feature_matrix(const std::string& path, const FeatureMatrix& f) {
+  throw_status(gspmm_fmat1_write(path.c_str(), f.data.data(), f.rows, f.dim, 0));
+}
+
+FeatureMatrix load_feature_matrix(const std::string& path) {
+  int64_t rows = 0, dim = 0;
+  throw_status(gspmm_fmat1_info(path.c_str(), &rows, &dim));
+  FeatureMatrix f(rows, dim);
+  throw_status(gspmm_fmat1_read(path.c_str(), f.data.data(), 0));
+  return f;
+}
+
+void save_csr(const std::string& path, const CsrGraph& g) {
+  throw_status(gspmm_csr1_write(path.c_str(), static_cast<int>(g.orientation), g.num_rows,
+                                g.num_cols, g.indptr.data(), g.indices.data(),
+                                g.edge_ids.data()));
+}
+
+CsrGraph load_csr(const std::string& path) {
+  int orientation = 0;
+  uint64_t rows = 0, cols = 0, m = 0;
+  throw_status(gspmm_csr1_info(path.c_str(), &orientation, &rows, &cols, &m));
+  CsrGraph g;
+  g.orientation = orientation == GSPMM_DST_MAJOR ? Orientation::DstMajor : Orientation::SrcMajor;
+  g.num_rows = static_cast<NodeId>(rows);
+  g.num_cols = static_cast<NodeId>(cols);
+  g.indptr.resize(rows + 1);
+  g.indices.resize(m);
+  g.edge_ids.resize(m);
+  throw_status(gspmm_csr1_read(path.c_str(), g.indptr.data(), g.indices.data(), g.edge_ids.data()));
+  return g;
 }
 
 }  // namespace gspmm_b200

@@ -35,7 +35,7 @@ def main():
         tot_t += t
         short = name.split("(")[0][-60:]
         print(f"{i:4d} {short:60s} {t:9.1f} us  dram r {rd:6.3f} w {wr:6.3f} GB "
-              f"({(rd + wr) / max(t, 1e-9) * 1e3:6.0f} GB/s)  L2 {l2:6.2f} GB hit {hit:5.1f}%")
+              f"({(rd + wr) / max(t, 1e-9) * 1e3:6.2f} TB/s)  L2 {l2:6.2f} GB hit {hit:5.1f}%")
     print(f"total {tot_t:.1f} us")
 
 

@@ -15,6 +15,7 @@
 #include "gspmm/compare.hpp"
 #include "gspmm/error.hpp"
 #include "gspmm/generate.hpp"
+#include "gspmm/io.hpp"
 #include "gspmm/kernels.hpp"
 #include "gspmm/oracle.hpp"
 #include "gspmm/rng.hpp"
@@ -332,6 +333,58 @@ int main() {
     fe.data = {1, 10};
     const B::FeatureMatrix o = B::copy_reduce(B::Strategy::Pull, to_b(v3.dst_major), fe, B::ReduceOp::Sum);
     CHECK(o.at(2, 0) == 11);
+  }
+  // file containers (test_io.cpp:93-123): each library reads what the other
+  // wrote; corrupt files raise IoError in both
+  {
+    const std::string dir = "/tmp/gspmm_b200_shim_io_";
+    for (std::uint64_t seed : {1ull, 8ull}) {
+      const R::EdgeList el = random_small_graph(seed);
+      for (const auto orient : {R::Orientation::SrcMajor, R::Orientation::DstMajor}) {
+        const R::CsrGraph g = R::build_csr(el, orient);
+        R::save_csr(dir + "r.csr", g);
+        B::save_csr(dir + "b.csr", to_b(g));
+        const B::CsrGraph from_r = B::load_csr(dir + "r.csr");
+        const R::CsrGraph from_b = R::load_csr(dir + "b.csr");
+        CHECK(from_r.orientation == static_cast<B::Orientation>(g.orientation));
+        CHECK(from_r.num_rows == g.num_rows && from_r.num_cols == g.num_cols);
+        CHECK(from_r.indptr == g.indptr && from_r.indices == g.indices && from_r.edge_ids == g.edge_ids);
+        CHECK(from_b.orientation == g.orientation && from_b.indptr == g.indptr &&
+              from_b.indices == g.indices && from_b.edge_ids == g.edge_ids);
+      }
+      B::EdgeList bel;
+      bel.num_nodes = el.num_nodes;
+      for (const R::Edge& e : el.edges) bel.edges.push_back({e.src, e.dst});
+      B::save_edge_list(dir + "b.txt", bel);
+      const R::EdgeList back = R::load_edge_list(dir + "b.txt");
+      CHECK(back.num_nodes == el.num_nodes && back.edges == el.edges);
+      R::save_edge_list(dir + "r.txt", el);
+      CHECK(B::load_edge_list(dir + "r.txt").edges == bel.edges);
+    }
+    const R::FeatureMatrix a = R::random_features(37, 5, 123);
+    R::save_feature_matrix(dir + "r.fmat", a);
+    const B::FeatureMatrix fb = B::load_feature_matrix(dir + "r.fmat");
+    CHECK(fb.rows == a.rows && fb.dim == a.dim && fb.data == a.data);
+    B::save_feature_matrix(dir + "b.fmat", fb);
+    CHECK(R::load_feature_matrix(dir + "b.fmat").data == a.data);
+    {
+      std::FILE* f = std::fopen((dir + "bogus.bin").c_str(), "wb");
+      std::fputs("definitely not a matrix", f);
+      std::fclose(f);
+    }
+    CHECK_THROWS_AS(B::load_feature_matrix(dir + "bogus.bin"), B::IoError);
+    CHECK_THROWS_AS(B::load_csr(dir + "bogus.bin"), B::IoError);
+    CHECK_THROWS_AS(B::load_feature_matrix("/nonexistent/path"), B::IoError);
+    CHECK_THROWS_AS(R::load_csr(dir + "bogus.bin"), R::IoError);
+    {
+      std::FILE* f = std::fopen((dir + "bad.txt").c_str(), "wb");
+      std::fputs("0 1\n%nodes 2\n5 1\n", f);
+      std::fclose(f);
+    }
+    CHECK_THROWS_AS(B::load_edge_list(dir + "bad.txt"), B::ParseError);
+    CHECK_THROWS_AS(R::load_edge_list(dir + "bad.txt"), R::ParseError);
+    for (const char* n : {"r.csr", "b.csr", "b.txt", "r.txt", "r.fmat", "b.fmat", "bogus.bin", "bad.txt"})
+      std::remove((dir + n).c_str());
   }
   std::printf("shim_parity: %d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
