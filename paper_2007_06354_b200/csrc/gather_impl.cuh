@@ -402,18 +402,32 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
 // chain itself, ~0.67 ms; 100k-edge rows become 32-column units), and hands
 // the units out heaviest first (LPT).
 //
-// The CTA is warp-specialised: 12 producer warps gather each stage of R
+// The CTA is warp-specialised.  12 producer warps gather each stage of R
 // edges x cw columns with 128-bit LDGs into registers -- the (edge, column
 // quad) items of a stage are spread over all 384 producer lanes, so a
 // narrow slice still keeps every lane busy -- one stage ahead of the stage
-// they store into the shared-memory ring (NB stages, empty/full
-// mbarriers); 4 consumer warps (one or four columns per thread) fold each
-// landed stage.  Neighbour ids ride four stages ahead as cp.async copies into
-// a small id ring.
+// they store into the shared-memory ring (NB stages, empty / full
+// mbarriers).  Neighbour ids ride four stages ahead as cp.async copies into
+// a small id ring.  4 consumer warps fold each landed stage: units of <= 32
+// columns (the chain-bound ones) use a compile-time stage stride -- per edge
+// one LDS at an immediate offset and the chain add, nothing else
+// (scripts/mb_chain.cu: 5.1 cycles per edge for that pair, 4.1 for the bare
+// chain); wider units one or four columns per thread.  Whole blocks of edges
+// run straight-line with the next block's loads in flight.
+// Measured alternatives (r02n - r02s, unit traces by scripts/trace_long.py):
+//   * a lane-per-quad / warp-per-edges producer (an id read, one address and
+//     the load per item instead of ~60 instructions): wide units 29 -> 23
+//     GB/s per CTA -- 25 of 32 lanes carry a 100-column row, and the stream
+//     rate follows the number of warp gathers, not the instruction count;
+//   * two stages of gathers in flight per lane (three register sets): the
+//     same rate with either producer;
+//   * column-major stages for narrow units (four edges of a column per
+//     LDS.128, the fastest consumer in mb_chain): the transposing scalar
+//     stores slow the producers of every unit, config-3 mean 5.2 -> 6.1 ms;
+//   * pacing the producers of chain-bound units with nanosleep: no change.
 // Measured (round 1, scripts/mb_gather.cu): random 400 B rows stream at
 // 34 GB/s per SM through LDG.128 into registers against 9.5 GB/s through
-// LDGSTS (the previous long-row CTA) and ~100 rows/us through TMA gather4
-// (row-rate bound: no help for the 329k-edge chains).
+// LDGSTS and ~100 rows/us through TMA gather4.
 #ifndef LG_NB
 #define LG_NB 3
 #endif
@@ -426,8 +440,10 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
 #ifndef LG_ID
 #define LG_ID 4
 #endif
-#ifndef LG_PIPE
-#define LG_PIPE 1
+// LG_TRACE 1 (development builds only): every long-row unit prints its row,
+// slice, globaltimer span and wait times (scripts/trace_long.py)
+#ifndef LG_TRACE
+#define LG_TRACE 0
 #endif
 constexpr int kLgProducers = 12, kLgConsumers = 4;
 constexpr int kLgThreads = 32 * (kLgProducers + kLgConsumers);
@@ -455,6 +471,10 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
   constexpr bool SMALL = SK != SK_NONE;
   extern __shared__ __align__(16) float sm[];
   __shared__ uint32_t s_unit;
+#if LG_TRACE
+  __shared__ long long s_wait[3];  // cycles waiting: consumer on full, producer on empty, on the ids
+  long long w_acc = 0, w_acc2 = 0;
+#endif
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool producer = warp < kLgProducers;
   const RowLaunch& L = p.row;
@@ -486,16 +506,26 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
     const uint32_t r = ud.x;
     const int c0 = static_cast<int>(ud.y & 0xffffu);
     const int cw = static_cast<int>(ud.y >> 16);
-    const int slot_f = (cw + 3) & ~3;
-    const int qpe = slot_f >> 2;
+    const int qpe = (cw + 3) >> 2;  // column quads per edge
+    // stage stride of an edge, floats: narrow units pad to a compile-time
+    // stride of the consumer (8 / 16 / 32), wider ones to the quad
+    const int sst = cw <= 8 ? 8 : cw <= 16 ? 16 : cw <= 32 ? 32 : 4 * qpe;
+    // (Column-major stages for narrow units -- four edges of a column per
+    // LDS.128, the fastest consumer in scripts/mb_chain.cu -- were measured
+    // twice (r02n, r02q): the transposing scalar stores slow the producers
+    // of every unit, 5.2 -> 6.1 ms on the config-3 mean.)
     const int h0 = (SMALL && rw > 1) ? c0 / L.rhs.group : 0;
     const int nh = (SMALL && rw > 1) ? (c0 + cw - 1) / L.rhs.group - h0 + 1 : 1;
-    uint32_t R = static_cast<uint32_t>(G::DF / slot_f);
+    uint32_t R = static_cast<uint32_t>(G::DF / sst);
     if (R > static_cast<uint32_t>(G::MR)) R = G::MR;
     if (SMALL && R * nh > static_cast<uint32_t>(G::SF)) R = G::SF / nh;
     const uint32_t e0 = __ldg(L.indptr + r), e1 = __ldg(L.indptr + r + 1);
     const uint32_t n = e1 - e0;
     const uint32_t rounds = (n + R - 1) / R;
+#if LG_TRACE
+    unsigned long long t_begin = 0;
+    if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+#endif
 
     if (producer) {
       const int ptid = tid;  // 0 .. PL - 1
@@ -535,7 +565,7 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
                                      ? o
                                      : static_cast<uint32_t>(operand_row(lrole, 0, o, e, e0 + m * R + q));
             x[k] = __ldg(reinterpret_cast<const float4*>(lbase + static_cast<int64_t>(row) * lld + 4 * t));
-            off[k] = static_cast<int>(q) * slot_f + 4 * t;
+            off[k] = static_cast<int>(q) * sst + 4 * t;
           }
           q += dq;
           t += dt;
@@ -603,9 +633,36 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
       cp_async_wait_group<0>();
     } else {
       const int ctid = tid - PL;  // 0 .. 127
-      auto run = [&](auto fw_tag) {
+      // The fold of a column is one dependent fp32 chain over the row's
+      // edges (~4 cycles per edge: 0.67 ms for config 3's 329k-edge row), so
+      // a unit's consumer must issue nothing per edge but the chain and its
+      // operand load: whole blocks of KB edges run straight-line (no clamps
+      // or selects; the partial block of a stage's end folds edge by edge),
+      // the next block's shared-memory loads in flight behind the current
+      // block's chain.  The chain's 4 cycles leave room for little else: 3.75
+      // instructions per edge ran 7.2 cycles per edge and 8 ran 16.5 (r02r
+      // unit traces), so narrow units issue one LDS at an immediate offset
+      // and the add per edge, nothing more.  Max / Min with argmax over
+      // copied rows are not a chain at all: the extremum is exact and
+      // associative, so each block's extremum comes from a tree of FMNMX
+      // and one comparison per block decides whether the block takes over
+      // (`a < m ? m : a` and fmaxf agree except for the sign of a zero
+      // extremum); the flush re-reads the winning block from global memory
+      // and takes the first edge equal to the extremum -- the reference's
+      // first-wins rule -- with that element's bits.  A DUAL unit of <= 64
+      // columns splits its two folds over the two halves of the consumer
+      // threads (max + argmax on warps 0-1, the sum on warps 2-3).
+      constexpr bool FASTMM = ARG && BOP == B_COPY && SK == SK_NONE &&
+                              (ROP == R_MAX || ROP == R_MIN);
+      // FW columns per thread; ST = compile-time stage stride (0: runtime sst)
+      auto run = [&](auto fw_tag, auto st_tag) {
         constexpr int FW = decltype(fw_tag)::value;
-        const int cc = ctid * FW;
+        constexpr int ST = decltype(st_tag)::value;
+        constexpr int KB = FW == 4 ? 4 : 16;  // edges per straight-line block
+        const int stf = ST ? ST : sst;
+        const bool split = DUAL && FW * 64 >= cw;      // both folds fit 64 threads each
+        const bool second = split && ctid >= 64;       // the sum half of a split unit
+        const int cc = (split ? (ctid & 63) : ctid) * FW;
         const bool own = cc < cw;
         const int hrel = (SMALL && rw > 1) ? (c0 + cc) / L.rhs.group - h0 : 0;
         float acc[FW];
@@ -619,75 +676,135 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
           if (L.acc_in && own && cc + t < cw)  // source-blocked pass: the partial
             acc[t] = L.acc_in[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t];
         }
-        for (uint32_t s = 0; s < rounds; ++s) {
-          const uint32_t gsi = gs0 + s;
-          const int b = static_cast<int>(gsi % NB);
-          mbar_wait(&full[b], (gsi / NB) & 1u);
-          if (own) {
-            const uint32_t cnt = min(R, n - s * R);
-            const float* col = sdata + static_cast<size_t>(b) * G::DF + cc;
-            const float* sv = ssmall + static_cast<size_t>(b) * G::SF + hrel;
-            // blocks of KB edges with the next block's shared-memory loads in
-            // flight while this block folds (two register sets alternate):
-            // the fold is then the add / compare chain itself, not chain +
-            // load latency per block (r02e: ~7.8 cycles per edge, 4 ideal)
-            constexpr int KB = FW == 4 ? 4 : 8;
-            float xa[KB][FW], xb[KB][FW], sa[KB], sb[KB];
-            auto ld = [&](uint32_t e, float (&x)[KB][FW], float (&sv8)[KB]) {
+        auto message = [&](float x, float sv) {
+          if constexpr (SK == SK_SCALE) return __fmul_rn(bin_apply<BOP>(x, 0.0f), sv);
+          else if constexpr (SK == SK_NONE) return bin_apply<BOP>(x, 0.0f);
+          else return bin_apply<BOP>(x, sv);
+        };
+        // one stage: PRIM = the config's own reduction, SEC = the DUAL sum
+        auto fold_stage = [&](auto prim_tag, auto sec_tag, const float* sd, const float* sv,
+                              uint32_t cnt, uint32_t ebase) {
+          constexpr bool PRIM = decltype(prim_tag)::value, SEC = decltype(sec_tag)::value;
+          const float* col = sd + cc;
+          float xa[KB][FW], xb[KB][FW], sa[KB], sb[KB];
+          auto ld = [&](uint32_t blk, float (&x)[KB][FW], float (&s8)[KB]) {
+            const float* pb = col + static_cast<size_t>(blk) * (KB * stf);
 #pragma unroll
-              for (int k = 0; k < KB; ++k) {
-                const uint32_t ek = min(e + k, cnt - 1);  // clamped: inside the stage
-                if constexpr (FW == 4) {
-                  const float4 v = *reinterpret_cast<const float4*>(col + static_cast<size_t>(ek) * slot_f);
-                  x[k][0] = v.x; x[k][1] = v.y; x[k][2] = v.z; x[k][3] = v.w;
-                } else {
-                  x[k][0] = col[static_cast<size_t>(ek) * slot_f];
-                }
-                if constexpr (SMALL) sv8[k] = sv[ek * nh];
+            for (int k = 0; k < KB; ++k) {
+              if constexpr (FW == 4) {
+                const float4 v = *reinterpret_cast<const float4*>(pb + k * stf);
+                x[k][0] = v.x; x[k][1] = v.y; x[k][2] = v.z; x[k][3] = v.w;
+              } else {
+                x[k][0] = pb[k * stf];
               }
-            };
-            auto fold = [&](uint32_t e, const float (&x)[KB][FW], const float (&sv8)[KB]) {
+            }
+            if constexpr (SMALL) {
+              const float* ps = sv + static_cast<size_t>(blk) * KB * nh;
 #pragma unroll
-              for (int k = 0; k < KB; ++k) {
-                // edges past the stage fold the reduce identity: exact (a
-                // sum from +0 is never -0, so + 0 changes nothing; -inf
-                // never wins a max), and the block stays straight-line code
-                const bool ok = e + k < cnt;
+              for (int k = 0; k < KB; ++k) s8[k] = ps[k * nh];
+            }
+          };
+          auto fold_one = [&](float x, float s1, int t, uint32_t pos) {
+            const float m = message(x, s1);
+            if constexpr (SEC) acc2[t] = __fadd_rn(acc2[t], m);
+            if constexpr (PRIM) {
+              if constexpr (ARG) {
+                if (red_wins<ROP>(acc[t], m)) {
+                  acc[t] = m;
+                  arg[t] = pos;
+                }
+              } else {
+                acc[t] = red_combine<ROP>(acc[t], m);
+              }
+            }
+          };
+          auto fold = [&](uint32_t blk, const float (&x)[KB][FW], const float (&s8)[KB]) {
+            int ak[FW];
 #pragma unroll
-                for (int t = 0; t < FW; ++t) {
-                  float m;
-                  if constexpr (SK == SK_SCALE) m = __fmul_rn(bin_apply<BOP>(x[k][t], 0.0f), sv8[k]);
-                  else if constexpr (SK == SK_NONE) m = bin_apply<BOP>(x[k][t], 0.0f);
-                  else m = bin_apply<BOP>(x[k][t], sv8[k]);
-                  if constexpr (DUAL) acc2[t] = __fadd_rn(acc2[t], ok ? m : 0.0f);
-                  m = ok ? m : red_identity<ROP>();
-                  if constexpr (ARG) {
+            for (int t = 0; t < FW; ++t) ak[t] = -1;
+            if constexpr (PRIM && FASTMM) {
+              // the block's extremum by a tree (exact and order-free up to
+              // the sign of zero), one comparison per block on the chain
+#pragma unroll
+              for (int t = 0; t < FW; ++t) {
+                float v[KB];
+#pragma unroll
+                for (int k = 0; k < KB; ++k) v[k] = x[k][t];
+#pragma unroll
+                for (int h = KB / 2; h > 0; h >>= 1)
+#pragma unroll
+                  for (int k = 0; k < h; ++k)
+                    v[k] = ROP == R_MAX ? fmaxf(v[k], v[k + h]) : fminf(v[k], v[k + h]);
+                const bool w = red_wins<ROP>(acc[t], v[0]);
+                acc[t] = ROP == R_MAX ? fmaxf(acc[t], v[0]) : fminf(acc[t], v[0]);
+                ak[t] = w ? 0 : -1;  // the block's first edge: resolved at the flush
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < KB; ++k) {
+#pragma unroll
+              for (int t = 0; t < FW; ++t) {
+                const float m = message(x[k][t], s8[k]);
+                if constexpr (SEC) acc2[t] = __fadd_rn(acc2[t], m);
+                if constexpr (PRIM) {
+                  if constexpr (FASTMM) {
+                    // folded above
+                  } else if constexpr (ARG) {
                     if (red_wins<ROP>(acc[t], m)) {
                       acc[t] = m;
-                      arg[t] = e0 + s * R + e + k;
+                      ak[t] = k;
                     }
                   } else {
                     acc[t] = red_combine<ROP>(acc[t], m);
                   }
                 }
               }
-            };
-#if LG_PIPE
+            }
+            if constexpr (ARG && PRIM) {
+#pragma unroll
+              for (int t = 0; t < FW; ++t)
+                if (ak[t] >= 0) arg[t] = ebase + blk * KB + static_cast<uint32_t>(ak[t]);
+            }
+          };
+          const uint32_t nfull = cnt / KB;
+          if (nfull) {
             ld(0, xa, sa);
-            for (uint32_t e = 0; e < cnt; e += 2 * KB) {
-              ld(e + KB, xb, sb);
-              fold(e, xa, sa);
-              ld(e + 2 * KB, xa, sa);
-              fold(e + KB, xb, sb);
+            uint32_t bk = 0;
+            for (; bk + 2 <= nfull; bk += 2) {
+              ld(bk + 1, xb, sb);
+              fold(bk, xa, sa);
+              ld(min(bk + 2, nfull - 1), xa, sa);
+              fold(bk + 1, xb, sb);
             }
-#else
-            for (uint32_t e = 0; e < cnt; e += KB) {
-              ld(e, xa, sa);
-              fold(e, xa, sa);
-            }
-            (void)xb;
-            (void)sb;
+            if (bk < nfull) fold(bk, xa, sa);  // xa holds block nfull - 1
+          }
+          for (uint32_t e = nfull * KB; e < cnt; ++e) {
+            const float s1 = SMALL ? sv[static_cast<size_t>(e) * nh] : 0.0f;
+#pragma unroll
+            for (int t = 0; t < FW; ++t) fold_one(col[static_cast<size_t>(e) * stf + t], s1, t, ebase + e);
+          }
+        };
+        using T = std::true_type;
+        using F = std::false_type;
+        for (uint32_t s = 0; s < rounds; ++s) {
+          const uint32_t gsi = gs0 + s;
+          const int b = static_cast<int>(gsi % NB);
+#if LG_TRACE
+          const long long tw0 = clock64();
 #endif
+          mbar_wait(&full[b], (gsi / NB) & 1u);
+#if LG_TRACE
+          w_acc += clock64() - tw0;
+#endif
+          if (own) {
+            const uint32_t cnt = min(R, n - s * R);
+            const float* sd = sdata + static_cast<size_t>(b) * G::DF;
+            const float* sv = ssmall + static_cast<size_t>(b) * G::SF + hrel;
+            const uint32_t ebase = e0 + s * R;
+            if constexpr (!DUAL) fold_stage(T{}, F{}, sd, sv, cnt, ebase);
+            else if (!split) fold_stage(T{}, T{}, sd, sv, cnt, ebase);
+            else if (!second) fold_stage(T{}, F{}, sd, sv, cnt, ebase);
+            else fold_stage(F{}, T{}, sd, sv, cnt, ebase);
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[b]);
@@ -698,31 +815,79 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
 #pragma unroll
           for (int t = 0; t < FW; ++t) {
             if (cc + t >= cw) break;
-            float a = acc[t];
-            if constexpr (ROP == R_MAX || ROP == R_MIN) {
-              if (fix && deg == 0) a = 0.0f;
+            if (!second) {
+              float a = acc[t];
+              if constexpr (FASTMM) {
+                // arg is the first edge of the winning block (or the winning
+                // edge itself): the winner is the first edge from there that
+                // compares equal to the extremum; its bits are the result
+                // (the sign of a zero extremum included)
+                if (arg[t] != 0xffffffffu) {
+                  const uint32_t lim = min(arg[t] + static_cast<uint32_t>(KB), e1);
+                  for (uint32_t pos = arg[t]; pos < lim; ++pos) {
+                    const uint32_t o = __ldg(L.indices + pos);
+                    const uint32_t e = L.lhs.role == ROLE_EID ? __ldg(L.eids + pos) : 0u;
+                    const float v =
+                        __ldg(L.lhs.base + operand_row(L.lhs.role, r, o, e, pos) * L.lhs.ld + c0 + cc + t);
+                    if (v == a) {
+                      a = v;
+                      arg[t] = pos;
+                      break;
+                    }
+                  }
+                }
+              }
+              if constexpr (ROP == R_MAX || ROP == R_MIN) {
+                if (fix && deg == 0) a = 0.0f;
+              }
+              if (fix && L.mean) a = deg ? __fdiv_rn(a, __uint2float_rn(deg)) : 0.0f;
+              L.out[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t] = a;
+              if constexpr (ARG) {
+                const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + cc + t;
+                const bool none = arg[t] == 0xffffffffu;
+                if (L.arg_other)
+                  L.arg_other[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.indices + arg[t]));
+                if (L.arg_edge)
+                  L.arg_edge[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.eids + arg[t]));
+              }
             }
-            if (fix && L.mean) a = deg ? __fdiv_rn(a, __uint2float_rn(deg)) : 0.0f;
-            L.out[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t] = a;
-            if constexpr (DUAL)
-              L.out2[static_cast<int64_t>(r) * L.out2_ld + c0 + cc + t] =
-                  L.mean2 ? (deg ? __fdiv_rn(acc2[t], __uint2float_rn(deg)) : 0.0f) : acc2[t];
-            if constexpr (ARG) {
-              const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + cc + t;
-              const bool none = arg[t] == 0xffffffffu;
-              if (L.arg_other)
-                L.arg_other[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.indices + arg[t]));
-              if (L.arg_edge)
-                L.arg_edge[ab] = none ? -1 : static_cast<int32_t>(__ldg(L.eids + arg[t]));
+            if constexpr (DUAL) {
+              if (!split || second)
+                L.out2[static_cast<int64_t>(r) * L.out2_ld + c0 + cc + t] =
+                    L.mean2 ? (deg ? __fdiv_rn(acc2[t], __uint2float_rn(deg)) : 0.0f) : acc2[t];
             }
           }
         }
       };
-      if (cw > 128) run(std::integral_constant<int, 4>{});
-      else run(std::integral_constant<int, 1>{});
+      using I0 = std::integral_constant<int, 0>;
+      using I1 = std::integral_constant<int, 1>;
+      using I4 = std::integral_constant<int, 4>;
+      if (cw > 128) run(I4{}, I0{});
+      else if (cw > 32) run(I1{}, I0{});
+      else if (sst == 8) run(I1{}, std::integral_constant<int, 8>{});
+      else if (sst == 16) run(I1{}, std::integral_constant<int, 16>{});
+      else run(I1{}, std::integral_constant<int, 32>{});
     }
     gs0 += rounds;
+#if LG_TRACE
+    if (tid == PL) s_wait[0] = w_acc;
+    if (tid == 0) {
+      s_wait[1] = w_acc;
+      s_wait[2] = w_acc2;
+    }
+    w_acc = 0;
+    w_acc2 = 0;
+#endif
     __syncthreads();  // next unit: the id ring's first slots are rewritten
+#if LG_TRACE
+    if (tid == 0) {
+      unsigned long long t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      printf("LGW %u full %lld empty %lld idbar %lld ld 0 st 0 ar 0\n", unit, s_wait[0], s_wait[1], s_wait[2]);
+      printf("LGU %u row %u c0 %d cw %d n %u t0 %llu t1 %llu cta %u\n", unit, r, c0, cw, n, t_begin,
+             t_end, blockIdx.x);
+    }
+#endif
   }
 }
 
