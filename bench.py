@@ -31,6 +31,7 @@ scatters into its own source rows (owner computes).
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
@@ -864,32 +865,76 @@ class C3Reference:
         self.deg = np.diff(dcsr[0].astype(np.int64)).astype(np.float32)[:, None]
         self.sum = np.empty((C3_N, C3_F), np.float32)
         self.gy = gy
+        # strategy per reference pass: RowParallelSpmm until pick_strategies()
+        self.strategy = {k: O.SPMM for k in C3_PASSES[:3]}
+        self.strategy_table, self.csv = None, None
         # the max backward's input (untimed): the restated a17.2 argmax
         _, self.au, _ = O.copy_max_argmax_csr(dcsr, C3_N, C3_N, x, threads=threads)
 
-    def _call(self, cfg, u=None, v=None, e=None, out=None, src_major=False):
+    def _call(self, cfg, u=None, v=None, e=None, out=None, src_major=False, strategy=None):
         O, R = self.O, self.R
+        strategy = O.SPMM if strategy is None else strategy
         if self.views is not None:
-            t = R.ref_run(self.views, O.SPMM, *cfg, u, v, e, self.threads,
+            t = R.ref_run(self.views, strategy, *cfg, u, v, e, self.threads,
                           None if out is None else out.ctypes.data)
         else:
             g = self.gs if src_major else self.gd
-            t = R.ref_run_graph(g.h, O.SPMM, *cfg, u, v, e, self.threads,
+            t = R.ref_run_graph(g.h, strategy, *cfg, u, v, e, self.threads,
                                 None if out is None else out.ctypes.data, 0)
         if t < 0:
             raise RuntimeError("reference binary_reduce failed")
         return t
 
+    def _pass_args(self):
+        O = self.O
+        return {C3_PASSES[0]: ((O.U, O.NONE, O.COPY, O.MAX, O.V), dict(u=self.fx)),
+                C3_PASSES[1]: ((O.U, O.NONE, O.COPY, O.SUM, O.V), dict(u=self.fx)),
+                C3_PASSES[2]: ((O.V, O.E, O.MUL, O.SUM, O.U),
+                               dict(v=self.fg, e=self.fe, src_major=True))}
+
+    def pick_strategies(self, iters=1):
+        """BASELINE.md 2 / SURVEY 8d: the reference CPU number is the BEST of
+        RowParallelSpmm, BlockedPull (the reference's default kb / nb, plan
+        built outside the clock) and Pull, per pass.  With reference views
+        the cells run through the reference's own bench_case (bench.cpp:55-
+        126) and its CSV rows (bench.cpp:128-145) are kept."""
+        O, R = self.O, self.R
+        names = {O.SPMM: "RowParallelSpmm", O.BLOCKED: "BlockedPull", O.PULL: "Pull"}
+        table, rows = {}, []
+        for name, (cfg, kw) in self._pass_args().items():
+            table[name] = {}
+            for st, sname in names.items():
+                if self.views is not None:
+                    buf = C.create_string_buffer(512)
+                    t = R.ref_bench_csv(self.views, st, *cfg, kw.get("u"), kw.get("v"),
+                                        kw.get("e"), self.threads, 1, iters, buf, 512)
+                    rows.append(buf.value.decode())
+                else:
+                    self._call(cfg, strategy=st, **kw)  # warm
+                    t = min(self._call(cfg, strategy=st, **kw) for _ in range(iters))
+                if t < 0:
+                    raise RuntimeError(f"reference {sname} failed on {name}")
+                table[name][sname] = t
+            best = min(table[name], key=table[name].get)
+            self.strategy[name] = {v: k for k, v in names.items()}[best]
+        self.strategy_table = table
+        if rows:
+            self.csv = [R.ref_bench_csv_header().decode()] + rows
+        return table
+
     def step(self):
         O = self.O
         ts = {}
-        ts[C3_PASSES[0]] = self._call((O.U, O.NONE, O.COPY, O.MAX, O.V), u=self.fx)
-        t = self._call((O.U, O.NONE, O.COPY, O.SUM, O.V), u=self.fx, out=self.sum)
+        args = self._pass_args()
+        cfg, kw = args[C3_PASSES[0]]
+        ts[C3_PASSES[0]] = self._call(cfg, strategy=self.strategy[C3_PASSES[0]], **kw)
+        cfg, kw = args[C3_PASSES[1]]
+        t = self._call(cfg, out=self.sum, strategy=self.strategy[C3_PASSES[1]], **kw)
         t0 = time.perf_counter()
         np.divide(self.sum, self.deg, out=self.sum, where=self.deg > 0)
         ts[C3_PASSES[1]] = t + time.perf_counter() - t0
-        ts[C3_PASSES[2]] = self._call((O.V, O.E, O.MUL, O.SUM, O.U), v=self.fg, e=self.fe,
-                                      src_major=True)
+        cfg, kw = args[C3_PASSES[2]]
+        ts[C3_PASSES[2]] = self._call(cfg, strategy=self.strategy[C3_PASSES[2]], **kw)
         t0 = time.perf_counter()
         O.argmax_backward_mt(self.au, self.gy, C3_N, threads=self.threads)
         ts[C3_PASSES[3]] = time.perf_counter() - t0
@@ -1043,34 +1088,54 @@ def run_cfg3(args, rank, world, dist):
         xn, gyn = x_h.numpy(), gy_h.numpy()
         gy_rows_h = np.ascontiguousarray(gyn[d_lo:d_hi]) if world > 1 else gyn
         pin = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True).numpy()  # noqa: E731
-        mx_h, mean_h = pin((rd, F), torch.float32), pin((rd, F), torch.float32)
-        au_h = pin((rd, F), torch.int32)
-        gxm_h, gmax_h = pin((rs, F), torch.float32), pin((C3_N, F), torch.float32)
         inv_h = torch.from_numpy(inv).pin_memory().numpy()
-        s_a, s_b = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        ev_a, ev_b = torch.cuda.Event(), torch.cuda.Event()
-        ev_a.record(s_a)
-        ev_b.record(s_b)
+        # Consecutive steps alternate between two sets of (three streams,
+        # host output buffers), every call through the C-ABI host entries:
+        #   A: max + argmax with the mean as second output (x up; max,
+        #      argmax, mean down);
+        #   B: mean backward (grad + 1/deg up, grad_x down);
+        #   C: max backward (argmax + grad up, grad_x down), which waits for
+        #      A's argmax to be back on the host.
+        # A stream runs its upload, kernel and download in order.  With a
+        # step's calls on two streams (r02k) A's 2.9 GB download serialised
+        # with C's 2 GB upload and with the next step's uploads: 136 ms per
+        # step.  With the calls on their own streams and the next step on the
+        # other set, step i + 1 uploads while step i downloads and the step
+        # is bound by the 4.9 GB of PCIe D2H.  (At N > 1 each rank runs its
+        # shard; the max backward there scatters its own rows into all source
+        # rows -- a per-rank partial, like the reference's per-thread work;
+        # the device path above is the exact one.)
+        sets = []
+        for _ in range(2):
+            st = {"a": torch.cuda.Stream(dev), "b": torch.cuda.Stream(dev),
+                  "c": torch.cuda.Stream(dev), "fwd": torch.cuda.Event(),
+                  "cup": torch.cuda.Event(),
+                  "mx": pin((rd, F), torch.float32), "mean": pin((rd, F), torch.float32),
+                  "au": pin((rd, F), torch.int32), "gxm": pin((rs, F), torch.float32),
+                  "gmax": pin((C3_N, F), torch.float32)}
+            st["cup"].record(st["c"])
+            sets.append(st)
+        mx_h, mean_h, au_h, gxm_h, gmax_h = (sets[0][k] for k in ("mx", "mean", "au", "gxm", "gmax"))
+        e2e_i = [0]
 
-        # stream A: max + argmax (x up; max, argmax down), then the max
-        # backward (argmax, grad up; grad_x down); stream B: mean (x up),
-        # mean backward (grad + 1/deg up).  Uploads alternate between the
-        # streams so both PCIe directions stay busy.  (At N > 1 each rank
-        # runs its shard; the max backward there scatters its own rows into
-        # all source rows -- a per-rank partial, like the reference's
-        # per-thread work; the device path above is the exact one.)
         def e2e_steps(k):
             for _ in range(k):
-                P.binary_reduce_host_async(gd, cfg_max, u=xn, out=mx_h, arg_other=au_h,
-                                           out2=mean_h, reduce2=P.MEAN, stream=s_a,
-                                           wait_event=ev_b, upload_event=ev_a)
-                P.binary_reduce_host_async(gs, cfg_bwd, v=gyn, out=gxm_h, other_scale=inv_h,
-                                           stream=s_b, wait_event=ev_a, upload_event=ev_b)
-                P.argmax_backward_host_async(au_h, gy_rows_h, gmax_h.shape[0], out=gmax_h,
-                                             device=dev, stream=s_a, wait_event=ev_b,
-                                             upload_event=ev_a)
-            s_a.synchronize()
-            s_b.synchronize()
+                st = sets[e2e_i[0] & 1]
+                e2e_i[0] += 1
+                # this set's previous max backward has uploaded the argmax buffer
+                st["a"].wait_event(st["cup"])
+                P.binary_reduce_host_async(gd, cfg_max, u=xn, out=st["mx"], arg_other=st["au"],
+                                           out2=st["mean"], reduce2=P.MEAN, stream=st["a"])
+                st["fwd"].record(st["a"])
+                P.binary_reduce_host_async(gs, cfg_bwd, v=gyn, out=st["gxm"], other_scale=inv_h,
+                                           stream=st["b"])
+                st["c"].wait_event(st["fwd"])
+                P.argmax_backward_host_async(st["au"], gy_rows_h, st["gmax"].shape[0],
+                                             out=st["gmax"], device=dev, stream=st["c"],
+                                             upload_event=st["cup"])
+            for st in sets:
+                for k in "abc":
+                    st[k].synchronize()
         e2e_steps(1)
         torch.cuda.synchronize(dev)
         if dist:
@@ -1090,7 +1155,8 @@ def run_cfg3(args, rank, world, dist):
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
                "path": "C-ABI host entries (gspmm_binary_reduce_host_async: max + argmax with "
                        "the mean as second output, mean backward; "
-                       "gspmm_argmax_backward_host_async), pinned host buffers, two streams"}
+                       "gspmm_argmax_backward_host_async), pinned host buffers, one stream per "
+                       "call, consecutive steps on alternating stream / buffer sets"}
 
     # --- CPU baseline (rank 0, N=1): the reference library, bounded sample ----
     cpu = None
@@ -1101,6 +1167,7 @@ def run_cfg3(args, rank, world, dist):
         else:
             threads = os.cpu_count() or 1
             ref = C3Reference(dcsr, scsr, dst, inv, x_h.numpy(), gy_h.numpy(), threads)
+            ref.pick_strategies()
             ref.step()  # warm
             times, t_begin = [], time.time()
             while len(times) < 3 and time.time() - t_begin < 30:
@@ -1111,10 +1178,11 @@ def run_cfg3(args, rank, world, dist):
             cpu = {"value": 3 * E / mean_s, "unit": "edges/s", "cores": threads,
                    "kind": "reference",
                    "sample": f"{len(times)} full cfg3 steps after 1 warm-up: reference "
-                             f"binary_reduce (RowParallelSpmm, {threads} OpenMP threads, {model}) "
+                             f"binary_reduce ({threads} OpenMP threads, {model}; per pass the best "
+                             "of RowParallelSpmm / BlockedPull / Pull, see strategies_s) "
                              "for max (no argmax), sum + /deg, mean backward; the max backward "
                              "by the restated oracle's threaded scatter (the reference lacks it)",
-                   "s_per_step": mean_s,
+                   "s_per_step": mean_s, "strategies_s": ref.strategy_table,
                    "passes_s": {k: sum(ts[k] for _, ts in times) / len(times) for k in C3_PASSES}}
 
     # --- roofline of the dominant pass ---------------------------------------
@@ -1179,9 +1247,12 @@ def run_reference_cfg3(args, rank, world):
     P.synth_normal(C3_N, C3_F, SEEDS["grad"], out=gy)  # N(0,1) input (reference has none)
     log(f"[bench-ref] cfg3 inputs + views in {time.time() - t0:.1f}s")
     ref = C3Reference(dcsr, None, dst, inv, x, gy, threads, views=views)
+    ref.pick_strategies(iters=2)
+    log("[bench-ref] strategies (s per pass): " + json.dumps(ref.strategy_table))
     for _ in range(args.warmup):
         ref.step()
     runs = [ref.step() for _ in range(args.steps)]
+    strategy_table, csv_rows = ref.strategy_table, ref.csv
     ref.close()
     O.REF.ref_views_free(views)
     mean_s = sum(t for t, _ in runs) / len(runs)
@@ -1196,9 +1267,12 @@ def run_reference_cfg3(args, rank, world):
         "passes_ms": {k: 1e3 * sum(ts[k] for _, ts in runs) / len(runs) for k in C3_PASSES},
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
                          "sample": f"full cfg3 step x{args.steps} after {args.warmup} warm-up: "
-                                   f"reference binary_reduce (RowParallelSpmm, {threads} "
-                                   f"threads, {model}) for max (no argmax), sum + /deg and the "
-                                   "mean backward; max backward by the restated oracle"},
+                                   f"reference binary_reduce ({threads} threads, {model}; per "
+                                   "pass the best of RowParallelSpmm / BlockedPull / Pull) for "
+                                   "max (no argmax), sum + /deg and the mean backward; max "
+                                   "backward by the restated oracle",
+                         "strategies_s": strategy_table},
+        "reference_csv": csv_rows,
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

@@ -132,6 +132,9 @@ def _load_ref():
         "ref_run_graph": (dbl, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, i32, vp, i64]),
         "ref_bench_case": (dbl, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, i32, i32, i32,
                                  C.POINTER(dbl), C.POINTER(dbl)]),
+        "ref_bench_csv": (dbl, [vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, i32, i32, i32,
+                                C.c_char_p, i32]),
+        "ref_bench_csv_header": (C.c_char_p, []),
         "ref_io_error": (C.c_char_p, []),
         "ref_save_csr": (i32, [C.c_char_p, vp]),
         "ref_load_csr": (i32, [C.c_char_p, C.POINTER(vp), C.POINTER(i32), C.POINTER(u32),

@@ -8,6 +8,7 @@
 // tests use it to pin the C restatement (oracle/gspmm_oracle.c), and
 // bench.py --impl reference times binary_reduce through it.
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -275,11 +276,21 @@ double ref_run(void* views, int strategy, int lhs, int rhs, int binop,
     const BrConfig cfg = make_cfg(lhs, rhs, binop, reduce, out_ent);
     const Strategy s = static_cast<Strategy>(strategy);
     const CsrGraph& g = gv->oriented(required_orientation(s, cfg.out));
+    // BlockedPull: the plan with the reference's default blocking, built
+    // before the clock starts (as bench_case does, bench.cpp:95-97)
+    BlockPlan plan;
+    if (s == Strategy::BlockedPull) {
+      const auto* fu = static_cast<FeatureMatrix*>(u);
+      const auto* fv = static_cast<FeatureMatrix*>(v);
+      const auto* fe = static_cast<FeatureMatrix*>(e);
+      const int64_t dim = fu ? fu->dim : fv ? fv->dim : fe ? fe->dim : 4;
+      plan = build_block_plan(g, default_kb(dim, g.num_cols), default_nb(g.num_rows, dim));
+    }
     const auto t0 = std::chrono::steady_clock::now();
     const FeatureMatrix res = binary_reduce(
         s, g, cfg, static_cast<FeatureMatrix*>(u),
         static_cast<FeatureMatrix*>(v), static_cast<FeatureMatrix*>(e),
-        nullptr, threads);
+        s == Strategy::BlockedPull ? &plan : nullptr, threads);
     const double dt =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0)
             .count();
@@ -313,6 +324,30 @@ double ref_bench_case(void* views, int strategy, int lhs, int rhs, int binop,
     return -static_cast<double>(status_of(std::current_exception()));
   }
 }
+
+// The same cell as the reference's own CSV row (bench_csv_row,
+// bench.cpp:133-145: config,strategy,nodes,edges,dim,threads,kb,nb,iters,
+// mean_s,min_s,gbps) written to buf; returns mean seconds.
+double ref_bench_csv(void* views, int strategy, int lhs, int rhs, int binop,
+                     int reduce, int out_ent, void* u, void* v, void* e,
+                     int threads, int warmup, int iters, char* buf, int cap) {
+  try {
+    const GraphViews* gv = static_cast<GraphViews*>(views);
+    const BrConfig cfg = make_cfg(lhs, rhs, binop, reduce, out_ent);
+    BenchOptions opts;
+    opts.warmup = warmup;
+    opts.iters = iters;
+    const BenchReport r = bench_case(
+        *gv, config_name(cfg), cfg, static_cast<FeatureMatrix*>(u),
+        static_cast<FeatureMatrix*>(v), static_cast<FeatureMatrix*>(e),
+        static_cast<Strategy>(strategy), threads, 0, 0, opts);
+    if (buf && cap > 0) std::snprintf(buf, cap, "%s", bench_csv_row(r).c_str());
+    return r.mean_s;
+  } catch (...) {
+    return -static_cast<double>(status_of(std::current_exception()));
+  }
+}
+const char* ref_bench_csv_header(void) { return bench_csv_header(); }
 
 // ---- canonical CSR handed in directly (BASELINE-size parity) -------------
 

@@ -61,7 +61,8 @@ const char* operand_name(int o) {
 // -- / -- / 15.6 / 15.5 / 15.5; 2048: cfg2 2.08).  The long-row thresholds
 // of the plan levels are kLevelThresholds.
 constexpr uint32_t kSegEdges = 256;
-constexpr uint32_t kLevelThresholds[5] = {1024, 4096, 16384, 32768, 65536};
+constexpr int kLevels = 6;
+constexpr uint32_t kLevelThresholds[kLevels] = {1024, 4096, 8192, 16384, 32768, 65536};
 // Source blocking: blocks of <= 48 MB of gathered rows (a share of the
 // 126 MB L2), see source_blocks_for.
 constexpr double kSrcBlockBytes = 48.0 * 1048576.0;
@@ -136,7 +137,7 @@ struct gspmm_graph_s {
     uint2* d_segs = nullptr;          // segments of consecutive non-long rows
     uint32_t num_segs = 0;
   };
-  Level level[5];
+  Level level[kLevels];
   int n_levels = 0;
   // long-row column units per (level, width), built on first use
   struct Units {
@@ -293,13 +294,14 @@ int bind(const gspmm_graph_s* g, const gspmm_config* cfg, const gspmm_mat* u,
   // bind_operand, kernels.cpp:361-377
   auto bind_one = [&](int o, const gspmm_mat*& m) -> int {
     m = pick(o);
-    if (!m || !m->data)
+    // a rows x 0 matrix has no data (FeatureMatrix(rows, 0), feature_matrix.hpp:36-38)
+    if (!m || (!m->data && !(m->rows > 0 && m->dim == 0)))
       return fail(GSPMM_ERR_SHAPE, std::string("missing feature matrix for operand ") + operand_name(o));
     if (m->rows != entity_rows(g, o))
       return fail(GSPMM_ERR_SHAPE, std::string("operand ") + operand_name(o) + " has " +
                                        std::to_string(m->rows) + " rows, entity has " +
                                        std::to_string(entity_rows(g, o)));
-    if (m->dim < 1 || (m->ld != 0 && m->ld < m->dim))
+    if (m->dim < 0 || (m->ld != 0 && m->ld < m->dim))
       return fail(GSPMM_ERR_SHAPE, std::string("operand ") + operand_name(o) + " has a bad dim/ld");
     return GSPMM_OK;
   };
@@ -322,6 +324,19 @@ int bind(const gspmm_graph_s* g, const gspmm_config* cfg, const gspmm_mat* u,
   if (is_dot && heads > 1 && gather % heads != 0)
     return fail(GSPMM_ERR_SHAPE, "dot heads must divide the operand width");
   int64_t w = is_dot ? heads : cfg->binary == GSPMM_COPY ? dl : gather;
+  // Zero-width operands: the reference returns a rows x 0 matrix
+  // (binary_out_dim, ops.cpp:63-67); nothing to launch.  A dot over zero
+  // columns or a 0-against-1 broadcast reads past an empty row there.
+  if (dl == 0 || dr == 0) {
+    if (is_dot || gather != 0)
+      return fail(GSPMM_ERR_SHAPE, "zero-width operands take no dot and no broadcast");
+    if (out && (out->rows != entity_rows(g, cfg->out) || out->dim != 0))
+      return fail(GSPMM_ERR_SHAPE, "output must be " + std::to_string(entity_rows(g, cfg->out)) + " x 0");
+    b->L = RowLaunch{};
+    b->out_rows = entity_rows(g, cfg->out);
+    b->width = 0;
+    return GSPMM_OK;
+  }
   if (cfg->reduce == GSPMM_MEAN && cfg->out == GSPMM_E)
     return fail(GSPMM_ERR_CONFIG, "mean reduces into nodes only");
   const bool want_arg = opt->arg_other || opt->arg_edge;
@@ -370,7 +385,7 @@ int bind(const gspmm_graph_s* g, const gspmm_config* cfg, const gspmm_mat* u,
   L.arg_edge = opt->arg_edge;
   L.arg_ld = opt->arg_ld ? opt->arg_ld : w;
   {
-    const auto& lv = g->level[g->n_levels > 2 ? 2 : g->n_levels - 1];  // rows.cu: 16384
+    const auto& lv = g->level[g->n_levels > 3 ? 3 : g->n_levels - 1];  // rows.cu: 16384
     L.long_rows = lv.d_long;
     L.num_long = lv.num_long;
     L.long_threshold = lv.num_long ? lv.threshold : 0xffffffffu;
@@ -688,21 +703,29 @@ int launch(gspmm_graph_s* g, CallCtx* ctx, Bound& b, cudaStream_t s) {
   } else if (planned(g, b.L, &rw)) {
     StreamLaunch p;
     p.row = b.L;
-    // plan level: rows gathering more than ~8 MB run as long-row units
-    // (measured: 4096 edges of 1 KB, 16384 of 400 B); a row no heavier than
-    // half the average per-warp share of the segment work finishes inside
-    // the segment kernel's span and stays there
+    // Plan level.  A row in the segment kernel is one warp's sequential
+    // work per slice, so a row much heavier than a warp's fair share of the
+    // pass ends after everything else; a row in the long-row kernel streams
+    // at a third of the segment kernel's rate per SM, so no more rows than
+    // necessary should go there.  Two bounds, both in edges: `share`, half
+    // the average per-warp share of the segment work, and `bytes`, ~8 MB of
+    // gathered bytes per row.  The level is the first threshold at or above
+    // `share`, but never above the last threshold within max(bytes, share).
+    // Measured (r02w-r02y, ms per pass at long-row thresholds 4096 / 8192 /
+    // 16384): cfg2 (share 1.8k) 1.73 / 2.50 / 2.50; cfg4 (share 6.8k) 8.23 /
+    // 7.07 / 8.16; cfg3 (share 17k; 16384 / 32768 / 65536) 5.01 / 5.04 / 5.13.
     const int slice_bytes = 4 * std::min(b.L.width, 256);
-    uint32_t target = std::max<uint32_t>(1024, (8u << 20) / static_cast<uint32_t>(slice_bytes));
-    {
-      const uint32_t slices = static_cast<uint32_t>((b.L.width + 255) / 256);
-      const double warps = static_cast<double>(g->num_sms) * (b.L.width > 128 ? 32 : 24);
-      const double half_share = 0.5 * static_cast<double>(g->m) * slices / warps;
-      if (half_share > target) target = static_cast<uint32_t>(std::min(half_share, 4.0e9));
-    }
-    int li = 0;
+    const uint32_t bytes_rule = std::max<uint32_t>(1024, (8u << 20) / static_cast<uint32_t>(slice_bytes));
+    const uint32_t slices = static_cast<uint32_t>((b.L.width + 255) / 256);
+    const double warps = static_cast<double>(g->num_sms) * (b.L.width > 128 ? 32 : 24);
+    const double share = std::min(0.5 * static_cast<double>(g->m) * slices / warps, 4.0e9);
+    const double cap = std::max<double>(bytes_rule, share);
+    int li = 0, li_share = g->n_levels - 1;
     for (int k = 0; k < g->n_levels; ++k)
-      if (g->level[k].threshold <= target) li = k;
+      if (g->level[k].threshold <= cap) li = k;
+    for (int k = g->n_levels - 1; k >= 0; --k)
+      if (g->level[k].threshold >= share) li_share = k;
+    li = std::min(li, li_share);
     const auto& lv = g->level[li];
     p.segs = lv.d_segs;
     p.n_segs = lv.num_segs;
@@ -784,7 +807,7 @@ void free_plan(gspmm_graph_s* g) {
 int build_plan(gspmm_graph_s* g, const uint32_t* indptr) {
   free_plan(g);
   const uint32_t seg_edges = g->seg_cost ? g->seg_cost : kSegEdges;
-  g->n_levels = g->forced_long ? 1 : 5;
+  g->n_levels = g->forced_long ? 1 : kLevels;
   for (int k = 0; k < g->n_levels; ++k) {
     auto& lv = g->level[k];
     lv.threshold = g->forced_long ? g->forced_long : kLevelThresholds[k];
@@ -1167,6 +1190,7 @@ int gspmm_binary_reduce_ex(gspmm_graph g, const gspmm_config* cfg,
   int st = bind(g, cfg, u, v, e, out, opt, &b);
   if (st) return st;
   if (!out) return fail(GSPMM_ERR_SHAPE, "missing output matrix");
+  if (b.width == 0) return GSPMM_OK;  // rows x 0: no element to compute
   return run_call(g, b, static_cast<cudaStream_t>(stream));
 }
 
@@ -1314,6 +1338,7 @@ static int host_call(gspmm_graph g, const gspmm_config* cfg, const gspmm_mat* u,
   Bound probe;
   int st = bind(g, cfg, u, v, e, out, opt, &probe);
   if (st) return st;
+  if (probe.width == 0) return GSPMM_OK;  // rows x 0: no element to compute
   CUDA_TRY(cudaSetDevice(g->device), "cudaSetDevice");
   retain_pool_memory();
   cudaStream_t s = static_cast<cudaStream_t>(stream);

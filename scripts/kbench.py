@@ -18,6 +18,9 @@ PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if 
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 
 
+PLAN = {}
+
+
 def graph(kind, n, m, seed=0, loops=False, sym=False):
     if kind == "powerlaw":
         return P.synth_powerlaw(n, 90, 21000, seed)
@@ -169,6 +172,8 @@ def run(name):
     else:
         fn = lambda: P.binary_reduce(g, "u_copy_add_v", u=x, out=out)
         eb = 0
+    if PLAN:
+        g.set_plan(**PLAN)
     ms = time_pass(fn)
     byts = E * F * 4 + (n + 1) * 4 + E * 4 + eb + n * F * 4
     if op == "maxbwd":  # read arg + grad_out, write grad (scatter): N x F each
@@ -177,7 +182,7 @@ def run(name):
         byts = E * F * 4 * 2 + eb + (n + 1) * 4
     gbs = byts / ms / 1e6
     res = dict(case=name, E=E, F=F, ms=round(ms, 4), gbs=round(gbs, 1), frac=round(gbs / PEAK, 3),
-               max_deg=int(deg.max()), long_rows=g.num_long_rows,
+               max_deg=int(deg.max()), long_rows=g.num_long_rows, plan=PLAN,
                setup_s=round(time.time() - t0, 1))
     print(json.dumps(res), flush=True)
     return res
@@ -186,6 +191,9 @@ def run(name):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", default="er128,er256,rmat256")
+    ap.add_argument("--plans", default="", help="plan options k=v ..., several plans separated by /")
     args = ap.parse_args()
-    for c in args.cases.split(","):
-        run(c)
+    for plan in args.plans.split("/"):
+        PLAN = {k: int(v) for k, v in (t.split("=") for t in plan.split() if t)}
+        for c in args.cases.split(","):
+            run(c)

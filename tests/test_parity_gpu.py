@@ -654,3 +654,57 @@ def test_second_reduction_fused_and_fallback(long_):
         assert O.bit_equal(o2.cpu().numpy(), np.where(deg > 0, want / np.maximum(deg, 1), 0)
                            .astype(np.float32))
         g.__dict__.pop("_dev", None)
+
+
+@pytest.mark.parametrize("cols", [0, 8, 28, 100])
+def test_long_row_argmax_ties_zeros_and_nans(cols):
+    # The long-row units take each 16-edge block's extremum from an FMNMX
+    # tree and resolve the winner at the flush: the first-canonical-position
+    # rule, the sign of a zero extremum (the reference's `a < m ? m : a`
+    # keeps the EARLIER of -0 / +0), NaN never winning, and rows whose every
+    # value is NaN or -inf must all come out bit for bit, max and min, with
+    # and without the fused mean.
+    rng = np.random.default_rng(91 + cols)
+    n = 2000
+    src = np.concatenate([rng.integers(0, n, 20000), rng.integers(0, n, 20000),
+                          rng.integers(0, 40, 3000), rng.integers(0, n, 1500)]).astype(np.uint32)
+    dst = np.concatenate([np.zeros(20000, np.int64) + 3, rng.integers(0, n, 20000),
+                          np.zeros(3000, np.int64) + 11,
+                          np.zeros(1500, np.int64) + 29]).astype(np.uint32)
+    g = O.Graph(n, src, dst)
+    g.plan = dict(long_threshold=1000, unit_cols=cols)
+    for dim in (8, 36, 100, 260):
+        # few distinct values: -1, -0.0, +0.0, 0.5, NaN; column 1 only zeros
+        # of both signs, column 2 only NaN, column 3 only -inf, column 4
+        # nothing above -0.0
+        pool = np.array([-1.0, -0.0, 0.0, 0.5, np.nan], np.float32)
+        x = pool[rng.integers(0, len(pool), (n, dim))]
+        x[:, 1] = np.where(rng.integers(0, 2, n) == 0, np.float32(-0.0), np.float32(0.0))
+        x[:, 2] = np.nan
+        x[:, 3] = -np.inf
+        x[:, 4] = np.where(rng.integers(0, 2, n) == 0, np.float32(-0.0), np.float32(-1.0))
+        for red in (O.MAX, O.MIN):
+            cfg = (O.U, O.NONE, O.COPY, red, O.V)
+            want = O.binary_reduce(g, cfg, u=x)
+            val, au, ae = gpu_reduce(g, cfg, u=x, want_arg_other=True, want_arg_edge=True)
+            assert val.tobytes() == want.tobytes(), (cols, dim, red)  # sign of zero included
+            if red == O.MAX:
+                v2, au2, ae2 = O.copy_max_argmax(g, x)
+                assert val.tobytes() == v2.tobytes()
+                assert np.array_equal(au, au2) and np.array_equal(ae, ae2), (cols, dim)
+            else:  # the winner's feature is the extremum, bit for bit (or no winner)
+                won = au >= 0
+                picked = x[np.where(won, au, 0), np.arange(dim)[None, :]]
+                assert (picked.view(np.uint32)[won] == val.view(np.uint32)[won]).all()
+            # plain extremum (no argmax) and the fused second reduction
+            assert gpu_reduce(g, cfg, u=x).tobytes() == want.tobytes()
+        xz = np.nan_to_num(x, nan=0.25, neginf=-2.0)  # finite values for the mean
+        o2 = torch.empty((n, dim), device="cuda")
+        h = dev_graph(g, O.DST_MAJOR)
+        res = P.binary_reduce(h, (O.U, O.NONE, O.COPY, O.MAX, O.V), u=cuda(xz), out2=o2,
+                              reduce2=P.MEAN, want_arg_other=True, want_arg_edge=True)
+        v2, au2, ae2 = O.copy_max_argmax(g, xz)
+        assert res[0].cpu().numpy().tobytes() == v2.tobytes()
+        assert np.array_equal(res[1].cpu().numpy(), au2) and np.array_equal(res[2].cpu().numpy(), ae2)
+        assert o2.cpu().numpy().tobytes() == O.mean(g, xz).tobytes()
+        g.__dict__.pop("_dev", None)
