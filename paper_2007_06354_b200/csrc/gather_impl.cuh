@@ -34,8 +34,23 @@ constexpr int kThreads = 256;
 // minimum resident blocks per SM.  Measured on B200 (scripts/var_ab.sh): warp
 // parallelism beats per-warp depth -- U=8 at 3 blocks/SM for <=128 columns,
 // U=2 at 4 blocks/SM (32 warps) for 256 columns: 94% of HBM on uniform graphs.
+// <= 128 columns have a second geometry, U=4 at 5 blocks/SM (48 registers,
+// 40 warps), used when the gathered table does not fit the L2: ncu on the
+// config-3 fused forward showed 24 warps per SM waiting on the long
+// scoreboard at 51% issue.  r02z, config 3 (max + argmax / mean / fused /
+// mean backward, ms): U8 x 3: 6.20 / 5.01 / 7.62 / 5.32; U4 x 3: 6.92 / 5.85
+// / 7.46 / 6.15; U4 x 4: 6.17 / 5.11 / 6.68 / 5.42; U4 x 5: 6.04 / 4.79 /
+// 6.51 / 5.15; U4 x 6 (spills): 6.46 / 6.38 / 9.45 / 6.55; U2 x 6: 7.71 /
+// 5.48 / 7.20 / 5.81; U8 x 4 (spills): 5.96 / 6.40 / 7.19 / 6.65.  The
+// L2-resident config-1 shape runs 0.070 ms with U8 x 3 and 0.099 with U4 x 5.
 #ifndef GATHER_U1
 #define GATHER_U1 8
+#endif
+#ifndef GATHER_U1B
+#define GATHER_U1B 4
+#endif
+#ifndef GATHER_MINB1B
+#define GATHER_MINB1B 5
 #endif
 #ifndef GATHER_U2
 #define GATHER_U2 2
@@ -893,7 +908,8 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
 
 // -------------------------------------------------------------- segments
 template <int VPL, int U, int BOP, int ROP, int ARG, int SK, bool LO, int MODE>
-__global__ void __launch_bounds__(kThreads, VPL == 1 ? GATHER_MINB1 : VPL == 5 ? GATHER_MINB5 : GATHER_MINB2) k_gather(const StreamLaunch p) {
+__global__ void __launch_bounds__(kThreads, VPL == 1 ? (U == GATHER_U1 ? GATHER_MINB1 : GATHER_MINB1B)
+                                                     : VPL == 5 ? GATHER_MINB5 : GATHER_MINB2) k_gather(const StreamLaunch p) {
   const int lane = threadIdx.x & 31;
   const RowLaunch& L = p.row;
   const bool need_eid = L.lhs.role == ROLE_EID ||
@@ -957,26 +973,39 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
       return cudaErrorInvalidValue;
     }
   } else {
-    constexpr int U = VPL == 1 ? GATHER_U1 : VPL == 5 ? GATHER_U5 : GATHER_U2;
     constexpr int MODE = DUAL ? 2 : 0;
-    static std::atomic<int> blocks_per_sm{0};
-    int bps = blocks_per_sm.load(std::memory_order_relaxed);
-    if (!bps) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps,
-                                                    k_gather<VPL, U, BOP, ROP, ARG, SK, LO, MODE>,
-                                                    kThreads, 0);
-      if (bps < 1) bps = 1;
-      blocks_per_sm.store(bps, std::memory_order_relaxed);
-    }
-    const unsigned grid = static_cast<unsigned>(sms * bps);
-    if constexpr (!ARG && !DUAL) {  // argmax / dual never run source-blocked
-      if (p.row.acc_in || p.row.epi) {
-        k_gather<VPL, U, BOP, ROP, ARG, SK, LO, 1><<<grid, kThreads, 0, s>>>(p);
-        note_launch();
-        return cudaGetLastError();
+    auto launch = [&](auto u_tag) -> cudaError_t {
+      constexpr int U = decltype(u_tag)::value;
+      static std::atomic<int> blocks_per_sm{0};
+      int bps = blocks_per_sm.load(std::memory_order_relaxed);
+      if (!bps) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps,
+                                                      k_gather<VPL, U, BOP, ROP, ARG, SK, LO, MODE>,
+                                                      kThreads, 0);
+        if (bps < 1) bps = 1;
+        blocks_per_sm.store(bps, std::memory_order_relaxed);
       }
+      const unsigned grid = static_cast<unsigned>(sms * bps);
+      if constexpr (!ARG && !DUAL) {  // argmax / dual never run source-blocked
+        if (p.row.acc_in || p.row.epi) {
+          k_gather<VPL, U, BOP, ROP, ARG, SK, LO, 1><<<grid, kThreads, 0, s>>>(p);
+          note_launch();
+          return cudaGetLastError();
+        }
+      }
+      k_gather<VPL, U, BOP, ROP, ARG, SK, LO, MODE><<<grid, kThreads, 0, s>>>(p);
+      note_launch();
+      return cudaGetLastError();
+    };
+    if constexpr (VPL == 1) {
+      // the gathered table against the L2 (126 MB): latency-bound gathers
+      // want more warps, L2-resident ones more edges per warp
+      const double table = static_cast<double>(p.row.lhs.rows) * static_cast<double>(p.row.lhs.ld) * 4.0;
+      if (table > 96.0 * 1048576.0) return launch(std::integral_constant<int, GATHER_U1B>{});
+      return launch(std::integral_constant<int, GATHER_U1>{});
+    } else {
+      return launch(std::integral_constant<int, VPL == 5 ? GATHER_U5 : GATHER_U2>{});
     }
-    k_gather<VPL, U, BOP, ROP, ARG, SK, LO, MODE><<<grid, kThreads, 0, s>>>(p);
   }
   note_launch();
   return cudaGetLastError();
