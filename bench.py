@@ -102,6 +102,27 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def poke(self):
+        """One in-process NVML sample, taken by the caller between enqueuing
+        the timed steps and synchronizing: a region of a few milliseconds
+        (config 1) ends before nvidia-smi's next 20 ms tick."""
+        try:
+            import pynvml as N
+            if not getattr(self, "_nvml", None):
+                N.nvmlInit()
+                self._nvml = N.nvmlDeviceGetHandleByIndex(int(self.device))
+            h = self._nvml
+            sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(h) if hasattr(
+                N, "nvmlDeviceGetCurrentClocksEventReasons") else \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            flag = lambda bit: "Active" if r & bit else "Not Active"  # noqa: E731
+            self.lines.append(",".join(str(v) for v in (
+                self.device, sm, mx, "", hex(r), flag(0x8), flag(0x40), flag(0x20), flag(0x4))))
+        except Exception:
+            pass
+
     def __exit__(self, *exc):
         if self.proc:
             self.proc.terminate()
@@ -349,6 +370,7 @@ def run_ours(args, rank, world, dist):
         for i in range(args.steps):
             step(evs[i])
         stop.record(stream)
+        clk.poke()
         torch.cuda.synchronize(dev)
     if dist:
         dist.barrier()
@@ -737,6 +759,7 @@ def run_config(args, rank, world, dist):
             if flush is not None:
                 flush.zero_()  # 256 MB > L2: every step starts cold (timing rule)
             step(evs[i])
+        clk.poke()
         torch.cuda.synchronize(dev)
     launches = P.launch_count() - launches0
     pass_ms = [[e[k].elapsed_time(e[k + 1]) for e in evs] for k in range(len(passes))]
@@ -1040,6 +1063,7 @@ def run_cfg3(args, rank, world, dist):
     with ClockSampler(dev) as clk:
         for i in range(args.steps):
             step(evs[i])
+        clk.poke()
         torch.cuda.synchronize(dev)
     if dist:
         dist.barrier()

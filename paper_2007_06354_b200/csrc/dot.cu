@@ -18,6 +18,12 @@
 //     grad_a: `heads` dots of gather_dim/heads columns each).
 // Edge outputs are stored by edge id; node outputs fold the 32 per-edge
 // dots in canonical order with the row's reducer.
+// Measured alternative (r03c / r03d): a systolic warp pipeline without the
+// shared-memory transpose -- lane l owns a few columns of the head, takes an
+// item's running sum from lane l - 1 by SHFL.UP and hands it on, lane l on
+// item s - l at step s.  Bit-exact, but the skew makes every warp load touch
+// 32 different 32-byte sectors for 8 bytes each: config 4 grad_a 13.4 ->
+// 33.8 ms (44.8 with the loads grouped), config 2 grad_e 3.4 -> 7.3 ms.
 #include "device_ops.cuh"
 
 namespace gspmm_b200 {

@@ -708,3 +708,23 @@ def test_long_row_argmax_ties_zeros_and_nans(cols):
         assert np.array_equal(res[1].cpu().numpy(), au2) and np.array_equal(res[2].cpu().numpy(), ae2)
         assert o2.cpu().numpy().tobytes() == O.mean(g, xz).tobytes()
         g.__dict__.pop("_dev", None)
+
+
+def test_zero_width_operands_give_rows_by_zero():
+    # the reference returns a rows x 0 FeatureMatrix for zero-width operands
+    # (binary_out_dim, ops.cpp:63-67); a dot or a 0-against-1 broadcast has
+    # nothing to read there and is rejected
+    g = g_of(4, [(0, 1), (2, 1), (3, 0)])
+    h = dev_graph(g, O.DST_MAJOR)
+    z = torch.empty((4, 0), device="cuda")
+    ze = torch.empty((3, 0), device="cuda")
+    assert tuple(P.out_shape(h, "u_copy_add_v", u=z)) == (4, 0)
+    assert P.binary_reduce(h, "u_copy_add_v", u=z).shape == (4, 0)
+    assert P.binary_reduce(h, "u_mul_e_add_v", u=z, e=ze).shape == (4, 0)
+    assert P.binary_reduce(h, "u_add_v_copy_e", u=z, v=z).shape == (3, 0)
+    with pytest.raises(P.ShapeError):
+        P.binary_reduce(h, "u_dot_v_copy_e", u=z, v=z)
+    with pytest.raises(P.ShapeError):
+        P.binary_reduce(h, "u_mul_e_add_v", u=z, e=torch.ones((3, 1), device="cuda"))
+    with pytest.raises(P.ShapeError):  # wrong row count is still reported first
+        P.binary_reduce(h, "u_copy_add_v", u=torch.empty((5, 0), device="cuda"))
