@@ -923,10 +923,12 @@ class C3Reference:
         126) and its CSV rows (bench.cpp:128-145) are kept."""
         O, R = self.O, self.R
         names = {O.SPMM: "RowParallelSpmm", O.BLOCKED: "BlockedPull", O.PULL: "Pull"}
-        table, rows = {}, []
+        table, rows, pruned = {}, [], set()
         for name, (cfg, kw) in self._pass_args().items():
             table[name] = {}
             for st, sname in names.items():
+                if st in pruned:  # more than 2x behind the best on the first pass
+                    continue
                 if self.views is not None:
                     buf = C.create_string_buffer(512)
                     t = R.ref_bench_csv(self.views, st, *cfg, kw.get("u"), kw.get("v"),
@@ -940,6 +942,9 @@ class C3Reference:
                 table[name][sname] = t
             best = min(table[name], key=table[name].get)
             self.strategy[name] = {v: k for k, v in names.items()}[best]
+            for st, sname in names.items():
+                if sname in table[name] and table[name][sname] > 2.0 * table[name][best]:
+                    pruned.add(st)
         self.strategy_table = table
         if rows:
             self.csv = [R.ref_bench_csv_header().decode()] + rows

@@ -26,6 +26,21 @@
 #include "stream.h"
 #include "tma.cuh"
 
+// GSPMM_BOUNDS=1 (a checking build, scripts/gpu/bounds.sh): device asserts on
+// every gathered row id, output row, shared-memory stage offset and id-ring
+// slot of the two planned kernels.  compute-sanitizer is closed on the GPU
+// pool this was developed on, so the parity case (scripts/sanitize_case.py)
+// runs against this build instead.
+#ifndef GSPMM_BOUNDS
+#define GSPMM_BOUNDS 0
+#endif
+#if GSPMM_BOUNDS
+#include <cassert>
+#define GS_ASSERT(c) assert(c)
+#else
+#define GS_ASSERT(c) ((void)0)
+#endif
+
 namespace gspmm_b200 {
 namespace gather_detail {
 
@@ -192,6 +207,7 @@ struct Acc {
       if (fix && L.mean) x = deg ? __fdiv_rn(x, __uint2float_rn(deg)) : 0.0f;
       o[t] = x;
     }
+    GS_ASSERT(r < L.num_rows && c0 + cw <= L.width);
     float* orow = L.out + static_cast<int64_t>(r) * L.out_ld + c0;
     if (c + 4 <= cw) {
 #if GATHER_STREAM_OUT
@@ -349,6 +365,7 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
       if constexpr (SK == SK_WIN || SK == SK_SCALE) r[k][0] = __shfl_sync(kFull, win_r, sl);
       if constexpr (ARG == 2) okey[k] = o;
       const uint32_t lr = LO ? o : static_cast<uint32_t>(operand_row(lrole, 0, o, e, jb + kk));
+      GS_ASSERT(static_cast<int64_t>(lr) < L.lhs.rows);
 #pragma unroll
       for (int v = 0; v < VPL; ++v)
         x[k][v] = __ldg(reinterpret_cast<const float4*>(lrow[v] + static_cast<uint64_t>(lr) * ldb));
@@ -548,6 +565,7 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
         if (m >= rounds) return;
         const uint32_t slot = (gs0 + m) % NI;
         const uint32_t cnt = min(R, n - m * R);
+        GS_ASSERT(cnt <= static_cast<uint32_t>(G::MR) && e0 + m * R + cnt <= e1);
         for (uint32_t t = static_cast<uint32_t>(ptid); t < cnt; t += PL) {
           cp_async_4(sid + slot * G::MR + t, L.indices + e0 + m * R + t);
           if (need_eid) cp_async_4(seid + slot * G::MR + t, L.eids + e0 + m * R + t);
@@ -579,8 +597,10 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
             const uint32_t row = lrole == ROLE_OTHER
                                      ? o
                                      : static_cast<uint32_t>(operand_row(lrole, 0, o, e, e0 + m * R + q));
+            GS_ASSERT(static_cast<int64_t>(row) < L.lhs.rows && q < static_cast<uint32_t>(G::MR));
             x[k] = __ldg(reinterpret_cast<const float4*>(lbase + static_cast<int64_t>(row) * lld + 4 * t));
             off[k] = static_cast<int>(q) * sst + 4 * t;
+            GS_ASSERT(off[k] + 4 <= G::DF);
           }
           q += dq;
           t += dt;
@@ -782,6 +802,8 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
             }
           };
           const uint32_t nfull = cnt / KB;
+          GS_ASSERT(static_cast<size_t>(cnt - 1) * stf + cc + FW <= static_cast<size_t>(G::DF));
+          GS_ASSERT(!SMALL || static_cast<size_t>(cnt - 1) * nh + hrel < static_cast<size_t>(G::SF));
           if (nfull) {
             ld(0, xa, sa);
             uint32_t bk = 0;
@@ -856,6 +878,7 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
                 if (fix && deg == 0) a = 0.0f;
               }
               if (fix && L.mean) a = deg ? __fdiv_rn(a, __uint2float_rn(deg)) : 0.0f;
+              GS_ASSERT(r < L.num_rows && c0 + cc + t < L.width);
               L.out[static_cast<int64_t>(r) * L.out_ld + c0 + cc + t] = a;
               if constexpr (ARG) {
                 const int64_t ab = static_cast<int64_t>(r) * L.arg_ld + c0 + cc + t;
