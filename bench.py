@@ -1247,6 +1247,20 @@ def run_cfg3(args, rank, world, dist):
         "roofline": roofline,
         "e2e": e2e, "cpu_baseline": cpu,
         "gpu_launches": int(launches), "clocks": clk.summary(), "impl": "b200",
+        # the reference's CSV schema (bench.cpp:128-145) plus the columns
+        # SURVEY 5 asks of the B200 build, one row per pass of the step
+        "csv": ["config,strategy,nodes,edges,dim,threads,kb,nb,iters,mean_s,min_s,gbps,gpus,"
+                "edges_per_s,alg_bytes,hbm_frac,dram_bytes"] + [
+            ",".join(str(v) for v in (
+                C3_PASSES_B200[k].replace(",", ";"), "b200", C3_N, gd.num_edges, F, 0, 0, 0,
+                args.steps, f"{pass_ms[k] * 1e-3:.6e}", "",
+                f"{alg[C3_PASSES_B200[k]] / (pass_ms[k] * 1e-3) / 1e9:.3f}", world,
+                f"{(gd.num_edges if k < 2 else 0) / (pass_ms[k] * 1e-3):.4e}",
+                alg[C3_PASSES_B200[k]],
+                f"{alg[C3_PASSES_B200[k]] / (pass_ms[k] * 1e-3) / 1e9 / peak:.3f}",
+                int(traffic["passes"][C3_PASSES_B200[k]]) if traffic and world == 1 and
+                C3_PASSES_B200[k] in traffic.get("passes", {}) else ""))
+            for k in range(len(passes))],
         **({"verify": verify} if verify is not None else {}),
     }
 
