@@ -728,3 +728,42 @@ def test_zero_width_operands_give_rows_by_zero():
         P.binary_reduce(h, "u_mul_e_add_v", u=z, e=torch.ones((3, 1), device="cuda"))
     with pytest.raises(P.ShapeError):  # wrong row count is still reported first
         P.binary_reduce(h, "u_copy_add_v", u=torch.empty((5, 0), device="cuda"))
+
+
+def test_large_table_geometry_all_operator_families():
+    # <= 128-column segment units switch to the 4-edges x 5-blocks geometry
+    # when the gathered table exceeds the L2 (gather_impl.cuh launch_k): a
+    # 400k x 64 table (102 MB) puts every operator family on that instance --
+    # copy, u_mul_e with scalar and per-head weights, add / sub / div, max +
+    # argmax with the fused mean, the mean backward's per-neighbour scale,
+    # copy_e -- bitwise against the oracle.
+    n, m, F = 400_000, 2_500_000, 64
+    src, dst = P.synth_rmat(n, m, 0.45, 0.22, 0.22, 0.11, 5)
+    g = O.Graph(n, src, dst)
+    x = O.normal_features(n, F, 1)
+    v = O.random_features(n, F, 2) + np.float32(2.0)  # away from zero: a divisor
+    w = O.gcn_weights(n, src, dst)
+    for name, kw in (("u_copy_add_v", dict(u=x)), ("u_mul_e_add_v", dict(u=x, e=w)),
+                     ("u_add_v_add_v", dict(u=x, v=v)), ("u_sub_v_add_v", dict(u=x, v=v)),
+                     ("u_div_v_add_v", dict(u=x, v=v)), ("u_mul_v_max_v", dict(u=x, v=v)),
+                     ("u_copy_min_v", dict(u=x)), ("v_mul_e_add_u", dict(v=x, e=w))):
+        cfg = O.named_config(name)
+        assert O.bit_equal(gpu_reduce(g, cfg, **kw), O.binary_reduce(g, cfg, **kw)), name
+    a = O.normal_features(m, 8, 3)
+    assert O.bit_equal(gpu_reduce(g, (O.U, O.E, O.MUL, O.SUM, O.V), u=x, e=a, heads=8),
+                       O.multihead_u_mul_e_sum(g, x, a, 8))
+    h = dev_graph(g, O.DST_MAJOR)
+    o2 = torch.empty((n, F), device="cuda")
+    val, au, ae = P.binary_reduce(h, (O.U, O.NONE, O.COPY, O.MAX, O.V), u=cuda(x), out2=o2,
+                                  reduce2=P.MEAN, want_arg_other=True, want_arg_edge=True)
+    v2, au2, ae2 = O.copy_max_argmax(g, x)
+    assert O.bit_equal(val.cpu().numpy(), v2) and np.array_equal(au.cpu().numpy(), au2)
+    assert np.array_equal(ae.cpu().numpy(), ae2) and O.bit_equal(o2.cpu().numpy(), O.mean(g, x))
+    deg = O.in_degree(g)
+    inv = np.zeros(n, np.float32)
+    inv[deg > 0] = np.float32(1) / deg[deg > 0].astype(np.float32)
+    got = gpu_reduce(g, (O.V, O.NONE, O.COPY, O.SUM, O.U), v=x, other_scale=torch.from_numpy(inv).cuda())
+    assert O.bit_equal(got, O.mean_backward(g, x))
+    ef = O.normal_features(m, F, 4)  # copy_e: the gathered table is the edge matrix (640 MB)
+    cfg = O.named_config("e_copy_add_v")
+    assert O.bit_equal(gpu_reduce(g, cfg, e=ef), O.binary_reduce(g, cfg, e=ef))
