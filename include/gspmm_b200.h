@@ -161,7 +161,12 @@ typedef struct {
   uint32_t unit_cols;      /* 0 -> automatic long-row unit widths; else this
                               many columns per unit (multiple of 4, <= 512) */
   int32_t kernel;          /* 0 = planned kernels; 1 = the register kernel
-                              (rows.cu) for every call (a reference path) */
+                              (rows.cu) for every call (a reference path);
+                              2 = planned kernels with the segment kernel
+                              launched as a programmatic dependent of the
+                              long-row kernel, its blocks taking each SM a
+                              long-row CTA leaves (measured slower on
+                              configs 2 and 3) */
   uint32_t long_ctas;      /* 0 -> long-row units first, on every SM, then the
                               segments (default); N -> the long-row units run
                               concurrently with the segment kernel on N CTAs

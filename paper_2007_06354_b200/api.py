@@ -168,7 +168,8 @@ class Graph:
     def set_plan(self, seg_cost=0, long_threshold=0, unit_cols=0, kernel=0, long_ctas=0):
         """Rebuild the device plan (gspmm_graph_set_plan): segment-unit cost,
         a fixed long-row threshold, a fixed long-row unit width (multiple of
-        4, <= 512), kernel=1 for the register kernel on every call, long_ctas
+        4, <= 512), kernel=1 for the register kernel on every call (2: planned kernels with
+        the segment kernel a programmatic dependent of the long-row kernel), long_ctas
         = N to run the long-row units concurrently with the segments on N
         CTAs.  0 = the default of each.  Results never depend on the plan."""
         p = A.Plan(seg_cost, long_threshold, unit_cols, kernel, long_ctas)

@@ -162,6 +162,7 @@ struct gspmm_graph_s {
   uint32_t unit_cols = 0;       // 0 -> automatic long-row unit widths
   int rows_kernel_only = 0;     // 1 -> every call on the register kernel (rows.cu)
   uint32_t long_ctas = 0;       // 0 -> long rows before the segments; N -> concurrent
+  int pdl_pair = 0;             // 1 -> programmatic overlap of the long-row / segment pair
 };
 
 namespace {
@@ -521,6 +522,7 @@ int build_source_blocks(gspmm_graph_s* g, uint32_t nb, cudaStream_t s) {
     sg->forced_long = g->forced_long;
     sg->unit_cols = g->unit_cols;
     sg->long_ctas = g->long_ctas;
+    sg->pdl_pair = g->pdl_pair;
     g->blocks.push_back(sg);
   }
   g->block_nb = nb;
@@ -761,6 +763,19 @@ int launch(gspmm_graph_s* g, CallCtx* ctx, Bound& b, cudaStream_t s) {
         // long-row CTAs concurrent on an automatic budget, 5.78 on 74 SMs --
         // a long-row CTA holds its SM's register file, and the segment
         // kernel, bound by the L2's throughput, needs every SM)
+        // Plan option kernel = 2 launches the two as a programmatic-
+        // dependent pair: the segment kernel's blocks take each SM as its
+        // long-row CTA runs out of units instead of waiting for the slowest
+        // unit.  Measured (r04a) slower where it matters: the latency-bound
+        // long-row units lose more to the segment blocks' traffic than the
+        // idle tail returns (cfg3 max + argmax 6.0 -> 6.7 ms, cfg2 1.73 ->
+        // 2.08, cfg4 7.08 -> 6.97), so the default stays strictly serial.
+        if (p.n_units && g->pdl_pair) {
+          err = cudaMemsetAsync(ctx->d_counter, 0, 2 * sizeof(uint32_t), s);
+          if (err != cudaSuccess) return cuda_fail(err, "counter reset");
+          pl.pdl = 1;
+          p.pdl = 2;
+        }
         err = launch_gather(pl, s);
       } else {
         // long-row units on a side stream on long_ctas CTAs, concurrently
@@ -1100,8 +1115,8 @@ int gspmm_graph_set_plan(gspmm_graph g, const gspmm_plan* plan) {
   if (!g) return fail(GSPMM_ERR_ARG, "null graph handle");
   const gspmm_plan dflt{};
   if (!plan) plan = &dflt;
-  if (plan->unit_cols % 4 || plan->unit_cols > 512 || plan->kernel < 0 || plan->kernel > 1)
-    return fail(GSPMM_ERR_ARG, "plan: unit_cols must be a multiple of 4 up to 512, kernel 0 or 1");
+  if (plan->unit_cols % 4 || plan->unit_cols > 512 || plan->kernel < 0 || plan->kernel > 2)
+    return fail(GSPMM_ERR_ARG, "plan: unit_cols must be a multiple of 4 up to 512, kernel 0, 1 or 2");
   std::lock_guard<std::recursive_mutex> lock(g->mu);
   CUDA_TRY(cudaSetDevice(g->device), "cudaSetDevice");
   // in-flight calls may still read the old plan
@@ -1109,7 +1124,8 @@ int gspmm_graph_set_plan(gspmm_graph g, const gspmm_plan* plan) {
   g->seg_cost = plan->seg_cost;
   g->forced_long = plan->long_threshold;
   g->unit_cols = plan->unit_cols;
-  g->rows_kernel_only = plan->kernel;
+  g->rows_kernel_only = plan->kernel == 1;
+  g->pdl_pair = plan->kernel == 2;
   g->long_ctas = plan->long_ctas;
   for (auto* sg : g->blocks) destroy_graph(sg);
   g->blocks.clear();

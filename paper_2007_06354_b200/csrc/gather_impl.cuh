@@ -510,6 +510,9 @@ __global__ void __launch_bounds__(kLgThreads, 1) k_long_rg(const StreamLaunch p)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool producer = warp < kLgProducers;
   const RowLaunch& L = p.row;
+  // the segment kernel launched behind this one (StreamLaunch::pdl) may take
+  // every SM a long-row CTA leaves: the two write disjoint output rows
+  if (p.pdl == 1) asm volatile("griddepcontrol.launch_dependents;");
   const int rw = SMALL ? p.rhs_width : 0;  // small floats per edge (1 = scalar)
   const bool need_eid = L.lhs.role == ROLE_EID || (SK != SK_SCALE && SMALL && L.rhs.role == ROLE_EID);
   float* sdata = sm;                                                          // NB x DF
@@ -971,12 +974,15 @@ __global__ void __launch_bounds__(kThreads, VPL == 1 ? (U == GATHER_U1 ? GATHER_
     u.e1 = __ldg(L.indptr + u.r1);
     wide_unit<VPL, U, BOP, ROP, ARG, SK, LO, MODE>(L, u, need_eid, sbase, sld, srole, lane);
   }
+  // dependent of the long-row kernel: do not complete before it has
+  if (p.pdl == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // p.mode: 0 = row segments (k_gather), 1 = long-row column units (k_long_rg)
 template <int VPL, int BOP, int ROP, int ARG, int SK, bool LO, bool DUAL = false>
 cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
+  cudaError_t e = cudaSuccess;
+  if (!p.pdl) e = cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const int sms = p.row.num_sms > 0 ? p.row.num_sms : 148;
   if (p.mode == 1) {
@@ -1009,16 +1015,28 @@ cudaError_t launch_k(const StreamLaunch& p, cudaStream_t s) {
         blocks_per_sm.store(bps, std::memory_order_relaxed);
       }
       const unsigned grid = static_cast<unsigned>(sms * bps);
+      // pdl 2: launched behind the long-row kernel with programmatic stream
+      // serialization -- blocks start on SMs as the long-row CTAs leave them
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(kThreads);
+      cfg.stream = s;
+      cudaLaunchAttribute at{};
+      at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at.val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = &at;
+      cfg.numAttrs = p.pdl == 2 ? 1 : 0;
+      cudaError_t le;
       if constexpr (!ARG && !DUAL) {  // argmax / dual never run source-blocked
         if (p.row.acc_in || p.row.epi) {
-          k_gather<VPL, U, BOP, ROP, ARG, SK, LO, 1><<<grid, kThreads, 0, s>>>(p);
+          le = cudaLaunchKernelEx(&cfg, k_gather<VPL, U, BOP, ROP, ARG, SK, LO, 1>, p);
           note_launch();
-          return cudaGetLastError();
+          return le != cudaSuccess ? le : cudaGetLastError();
         }
       }
-      k_gather<VPL, U, BOP, ROP, ARG, SK, LO, MODE><<<grid, kThreads, 0, s>>>(p);
+      le = cudaLaunchKernelEx(&cfg, k_gather<VPL, U, BOP, ROP, ARG, SK, LO, MODE>, p);
       note_launch();
-      return cudaGetLastError();
+      return le != cudaSuccess ? le : cudaGetLastError();
     };
     if constexpr (VPL == 1) {
       // the gathered table against the L2 (126 MB): latency-bound gathers

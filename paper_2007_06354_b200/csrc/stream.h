@@ -21,6 +21,14 @@ struct StreamLaunch {
   int rhs_width = 0;  // small-operand floats per edge (0 = none, 1 = scalar, H = heads)
   int mode = 0;       // 0 = row segments (k_gather), 1 = long-row units (k_long_rg)
   uint32_t grid = 0;  // mode 1: CTAs (0 = one per SM)
+  // Programmatic dependent launch of the pair (long-row kernel, segment
+  // kernel) on one stream: 0 = plain launches (each zeroes its counter);
+  // 1 = this kernel is the primary (its CTAs release the dependent grid as
+  // they start); 2 = this kernel is the dependent (its blocks take the SMs
+  // the primary's CTAs leave, and wait for the primary's end before they
+  // exit, so the stream sees the pair complete in order).  With 1 / 2 the
+  // caller has zeroed both counters before the primary.
+  int pdl = 0;
 };
 
 // The planned row kernels (gather_copy.cu dispatches on the operator).

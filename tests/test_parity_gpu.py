@@ -452,6 +452,25 @@ def test_register_path_matches_planned_path():
     assert O.bit_equal(reg, O.binary_reduce(g, O.named_config("u_mul_e_add_v"), u=x, e=w))
 
 
+def test_programmatic_dependent_pair_matches_serial_launches():
+    # plan kernel=2: the segment kernel is a programmatic dependent of the
+    # long-row kernel (its blocks start while long-row CTAs still run); the
+    # outputs, the fused second reduction included, stay bitwise, call after
+    # call on one stream
+    src, dst = O.gen_rmat(4000, 90000, seed=11)
+    g = O.Graph(4000, src, dst)
+    x = O.normal_features(4000, 100, 2)
+    h = P.Graph(*g.dst_major, orientation=P.DST_MAJOR)
+    h.set_plan(long_threshold=150, kernel=2)
+    assert h.num_long_rows > 0
+    want_sum = O.binary_reduce(g, O.named_config("u_copy_add_v"), u=x)
+    want_max = O.binary_reduce(g, O.named_config("u_copy_max_v"), u=x)
+    xd = cuda(x)
+    for _ in range(3):
+        assert O.bit_equal(P.binary_reduce(h, "u_copy_add_v", u=xd).cpu().numpy(), want_sum)
+        assert O.bit_equal(P.binary_reduce(h, "u_copy_max_v", u=xd).cpu().numpy(), want_max)
+
+
 @pytest.mark.parametrize("cols", [0, 4, 8, 12, 32, 64, 128, 132, 256, 512])
 def test_long_row_column_units(cols):
     # long rows run as column units of `cols` columns (0: the automatic
