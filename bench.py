@@ -1005,6 +1005,9 @@ def run_cfg3(args, rank, world, dist):
                  orientation=P.DST_MAJOR, device=dev)
     gs = P.Graph(*slice_csr(*scsr, s_lo, s_hi), num_rows=rs, num_cols=C3_N,
                  orientation=P.SRC_MAJOR, device=dev)
+    if args.split_edges:  # not the default: long rows' sums leave the reference's bits
+        gd.set_plan(split_edges=args.split_edges)
+        gs.set_plan(split_edges=args.split_edges)
     F = C3_F
     x = x_h.cuda(dev)
     gy = gy_h.cuda(dev)
@@ -1103,12 +1106,22 @@ def run_cfg3(args, rank, world, dist):
             xn, gyn = x_h.numpy(), gy_h.numpy()
             w_max, w_au, _ = O.copy_max_argmax(og, xn)
             w_gmax = O.argmax_backward(w_au, gyn, C3_N)
+            w_mean, w_gxm = O.mean(og, xn), O.mean_backward(og, gyn)
             verify = {"max": bool(O.bit_equal(full["mx"], w_max)),
                       "argmax": bool(np.array_equal(full["au"], w_au)),
-                      "mean": bool(O.bit_equal(full["mean"], O.mean(og, xn))),
-                      "mean_backward": bool(O.bit_equal(full["gxm"], O.mean_backward(og, gyn))),
+                      "mean": bool(O.bit_equal(full["mean"], w_mean)),
+                      "mean_backward": bool(O.bit_equal(full["gxm"], w_gxm)),
+                      "mean_rel_err": float(O.max_rel_error(full["mean"], w_mean)),
+                      "mean_backward_rel_err": float(O.max_rel_error(full["gxm"], w_gxm)),
                       "max_backward_rel_err": float(O.max_rel_error(full["gmax"], w_gmax))}
-            verify["ok"] = all(v for k, v in verify.items() if k != "max_backward_rel_err") and \
+            # default plan: every sum bitwise; --split-edges: max / argmax
+            # bitwise, the sums of the split rows only sanity-bounded (a
+            # re-associated sum of a 10^5-edge row differs from the
+            # reference's sequential fp32 fold by that fold's own rounding)
+            exact = ("max", "argmax") if args.split_edges else ("max", "argmax", "mean",
+                                                                "mean_backward")
+            verify["ok"] = all(verify[k] for k in exact) and \
+                verify["mean_rel_err"] <= 2e-3 and verify["mean_backward_rel_err"] <= 2e-3 and \
                 verify["max_backward_rel_err"] <= 1e-6
 
     # --- e2e: the C-ABI host entries with pinned host buffers ----------------
@@ -1240,7 +1253,12 @@ def run_cfg3(args, rank, world, dist):
         "config": c3_config(),
         "notes": {"parallelism": f"dst/src-row shards x{world}" if world > 1 else "single GPU",
                   "l2": "inputs (980 MB feature matrices) larger than the 126 MB L2; no flush",
-                  "mean_backward": "other_scale = 1/deg_in, prescaled rows"},
+                  "mean_backward": "other_scale = 1/deg_in, prescaled rows",
+                  **({"plan": f"split_edges={args.split_edges}: rows above the long-row threshold "
+                              "folded as chunks of edges (max / argmax bit-exact; sums of those "
+                              "rows re-associated: up to ~1e-3 from the reference's sequential "
+                              "fold, whose own rounding is that large); NOT the default, outside the parity "
+                              "contract"} if args.split_edges else {})},
         "passes_ms": {C3_PASSES_B200[k]: round(pass_ms[k], 4) for k in range(len(passes))},
         "passes_alg_gbs": {C3_PASSES_B200[k]: alg[C3_PASSES_B200[k]] / (pass_ms[k] * 1e-3) / 1e9
                            for k in range(len(passes))},
@@ -1384,6 +1402,9 @@ def main():
     ap.add_argument("--cfg5-chunk", type=int, default=0,
                     help="cfg5: all-gather / aggregation column chunk (0: 640 on one GPU, "
                          "else 256)")
+    ap.add_argument("--split-edges", type=int, default=0,
+                    help="cfg3 only, not the default: plan option split_edges (long rows folded "
+                         "as chunks of N edges; sums of those rows are no longer bit-identical)")
     ap.add_argument("--workload", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
                     help="cfg3 (the largest single-GPU BASELINE config, the headline), cfg2, "
                          "cfg1, cfg4, or cfg5 (multi-GPU GraphSAGE-mean with source-feature "

@@ -63,7 +63,7 @@
 extern "C" {
 #endif
 
-#define GSPMM_B200_ABI_VERSION 2
+#define GSPMM_B200_ABI_VERSION 3
 
 /* ---- status (error.hpp:22-45 taxonomy, plus device failures) ---- */
 enum {
@@ -153,7 +153,8 @@ typedef struct gspmm_graph_s* gspmm_graph;
 
 /* Device plan options (gspmm_graph_set_plan).  Zero-init = the defaults.
  * The plan only changes how work is cut into units, never a result: every
- * output stays the canonical left fold. */
+ * output stays the canonical left fold -- except under split_edges, the one
+ * option that trades the bits of long rows' sums for speed. */
 typedef struct {
   uint32_t seg_cost;       /* cost (edges + 2 per row) of a segment unit; 0 -> 256 */
   uint32_t long_threshold; /* 0 -> automatic plan levels; else rows above this
@@ -171,6 +172,20 @@ typedef struct {
                               segments (default); N -> the long-row units run
                               concurrently with the segment kernel on N CTAs
                               (one per SM; measured slower on config 3) */
+  uint32_t split_edges;    /* 0 -> every row is one sequential fold (the
+                              reference's bits for every operator; default).
+                              N -> rows above the plan's long-row threshold
+                              are cut into chunks of ~N edges, folded like
+                              short rows and combined in chunk order: Max /
+                              Min and argmax keep the reference's bits, a
+                              Sum / Mean becomes a fixed-order sum of chunk
+                              sums: deterministic, with no more rounding
+                              error than the sequential fold, but NOT within
+                              the reference's 1e-5 of that fold on hub rows
+                              (measured 9e-4 on config 3's mean backward:
+                              the fp32 fold of a 10^5-edge row carries that
+                              much rounding itself).  Outside the parity
+                              contract; opt-in. */
 } gspmm_plan;
 
 /* ---- errors ---- */

@@ -79,7 +79,8 @@ class Out(C.Structure):
 
 class Plan(C.Structure):
     _fields_ = [("seg_cost", C.c_uint32), ("long_threshold", C.c_uint32),
-                ("unit_cols", C.c_uint32), ("kernel", C.c_int32), ("long_ctas", C.c_uint32)]
+                ("unit_cols", C.c_uint32), ("kernel", C.c_int32), ("long_ctas", C.c_uint32),
+                ("split_edges", C.c_uint32)]
 
 
 class Options(C.Structure):

@@ -165,14 +165,20 @@ class Graph:
         check(A.LIB.gspmm_graph_set_source_blocks(self.handle, int(nblocks)), "set_source_blocks")
         return self
 
-    def set_plan(self, seg_cost=0, long_threshold=0, unit_cols=0, kernel=0, long_ctas=0):
+    def set_plan(self, seg_cost=0, long_threshold=0, unit_cols=0, kernel=0, long_ctas=0,
+                 split_edges=0):
         """Rebuild the device plan (gspmm_graph_set_plan): segment-unit cost,
         a fixed long-row threshold, a fixed long-row unit width (multiple of
         4, <= 512), kernel=1 for the register kernel on every call (2: planned kernels with
         the segment kernel a programmatic dependent of the long-row kernel), long_ctas
         = N to run the long-row units concurrently with the segments on N
-        CTAs.  0 = the default of each.  Results never depend on the plan."""
-        p = A.Plan(seg_cost, long_threshold, unit_cols, kernel, long_ctas)
+        CTAs.  0 = the default of each.  Results never depend on the plan,
+        except under split_edges = N: long rows are folded as chunks of ~N
+        edges combined in chunk order (max / min / argmax unchanged; sums of
+        those rows deterministic, but up to ~1e-3 from the reference's
+        sequential fold, whose own rounding is that large: outside the parity
+        contract)."""
+        p = A.Plan(seg_cost, long_threshold, unit_cols, kernel, long_ctas, split_edges)
         check(A.LIB.gspmm_graph_set_plan(self.handle, C.byref(p)), "set_plan")
         nl = C.c_uint32()
         check(A.LIB.gspmm_graph_info(self.handle, None, None, None, None, C.byref(nl)))

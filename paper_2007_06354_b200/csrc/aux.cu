@@ -123,6 +123,58 @@ unsigned grid_for(int64_t work, int threads) {
   return static_cast<unsigned>(b < 1 ? 1 : b);
 }
 
+// Long rows split by edges (plan option split_edges): one block per long
+// row, a thread per output column, the chunks' partials folded in chunk
+// order.  Sum adds the partial sums (a fixed order: deterministic, but not
+// the sequential fold's bits -- see gspmm_plan.split_edges);
+// Max / Min compare strictly, so the first chunk holding the extremum keeps
+// its value and its argmax -- the reference's first-wins result exactly.
+template <int ROP>
+__global__ void __launch_bounds__(128) k_combine_chunks(const CombineLaunch c) {
+  const uint32_t i = blockIdx.x;
+  const uint32_t r = __ldg(c.long_rows + i);
+  const uint2 rg = __ldg(c.ranges + i);
+  const uint32_t deg = __ldg(c.indptr + r + 1) - __ldg(c.indptr + r);
+  constexpr int KU = 8;  // partial loads in flight per thread
+  for (int col = threadIdx.x; col < c.width; col += blockDim.x) {
+    const float* pp = c.part + static_cast<int64_t>(rg.x) * c.pld + col;
+    float a = red_identity<ROP>();
+    float s2 = 0.0f;
+    int32_t ao = -1, ae = -1;
+    for (uint32_t k0 = 0; k0 < rg.y; k0 += KU) {
+      float v[KU], w[KU];
+#pragma unroll
+      for (int t = 0; t < KU; ++t) {
+        const uint32_t k = min(k0 + t, rg.y - 1);
+        v[t] = __ldg(pp + static_cast<int64_t>(k) * c.pld);
+        w[t] = c.part2 ? __ldg(c.part2 + static_cast<int64_t>(rg.x + k) * c.pld + col) : 0.0f;
+      }
+#pragma unroll
+      for (int t = 0; t < KU; ++t) {
+        if (k0 + t >= rg.y) break;
+        if constexpr (ROP == R_SUM) {
+          a = __fadd_rn(a, v[t]);
+        } else {
+          if (red_wins<ROP>(a, v[t])) {
+            a = v[t];
+            const int64_t q = static_cast<int64_t>(rg.x + k0 + t) * c.pld + col;
+            if (c.parg_other) ao = __ldg(c.parg_other + q);
+            if (c.parg_edge) ae = __ldg(c.parg_edge + q);
+          }
+        }
+        s2 = __fadd_rn(s2, w[t]);
+      }
+    }
+    if (c.mean) a = deg ? __fdiv_rn(a, __uint2float_rn(deg)) : 0.0f;
+    c.out[static_cast<int64_t>(r) * c.out_ld + col] = a;
+    if (c.out2)
+      c.out2[static_cast<int64_t>(r) * c.out2_ld + col] =
+          c.mean2 ? (deg ? __fdiv_rn(s2, __uint2float_rn(deg)) : 0.0f) : s2;
+    if (c.arg_other) c.arg_other[static_cast<int64_t>(r) * c.arg_ld + col] = ao;
+    if (c.arg_edge) c.arg_edge[static_cast<int64_t>(r) * c.arg_ld + col] = ae;
+  }
+}
+
 }  // namespace
 
 void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
@@ -199,6 +251,18 @@ cudaError_t launch_scale_rows(const float* x, int64_t rows, int64_t dim, int64_t
                               const float* scale, float* y, int64_t y_ld, cudaStream_t s) {
   if (rows == 0 || dim == 0) return cudaSuccess;
   k_scale_rows<<<grid_for(rows * 32, 256), 256, 0, s>>>(x, rows, dim, ld, scale, y, y_ld);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine_chunks(const CombineLaunch& c, cudaStream_t s) {
+  if (c.n_long == 0 || c.width == 0) return cudaSuccess;
+  switch (c.reduce) {
+    case R_SUM: k_combine_chunks<R_SUM><<<c.n_long, 128, 0, s>>>(c); break;
+    case R_MAX: k_combine_chunks<R_MAX><<<c.n_long, 128, 0, s>>>(c); break;
+    case R_MIN: k_combine_chunks<R_MIN><<<c.n_long, 128, 0, s>>>(c); break;
+    default: return cudaErrorInvalidValue;
+  }
   note_launch();
   return cudaGetLastError();
 }

@@ -145,6 +145,33 @@ cudaError_t launch_block_csr(const uint32_t* lo, const uint32_t* hi, uint32_t ro
 cudaError_t launch_scale_rows(const float* x, int64_t rows, int64_t dim, int64_t ld,
                               const float* scale, float* y, int64_t y_ld, cudaStream_t s);
 
+// Long rows split by edge ranges (plan option split_edges): the partial folds
+// of a long row's chunks (chunk rows [k0, k0 + nk) of part / part2 / parg_*,
+// leading dimension pld) are combined in chunk order into the row's outputs,
+// with the row epilogue (mean) applied.  ranges[i] = (k0, nk) of long_rows[i].
+struct CombineLaunch {
+  const uint32_t* long_rows = nullptr;
+  const uint2* ranges = nullptr;
+  uint32_t n_long = 0;
+  const uint32_t* indptr = nullptr;  // the graph's row pointer (degrees)
+  int32_t width = 0;
+  int32_t reduce = R_SUM;
+  int64_t pld = 0;
+  const float* part = nullptr;
+  const float* part2 = nullptr;
+  const int32_t* parg_other = nullptr;
+  const int32_t* parg_edge = nullptr;
+  float* out = nullptr;
+  int64_t out_ld = 0;
+  float* out2 = nullptr;
+  int64_t out2_ld = 0;
+  int32_t* arg_other = nullptr;
+  int32_t* arg_edge = nullptr;
+  int64_t arg_ld = 0;
+  bool mean = false, mean2 = false;
+};
+cudaError_t launch_combine_chunks(const CombineLaunch& c, cudaStream_t s);
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device),
 // thread-safe (aux.cu).
 cudaError_t set_max_dynamic_smem(const void* func, int bytes);

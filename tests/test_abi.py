@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert A.LIB.gspmm_abi_version() == 2
+    assert A.LIB.gspmm_abi_version() == 3
 
 
 def test_library_path_is_in_tree():
