@@ -172,20 +172,24 @@ typedef struct {
                               segments (default); N -> the long-row units run
                               concurrently with the segment kernel on N CTAs
                               (one per SM; measured slower on config 3) */
-  uint32_t split_edges;    /* 0 -> every row is one sequential fold (the
-                              reference's bits for every operator; default).
-                              N -> rows above the plan's long-row threshold
-                              are cut into chunks of ~N edges, folded like
-                              short rows and combined in chunk order: Max /
-                              Min and argmax keep the reference's bits, a
-                              Sum / Mean becomes a fixed-order sum of chunk
-                              sums: deterministic, with no more rounding
-                              error than the sequential fold, but NOT within
-                              the reference's 1e-5 of that fold on hub rows
-                              (measured 9e-4 on config 3's mean backward:
-                              the fp32 fold of a 10^5-edge row carries that
-                              much rounding itself).  Outside the parity
-                              contract; opt-in. */
+  uint32_t split_edges;    /* Rows above the plan's long-row threshold cut into
+                              chunks of edges, folded like short rows and
+                              combined in chunk order.  Max / Min are exact
+                              under any association and the strict compare
+                              keeps the first winner, so value and argmax
+                              stay the reference's bits; a Sum / Mean becomes
+                              a fixed-order sum of chunk sums: deterministic,
+                              the same order of rounding error as the
+                              sequential fold, but NOT within the reference's
+                              1e-5 of that fold on hub rows (measured 9e-4 on
+                              config 3's mean backward: the fp32 fold of a
+                              10^5-edge row carries that much rounding
+                              itself), i.e. outside the parity contract.
+                              0 -> automatic (default): Max / Min without a
+                              fused second sum in chunks of 512, every sum
+                              one sequential fold; 1 -> never split (every
+                              long row on the long-row kernel); N >= 16 ->
+                              split every reduction, sums included, at N */
 } gspmm_plan;
 
 /* ---- errors ---- */

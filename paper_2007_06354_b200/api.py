@@ -172,11 +172,13 @@ class Graph:
         4, <= 512), kernel=1 for the register kernel on every call (2: planned kernels with
         the segment kernel a programmatic dependent of the long-row kernel), long_ctas
         = N to run the long-row units concurrently with the segments on N
-        CTAs.  0 = the default of each.  Results never depend on the plan,
-        except under split_edges = N: long rows are folded as chunks of ~N
-        edges combined in chunk order (max / min / argmax unchanged; sums of
-        those rows deterministic, but up to ~1e-3 from the reference's
-        sequential fold, whose own rounding is that large: outside the parity
+        CTAs.  0 = the default of each.  split_edges: 0 = long rows of max /
+        min reductions are folded as chunks of 512 edges combined in chunk
+        order (exact: the reference's bits), sums stay sequential; 1 = never
+        split; N >= 16 = split every reduction at N.  Results never depend
+        on the plan, except the sums of long rows under split_edges >= 16
+        (deterministic, but up to ~1e-3 from the reference's sequential
+        fold, whose own rounding is that large: outside the parity
         contract)."""
         p = A.Plan(seg_cost, long_threshold, unit_cols, kernel, long_ctas, split_edges)
         check(A.LIB.gspmm_graph_set_plan(self.handle, C.byref(p)), "set_plan")

@@ -70,6 +70,7 @@ constexpr double kSrcBlockBytes = 48.0 * 1048576.0;
 // Long-row column units (k_long_rg): stream rate of one CTA on random rows
 // and the rate of one column's fp32 add chain (one dependent add per ~4
 // cycles at 1.965 GHz), the two bounds of a unit's time.
+constexpr uint32_t kSplitEdges = 512;  // default chunk of a long row's Max / Min fold
 constexpr double kUnitBytesPerS = 40.0e9;
 constexpr double kChainEdgesPerS = 490.0e6;
 
@@ -631,10 +632,10 @@ int long_units_for(gspmm_graph_s* g, int li, int W, const gspmm_graph_s::Units**
 }
 
 // Chunk view of plan level li's long rows (graph mutex held), built on first
-// use: every long row is cut into ceil(n / split_edges) balanced edge ranges.
-int chunks_for(gspmm_graph_s* g, int li, const gspmm_graph_s::Chunks** out) {
+// use: every long row is cut into ceil(n / edges) balanced edge ranges.
+int chunks_for(gspmm_graph_s* g, int li, uint32_t edges, const gspmm_graph_s::Chunks** out) {
   for (const auto& c : g->chunks)
-    if (c.level == li && c.edges == g->split_edges) {
+    if (c.level == li && c.edges == edges) {
       *out = &c;
       return GSPMM_OK;
     }
@@ -643,7 +644,7 @@ int chunks_for(gspmm_graph_s* g, int li, const gspmm_graph_s::Chunks** out) {
   std::vector<uint2> units, ranges;
   for (size_t i = 0; i < lv.long_rows.size(); ++i) {
     const uint64_t n = lv.long_deg[i];
-    const uint64_t nk = (n + g->split_edges - 1) / g->split_edges;
+    const uint64_t nk = (n + edges - 1) / edges;
     const uint32_t k0 = static_cast<uint32_t>(cptr.size());
     ranges.push_back(make_uint2(k0, static_cast<uint32_t>(nk)));
     for (uint64_t t = 0; t <= nk; ++t)  // t == nk: the row's end (start of the unused row)
@@ -653,7 +654,7 @@ int chunks_for(gspmm_graph_s* g, int li, const gspmm_graph_s::Chunks** out) {
   }
   gspmm_graph_s::Chunks c;
   c.level = li;
-  c.edges = g->split_edges;
+  c.edges = edges;
   c.rows = static_cast<uint32_t>(cptr.size());
   c.n_units = static_cast<uint32_t>(units.size());
   cptr.push_back(cptr.empty() ? 0u : cptr.back());  // rows + 1 entries
@@ -817,18 +818,27 @@ int launch(gspmm_graph_s* g, CallCtx* ctx, Bound& b, cudaStream_t s) {
     p.mode = 0;
     p.n_units = p.n_segs * p.seg_slices;
     p.counter = ctx->d_counter;
-    if (lv.num_long && g->split_edges && !b.L.acc_in && !b.L.epi &&
+    // Long rows split by EDGES: each chunk of a long row is folded like a
+    // short row by the segment kernel into a partial row, and a small kernel
+    // combines a row's partials in chunk order.  Max / Min are exact under
+    // any association and the strict comparison keeps the first winner, so
+    // for them (without a fused second sum) this is the DEFAULT path, the
+    // reference's bits at segment-kernel speed (cfg3 max + argmax 6.14 ->
+    // 5.22 ms, r04c).  Sums take it only under the plan option split_edges.
+    const bool exact_split = (b.L.reduce == R_MAX || b.L.reduce == R_MIN) && !b.L.out2;
+    const uint32_t split = g->split_edges == 1 ? 0u
+                           : g->split_edges  ? g->split_edges
+                           : exact_split     ? kSplitEdges
+                                             : 0u;
+    if (lv.num_long && split && !b.L.acc_in && !b.L.epi &&
         (b.L.reduce == R_SUM || b.L.reduce == R_MAX || b.L.reduce == R_MIN)) {
-      // Long rows split by EDGES (plan option split_edges): each chunk of a
-      // long row is folded like a short row by the segment kernel into a
-      // partial row, and a small kernel combines a row's partials in chunk
-      // order.  Max / Min and their argmax stay the reference's bits; a sum
+      // Max / Min and their argmax stay the reference's bits; a sum
       // becomes a fixed-order sum of chunk sums -- deterministic, closer to
       // the exact sum than the sequential fold, and for that reason up to
       // ~1e-3 (the reference's measure) away from the reference on 10^5-edge
       // rows: opt-in, outside the parity contract.
       const gspmm_graph_s::Chunks* ch = nullptr;
-      int st = chunks_for(g, li, &ch);
+      int st = chunks_for(g, li, split, &ch);
       if (st) return st;
       const int64_t pld = (W + 3) & ~3;
       const bool dual = b.L.out2 != nullptr;
@@ -1268,8 +1278,10 @@ int gspmm_graph_set_plan(gspmm_graph g, const gspmm_plan* plan) {
   if (!g) return fail(GSPMM_ERR_ARG, "null graph handle");
   const gspmm_plan dflt{};
   if (!plan) plan = &dflt;
-  if (plan->unit_cols % 4 || plan->unit_cols > 512 || plan->kernel < 0 || plan->kernel > 2)
-    return fail(GSPMM_ERR_ARG, "plan: unit_cols must be a multiple of 4 up to 512, kernel 0, 1 or 2");
+  if (plan->unit_cols % 4 || plan->unit_cols > 512 || plan->kernel < 0 || plan->kernel > 2 ||
+      (plan->split_edges > 1 && plan->split_edges < 16))
+    return fail(GSPMM_ERR_ARG, "plan: unit_cols must be a multiple of 4 up to 512, kernel 0, 1 or 2, "
+                               "split_edges 0, 1 or >= 16");
   std::lock_guard<std::recursive_mutex> lock(g->mu);
   CUDA_TRY(cudaSetDevice(g->device), "cudaSetDevice");
   // in-flight calls may still read the old plan

@@ -552,7 +552,8 @@ def test_long_rows_split_by_edges(edges):
 
 
 @pytest.mark.parametrize("cols", [0, 4, 8, 12, 32, 64, 128, 132, 256, 512])
-def test_long_row_column_units(cols):
+@pytest.mark.parametrize("split", [1, 0])  # 1: max on the long-row kernel; 0: max in edge chunks
+def test_long_row_column_units(cols, split):
     # long rows run as column units of `cols` columns (0: the automatic
     # widths); every unit width, argmax and scalar / per-head / per-neighbour
     # small operands included, stays bitwise for every feature width
@@ -563,7 +564,7 @@ def test_long_row_column_units(cols):
     dst = np.concatenate([np.zeros(40000, np.int64) + 5, rng.integers(0, n, 30000),
                           np.zeros(5000, np.int64) + 17]).astype(np.uint32)
     g = O.Graph(n, src, dst)
-    g.plan = dict(long_threshold=1000, unit_cols=cols)
+    g.plan = dict(long_threshold=1000, unit_cols=cols, split_edges=split)
     w = O.gcn_weights(n, src, dst)
     for dim in (4, 20, 100, 128, 256, 300, 512):
         x = O.normal_features(n, dim, dim)
@@ -756,13 +757,16 @@ def test_second_reduction_fused_and_fallback(long_):
 
 
 @pytest.mark.parametrize("cols", [0, 8, 28, 100])
-def test_long_row_argmax_ties_zeros_and_nans(cols):
+@pytest.mark.parametrize("split", [1, 0, 64])  # long-row kernel; default edge chunks; small chunks
+def test_long_row_argmax_ties_zeros_and_nans(cols, split):
     # The long-row units take each 16-edge block's extremum from an FMNMX
     # tree and resolve the winner at the flush: the first-canonical-position
     # rule, the sign of a zero extremum (the reference's `a < m ? m : a`
     # keeps the EARLIER of -0 / +0), NaN never winning, and rows whose every
     # value is NaN or -inf must all come out bit for bit, max and min, with
-    # and without the fused mean.
+    # and without the fused mean.  The same holds for the default path of a
+    # plain max / min, long rows folded as chunks of edges and combined in
+    # chunk order (split 0 and 64; the fused mean keeps the long-row kernel).
     rng = np.random.default_rng(91 + cols)
     n = 2000
     src = np.concatenate([rng.integers(0, n, 20000), rng.integers(0, n, 20000),
@@ -771,7 +775,7 @@ def test_long_row_argmax_ties_zeros_and_nans(cols):
                           np.zeros(3000, np.int64) + 11,
                           np.zeros(1500, np.int64) + 29]).astype(np.uint32)
     g = O.Graph(n, src, dst)
-    g.plan = dict(long_threshold=1000, unit_cols=cols)
+    g.plan = dict(long_threshold=1000, unit_cols=cols, split_edges=split)
     for dim in (8, 36, 100, 260):
         # few distinct values: -1, -0.0, +0.0, 0.5, NaN; column 1 only zeros
         # of both signs, column 2 only NaN, column 3 only -inf, column 4
@@ -797,6 +801,9 @@ def test_long_row_argmax_ties_zeros_and_nans(cols):
                 assert (picked.view(np.uint32)[won] == val.view(np.uint32)[won]).all()
             # plain extremum (no argmax) and the fused second reduction
             assert gpu_reduce(g, cfg, u=x).tobytes() == want.tobytes()
+        if split > 1:  # sums of split rows are not the reference's bits
+            g.__dict__.pop("_dev", None)
+            continue
         xz = np.nan_to_num(x, nan=0.25, neginf=-2.0)  # finite values for the mean
         o2 = torch.empty((n, dim), device="cuda")
         h = dev_graph(g, O.DST_MAJOR)
