@@ -122,6 +122,16 @@ def test_cfg3_whole_output(cfg3):
     mean = P.binary_reduce(hd, (P.U, P.NONE, P.COPY, P.MEAN, P.V), u=xd).cpu().numpy()
     mx, au, ae = P.binary_reduce(hd, "u_copy_max_v", u=xd, want_arg_other=True,
                                  want_arg_edge=True)
+    # the bench step's forward: max + argmax with the mean as a fused second
+    # output (hub rows on the long-row kernel) against the separate calls
+    # (a plain max folds hub rows as edge chunks): the same bits
+    o2 = torch.empty((n, F), device="cuda")
+    fused = P.binary_reduce(hd, "u_copy_max_v", u=xd, out2=o2, reduce2=P.MEAN,
+                            want_arg_other=True)
+    assert torch.equal(fused[0].view(torch.int32), mx.view(torch.int32))
+    assert torch.equal(fused[1], au)
+    assert np.array_equal(o2.cpu().numpy().view(np.uint32), mean.view(np.uint32))
+    del fused, o2
     gmean = P.binary_reduce(hs, (P.V, P.NONE, P.COPY, P.SUM, P.U), v=gyd,
                             other_scale=torch.from_numpy(inv).cuda()).cpu().numpy()
     gmax = P.argmax_backward(au, gyd, n).cpu().numpy()
