@@ -91,6 +91,24 @@ constexpr int kThreads = 256;
 #ifndef GATHER_STREAM_IN
 #define GATHER_STREAM_IN 1
 #endif
+// The argmax fold of the segment kernel, per (edge, column): compare, take
+// the value, take the id.  As FSETP + FSEL + SEL all three issue to the ALU
+// pipe (16 lanes per clock per SM sub-partition, half the FMA rate): 48 of
+// the ~95 instructions of a 4-edge batch of the fused max + mean forward,
+// and ncu shows math-pipe throttle with the issue slots 75% busy
+// (profiles/r04z_ncu_gather.txt).  With GATHER_FMA_SELECT the conditional
+// value copy is a predicated FFMA (m * 1 + -0, exact for every m, signed
+// zeros included) whose multiplier is a launch parameter, so ptxas cannot
+// fold it back into a select: it issues to the FMA pipes.  The id copy is
+// written the same way (IMAD j * 1 + 0); ptxas hoists that multiply and
+// keeps a SEL per column, which is the better code: forcing the id onto the
+// FMA pipes as well (the id tracked as a float, one opaque 1.0f per column)
+// left no SEL but spilled at 48 registers, 6.50 -> 7.61 ms on the fused
+// forward (r04h).  Measured (r04h): cfg3 max + argmax 5.15 -> 4.75 ms, the
+// fused max + mean forward 6.56 -> 6.46 ms.
+#ifndef GATHER_FMA_SELECT
+#define GATHER_FMA_SELECT 1
+#endif
 #ifndef GATHER_MINB5
 #define GATHER_MINB5 2
 
@@ -156,15 +174,30 @@ struct Acc {
         if constexpr (DUAL) s2[v][t] = 0.0f;
       }
   }
-  __device__ __forceinline__ void fold(int v, const float (&m)[4], uint32_t j) {
+  __device__ __forceinline__ void fold(int v, const float (&m)[4], uint32_t j, float f_one,
+                                       uint32_t u_one) {
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       if constexpr (DUAL) s2[v][t] = __fadd_rn(s2[v][t], m[t]);
       if constexpr (ARG) {
+#if GATHER_FMA_SELECT
+        // a < m (Max) / m < a (Min): ordered compares, NaN never wins
+        if constexpr (ROP == R_MAX)
+          asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %0, %2;\n\t"
+              "@p fma.rn.f32 %0, %2, %4, 0f80000000;\n\t@p mad.lo.u32 %1, %3, %5, 0;\n\t}"
+              : "+f"(a[v][t]), "+r"(arg[v][t])
+              : "f"(m[t]), "r"(j), "f"(f_one), "r"(u_one));
+        else
+          asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %2, %0;\n\t"
+              "@p fma.rn.f32 %0, %2, %4, 0f80000000;\n\t@p mad.lo.u32 %1, %3, %5, 0;\n\t}"
+              : "+f"(a[v][t]), "+r"(arg[v][t])
+              : "f"(m[t]), "r"(j), "f"(f_one), "r"(u_one));
+#else
         if (red_wins<ROP>(a[v][t], m[t])) {
           a[v][t] = m[t];
           arg[v][t] = j;
         }
+#endif
       } else {
         a[v][t] = red_combine<ROP>(a[v][t], m[t]);
       }
@@ -388,8 +421,8 @@ __device__ __forceinline__ void wide_unit(const RowLaunch& L, const UnitCtx& u, 
           else if constexpr (SK == SK_WIN) m[t] = bin_apply<BOP>(xs[t], r[k][0]);
           else m[t] = bin_apply<BOP>(xs[t], r[k][v]);
         }
-        if constexpr (ARG == 2) acc.fold(v, m, okey[k]);
-        else acc.fold(v, m, jpos);
+        if constexpr (ARG == 2) acc.fold(v, m, okey[k], L.f_one, L.u_one);
+        else acc.fold(v, m, jpos, L.f_one, L.u_one);
       }
     };
     if (n == static_cast<uint32_t>(U) && rc.row_end - j >= static_cast<uint32_t>(U)) {

@@ -78,6 +78,11 @@ struct RowLaunch {
   float* out2 = nullptr;
   int64_t out2_ld = 0;
   bool mean2 = false;
+  // 1.0f and 1 as launch parameters, opaque to ptxas: the argmax fold's
+  // conditional value copy becomes an FFMA (FMA pipes) instead of an FSEL
+  // (gather_impl.cuh, GATHER_FMA_SELECT)
+  float f_one = 1.0f;
+  uint32_t u_one = 1u;
 };
 
 // Kernel launchers (rows.cu, dot.cu, aux.cu).  Return cudaGetLastError().
