@@ -32,6 +32,20 @@ def test_abi_version():
     assert A.LIB.gspmm_abi_version() == 3
 
 
+def test_plan_struct_mirrors_the_header():
+    # gspmm_plan (include/gspmm_b200.h): the ctypes mirror has the header's
+    # fields in the header's order (six 32-bit words)
+    import ctypes
+    import re
+    hdr = open(os.path.join(ROOT, "include", "gspmm_b200.h")).read()
+    body = hdr[:hdr.index("} gspmm_plan;")]
+    body = body[body.rindex("typedef struct {"):]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"(?:uint32_t|int32_t)\s+(\w+)\s*;", body)
+    assert fields == [f[0] for f in A.Plan._fields_]
+    assert ctypes.sizeof(A.Plan) == 4 * len(fields) == 24
+
+
 def test_library_path_is_in_tree():
     assert os.path.commonpath([P.LIB_PATH, ROOT]) == ROOT
 
