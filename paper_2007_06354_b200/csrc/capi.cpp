@@ -833,10 +833,11 @@ int launch(gspmm_graph_s* g, CallCtx* ctx, Bound& b, cudaStream_t s) {
     if (lv.num_long && split && !b.L.acc_in && !b.L.epi &&
         (b.L.reduce == R_SUM || b.L.reduce == R_MAX || b.L.reduce == R_MIN)) {
       // Max / Min and their argmax stay the reference's bits; a sum
-      // becomes a fixed-order sum of chunk sums -- deterministic, closer to
-      // the exact sum than the sequential fold, and for that reason up to
-      // ~1e-3 (the reference's measure) away from the reference on 10^5-edge
-      // rows: opt-in, outside the parity contract.
+      // becomes a fixed-order sum of chunk sums -- deterministic, another
+      // fp32 order with the same kind of rounding error as the sequential
+      // fold, and for that reason up to ~1e-3 (the reference's measure) away
+      // from the reference on 10^5-edge rows: opt-in, outside the parity
+      // contract.
       const gspmm_graph_s::Chunks* ch = nullptr;
       int st = chunks_for(g, li, split, &ch);
       if (st) return st;
