@@ -607,7 +607,11 @@ int long_units_for(gspmm_graph_s* g, int li, int W, const gspmm_graph_s::Units**
     sw = (((Wp + ns - 1) / ns) + 3) & ~3;  // balanced slices
     for (int c0 = 0; c0 < W; c0 += sw) {
       const int cw = std::min(sw, W - c0);
-      const double t = std::max(n * cw * 4.0 / kUnitBytesPerS, n / kChainEdgesPerS);
+      // hand-out order: the measured time of a unit (unit traces of r03c,
+      // every width within 10%): 2.5 ns per edge plus 0.115 ns per edge and
+      // column; the max() model above ranks 28-column units of 100k-edge
+      // rows below whole 100-column rows of 30k edges, which take less time
+      const double t = n * (2.5e-9 + 0.115e-9 * cw);
       us.push_back({lv.long_rows[i], static_cast<uint32_t>(c0), static_cast<uint32_t>(cw), t});
     }
   }
