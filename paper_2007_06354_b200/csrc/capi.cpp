@@ -1433,7 +1433,13 @@ static int softmax_common(gspmm_graph g, bool backward, const gspmm_mat* l, cons
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CallCtx* ctx = nullptr;
   if ((st = context_for(g, s, &ctx))) return st;
-  const auto& lv = g->level[0];
+  // Hub rows (one CTA each, side stream): above 4096 edges.  With the
+  // warp-per-row kernel's rows handed out from a counter, a 4096-edge row is
+  // no longer a tail, and a 1024-thread CTA on a 1500-edge row mostly waits
+  // at its barriers: cfg4 forward 1.21 ms at 1024, 0.96 at 4096, 0.99 at
+  // 8192, 1.82 at 16384 (r04s).  (The forward was 1.63 ms with the rows
+  // strided statically over the grid, r04j / r04r.)
+  const auto& lv = g->level[g->n_levels > 1 ? 1 : 0];
   if (lv.num_long && !ctx->side) {
     CUDA_TRY(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "side stream");
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming), "event");
@@ -1448,7 +1454,8 @@ static int softmax_common(gspmm_graph g, bool backward, const gspmm_mat* l, cons
       backward, g->d_indptr, g->d_eids, g->num_rows, static_cast<int>(heads),
       l->edge_order == GSPMM_EDGE_BY_POS, l->data, l->ld ? l->ld : heads,
       backward ? ga->data : nullptr, backward ? (ga->ld ? ga->ld : heads) : 0, out->data,
-      out->ld ? out->ld : heads, lv.d_long, lv.num_long, lv.threshold, g->num_sms, s, side);
+      out->ld ? out->ld : heads, lv.d_long, lv.num_long, lv.threshold, g->num_sms, s, side,
+      ctx->d_counter + 2);
   st = end_call(ctx, s);
   if (e != cudaSuccess) return cuda_fail(e, "edge_softmax");
   return st;

@@ -113,13 +113,16 @@ struct SideStream {
 
 // Fused edge softmax over in-edges (softmax.cu): forward (l -> out = a) or
 // backward (l = a, g = grad_a -> out = grad_l).  Rows above long_threshold
-// edges are listed in long_rows and run one CTA per row.
+// edges are listed in long_rows and run one CTA per row.  counter: one
+// uint32 of the call's context (the warp-per-row kernel hands rows out in
+// groups from it); nullptr = rows strided over the grid.
 cudaError_t launch_edge_softmax(bool backward, const uint32_t* indptr, const uint32_t* eids,
                                 uint32_t rows, int heads, bool by_pos, const float* l,
                                 int64_t l_ld, const float* g, int64_t g_ld, float* out,
                                 int64_t out_ld, const uint32_t* long_rows, uint32_t n_long,
                                 uint32_t long_threshold, int num_sms, cudaStream_t s,
-                                const SideStream& side = SideStream{});
+                                const SideStream& side = SideStream{},
+                                uint32_t* counter = nullptr);
 
 // Device-side canonical CSR build / transpose (build.cu).
 cudaError_t launch_build_csr(uint32_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,

@@ -40,6 +40,7 @@ struct SoftmaxArgs {
   float* out;      // forward: a; backward: grad_l
   int64_t out_ld;
   uint32_t long_threshold;  // rows above this many edges run on k_softmax_long
+  uint32_t* counter;        // zeroed per launch: rows are handed out in groups (nullptr: strided)
 };
 
 __device__ __forceinline__ float max_ref(float a, float x) { return a < x ? x : a; }
@@ -350,9 +351,30 @@ __device__ __forceinline__ void row_softmax_vec(const SoftmaxArgs& p, uint32_t r
   }
 }
 
+// Rows are handed out in groups of kSmGrab from a counter.  With the rows
+// strided statically over the persistent grid, the warp whose rows happened
+// to be heavy ran twice as long as the average one: 33% warps active over
+// the kernel (profiles/r04j_ncu_softmax.txt).
+constexpr uint32_t kSmGrab = 4;
+
 template <int H, bool BWD>
 __global__ void __launch_bounds__(kSmWarps * 32) k_softmax_vec_rows(const SoftmaxArgs p, bool vec) {
-  const int warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p.counter) {
+    for (;;) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(p.counter, kSmGrab);
+      base = __shfl_sync(kFull, base, 0);
+      if (base >= p.rows) break;
+      const uint32_t end = min(base + kSmGrab, p.rows);
+      for (uint32_t r = base; r < end; ++r) {
+        const uint32_t deg = __ldg(p.indptr + r + 1) - __ldg(p.indptr + r);
+        if (deg > p.long_threshold) continue;
+        row_softmax_vec<H, BWD, 1>(p, r, 0, nullptr, vec);
+      }
+    }
+    return;
+  }
   const uint32_t stride = gridDim.x * kSmWarps;
   for (uint32_t r = blockIdx.x * kSmWarps + warp; r < p.rows; r += stride) {
     const uint32_t deg = __ldg(p.indptr + r + 1) - __ldg(p.indptr + r);
@@ -405,6 +427,7 @@ void launch_vec(const SoftmaxArgs& p, bool vec, const uint32_t* long_rows, uint3
   if (p.rows) {
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
         (p.rows + kSmWarps - 1) / kSmWarps, static_cast<uint64_t>(sms) * occ_rows));
+    if (p.counter) cudaMemsetAsync(p.counter, 0, sizeof(uint32_t), s);
     k_softmax_vec_rows<H, BWD><<<grid, kSmWarps * 32, 0, s>>>(p, vec);
     note_launch();
   }
@@ -434,9 +457,9 @@ cudaError_t launch_edge_softmax(bool backward, const uint32_t* indptr, const uin
                                 int64_t l_ld, const float* g, int64_t g_ld, float* out,
                                 int64_t out_ld, const uint32_t* long_rows, uint32_t n_long,
                                 uint32_t long_threshold, int num_sms, cudaStream_t s,
-                                const SideStream& side) {
+                                const SideStream& side, uint32_t* counter) {
   SoftmaxArgs p{indptr, eids, rows, heads, by_pos, l, l_ld, g, g_ld, out, out_ld,
-                n_long ? long_threshold : 0xffffffffu};
+                n_long ? long_threshold : 0xffffffffu, counter};
   const int sms = num_sms > 0 ? num_sms : 148;
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
   const bool vec = heads % 4 == 0 && l_ld % 4 == 0 && out_ld % 4 == 0 && al16(l) && al16(out) &&
