@@ -329,6 +329,7 @@ __device__ __forceinline__ void row_softmax_vec(const SoftmaxArgs& p, uint32_t r
     float sacc[H];
 #pragma unroll
     for (int h = 0; h < H; ++h) sacc[h] = 0.0f;
+#pragma unroll 4
     for (uint32_t k = first; k < n; k += step) {
       const int64_t er = erow(k);
       float a[H], g[H];
@@ -339,6 +340,7 @@ __device__ __forceinline__ void row_softmax_vec(const SoftmaxArgs& p, uint32_t r
     }
     lane_reduce<H, false>(sacc);
     warps_reduce<H, false>(sacc, w, nw, red);
+#pragma unroll 2
     for (uint32_t k = first; k < n; k += step) {
       const int64_t er = erow(k);
       float a[H], g[H];
